@@ -1,0 +1,397 @@
+"""Integer oracle of LobRA's per-step dispatch -- TEST INFRASTRUCTURE ONLY.
+
+Follows the paper's algorithm step by step (DESIGN.md readings
+Q11-Q20).  Every quantity is an integer; there is no floating point anywhere except
+inside the HiGHS MILP library call, whose answers are re-verified in exact integers.
+
+Steps (``dispatch`` below):
+ 1. histogram on the grid u_k = k*grid_step: length l falls in interval k with
+    u_{k-1} < l <= u_k  ("equal-length division {256, 512, ...}")
+ 2. drop empty intervals (P:619 footnote "ignore empty intervals")
+ 3. dynamic bucketing DP, the literal recurrence of P:601-617:
+      State_{0,j} = 0, State_{i,0} = +inf,
+      State_{i+1,j+1} = min_{i' in [0,i]} State_{i',j}
+                         + sum_{i''=i'+1}^{i} |I_{i''}| (u_{i+1} - u_{i''})
+    then the lexicographically smallest optimal boundary list (reading Q17)
+ 4. r_i = #{j : s_j <= M_i}  (Table tab:notations P:316-334 "r_i")
+ 5. Eq. 3: min_d max_i sum_j c_ij * ceil(d_ij / p_i)
+      s.t. sum_i d_ij = B_j,  0 <= d_ij <= B_j p_i,  d_ij = 0 for j > r_i
+    with the per-sequence cost of App. D (linear in d), costs
+    being the caller's integers (reading Q15).  Solved by brute force on small
+    instances, else by HiGHS (scipy.optimize.milp) with exact integer re-checks.
+ 6. canonical tie-break: the lexicographically smallest optimal d in (group, bucket)
+    order (reading Q12), by fixing variables one at a time at their minimum
+ 7. bucket j's sequences in ascending original index: first d_1j to group 1, ...
+ 8. within a group, per bucket, strict round-robin starting at the replica with the
+    smallest running assigned cost (ties: lowest index) -> per-replica count in
+    {floor(d/p), ceil(d/p)} (P:576 objective "ceil(d_ij/p_i)"; reading Q14)
+ 9. chunks of b_j = floor(M_i / s_j) sequences plus one remainder chunk per bucket
+    (App. D), ordered by descending chunk cost, ties by bucket then
+    chunk index (App. D "sorting micro-batches in descending order of time cost")
+10. inside a chunk, sequences ordered by (task id, original index) -- packing order
+    grouped by task (reading Q6).
+"""
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+
+import numpy as np
+
+INF = float("inf")
+
+
+class DispatchError(Exception):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code          # 1 = input, 2 = infeasible (S:589 exit codes)
+
+
+@dataclass
+class Group:
+    tp: int            # n_i: GPUs per replica
+    replicas: int      # p_i
+    max_tokens: int    # M_i
+
+
+@dataclass
+class DispatchResult:
+    boundaries: list
+    d: np.ndarray                  # [G, R] int64 (R = len(boundaries))
+    seq_bucket: np.ndarray         # [n] 0-based bucket of every sequence
+    seq_replica: np.ndarray        # [n] global replica id
+    seq_chunk: np.ndarray          # [n] chunk index within its replica (execution order)
+    pack_order: np.ndarray         # [n] position within its chunk
+    replica_cost: np.ndarray       # [sum p] int64
+    t_hat: int
+    r: list = field(default_factory=list)
+
+
+# --------------------------------------------------------------------------- 1-3
+def histogram(lengths, grid_step: int, grid_max: int) -> np.ndarray:
+    """counts[k-1] = #{l : u_{k-1} < l <= u_k}, u_k = k*grid_step."""
+    U = grid_max // grid_step
+    counts = np.zeros(U, dtype=np.int64)
+    for l in np.asarray(lengths).tolist():
+        if l < 1:
+            raise DispatchError(1, f"sequence length {l} < 1")
+        if l > grid_max:
+            raise DispatchError(2, f"sequence length {l} exceeds grid maximum {grid_max}")
+        k = -(-l // grid_step)      # ceil
+        counts[k - 1] += 1
+    return counts
+
+
+def dp_state(u, cnt, R):
+    """Literal P:601-617 recurrence over the (compressed) intervals.
+    u[i], cnt[i] for i = 1..V (index 0 unused).  Returns the State table."""
+    V = len(u) - 1
+    S = [[INF] * (R + 1) for _ in range(V + 1)]
+    for j in range(R + 1):
+        S[0][j] = 0
+    for i in range(0, V):          # computes State_{i+1, j+1}
+        for j in range(0, R):
+            best = INF
+            for ip in range(0, i + 1):
+                if S[ip][j] == INF:
+                    continue
+                pad = 0
+                for ipp in range(ip + 1, i + 1):
+                    pad += cnt[ipp] * (u[i + 1] - u[ipp])
+                best = min(best, S[ip][j] + pad)
+            S[i + 1][j + 1] = best
+    return S
+
+
+def dynamic_buckets(counts, grid_step: int, R: int):
+    """Returns (boundaries, cross-interval padding) -- lexicographically smallest
+    optimal boundary list (reading Q17)."""
+    if R < 1:
+        raise DispatchError(1, "R must be >= 1")
+    occ = [k + 1 for k in range(len(counts)) if counts[k] > 0]       # 1-based grid idx
+    if not occ:
+        raise DispatchError(1, "empty batch")
+    u = [0] + [k * grid_step for k in occ]
+    cnt = [0] + [int(counts[k - 1]) for k in occ]
+    V = len(occ)
+    S = dp_state(u, cnt, R)
+    opt = S[V][R]
+
+    def seg_cost(a, b):   # intervals a..b (1-based, inclusive) padded to u[b]
+        return sum(cnt[v] * (u[b] - u[v]) for v in range(a, b + 1))
+
+    # suffix DP: G[b][j] = min padding for intervals b+1..V using <= j buckets
+    G = [[INF] * (R + 1) for _ in range(V + 1)]
+    for j in range(R + 1):
+        G[V][j] = 0
+    for b in range(V - 1, -1, -1):
+        for j in range(1, R + 1):
+            G[b][j] = min(seg_cost(b + 1, e) + G[e][j - 1] for e in range(b + 1, V + 1))
+    assert G[0][R] == opt, (G[0][R], opt)
+    bounds, b, j = [], 0, R
+    while b < V:
+        for e in range(b + 1, V + 1):          # smallest next boundary first
+            if seg_cost(b + 1, e) + G[e][j - 1] == G[b][j]:
+                bounds.append(u[e])
+                b, j = e, j - 1
+                break
+    return bounds, int(opt)
+
+
+def padding_cost(lengths, boundaries) -> int:
+    """sum over sequences of (smallest boundary >= l) - l."""
+    tot = 0
+    for l in np.asarray(lengths).tolist():
+        cands = [s for s in boundaries if s >= l]
+        if not cands:
+            raise DispatchError(2, "sequence beyond last boundary")
+        tot += min(cands) - l
+    return tot
+
+
+# --------------------------------------------------------------------------- 5-6
+def group_time(c_row, q_row) -> int:
+    return int(sum(int(c) * int(q) for c, q in zip(c_row, q_row)))
+
+
+def objective(d, p, c) -> int:
+    """t_hat = max_i sum_j c_ij ceil(d_ij / p_i)   (Eq. 3 objective)."""
+    G, R = d.shape
+    best = 0
+    for i in range(G):
+        tot = 0
+        for j in range(R):
+            if d[i, j]:
+                tot += int(c[i][j]) * (-(-int(d[i, j]) // int(p[i])))
+        best = max(best, tot)
+    return best
+
+
+def check_eq3(d, Bj, p, r) -> None:
+    """All constraints of Eq. 3 plus d_ij = 0 beyond r_i."""
+    G, R = d.shape
+    for j in range(R):
+        assert int(d[:, j].sum()) == int(Bj[j]), "coverage"
+        for i in range(G):
+            assert d[i, j] >= 0
+            assert d[i, j] <= Bj[j] * p[i], "d_ij <= B_j p_i"
+            if j >= r[i]:
+                assert d[i, j] == 0, "unsupported bucket"
+
+
+def _splits(total, k):
+    """All compositions of `total` into k non-negative parts, in lexicographic order."""
+    if k == 1:
+        yield (total,)
+        return
+    for a in range(total + 1):
+        for rest in _splits(total - a, k - 1):
+            yield (a,) + rest
+
+
+def solve_bruteforce(Bj, p, c, r, cap=10**7):
+    """Exhaustive Eq. 3: the lexicographically smallest optimal d."""
+    G, R = len(p), len(Bj)
+    per_bucket = []
+    space = 1
+    for j in range(R):
+        sup = [i for i in range(G) if j < r[i]]
+        if Bj[j] > 0 and not sup:
+            raise DispatchError(2, f"bucket {j} unsupported: re-plan required")
+        opts = []
+        for comp in _splits(int(Bj[j]), max(len(sup), 1)):
+            col = [0] * G
+            for i, v in zip(sup, comp):
+                col[i] = v
+            opts.append(col)
+        per_bucket.append(opts)
+        space *= len(opts)
+        if space > cap:
+            raise ValueError("instance too large for brute force")
+    best_val, best_vec = None, None
+    for combo in itertools.product(*per_bucket):
+        d = np.array(combo, dtype=np.int64).T           # [G, R]
+        val = objective(d, p, c)
+        vec = tuple(d.reshape(-1).tolist())
+        if best_val is None or val < best_val or (val == best_val and vec < best_vec):
+            best_val, best_vec = val, vec
+    return np.array(best_vec, dtype=np.int64).reshape(G, R), int(best_val)
+
+
+def _milp(Bj, p, c, r, t_cap=None, fixed=None, minimize_var=None):
+    """HiGHS MILP on Eq. 3 with ceil linearised by q_ij >= d_ij / p_i (integer q).
+    Variables: d_ij (G*R), q_ij (G*R), t.  Returns (d, q, t) or None if infeasible."""
+    from scipy.optimize import LinearConstraint, Bounds, milp
+    G, R = len(p), len(Bj)
+    nv = 2 * G * R + 1
+    D = lambda i, j: i * R + j
+    Q = lambda i, j: G * R + i * R + j
+    TT = 2 * G * R
+    rows, lo, hi = [], [], []
+    for j in range(R):                       # coverage
+        a = np.zeros(nv); [a.__setitem__(D(i, j), 1) for i in range(G)]
+        rows.append(a); lo.append(Bj[j]); hi.append(Bj[j])
+    for i in range(G):
+        for j in range(R):                   # p_i q_ij - d_ij >= 0
+            a = np.zeros(nv); a[Q(i, j)] = p[i]; a[D(i, j)] = -1
+            rows.append(a); lo.append(0); hi.append(np.inf)
+        a = np.zeros(nv)                     # sum_j c_ij q_ij - t <= 0
+        for j in range(R):
+            a[Q(i, j)] = c[i][j]
+        a[TT] = -1
+        rows.append(a); lo.append(-np.inf); hi.append(0)
+    lb = np.zeros(nv); ub = np.full(nv, np.inf)
+    for i in range(G):
+        for j in range(R):
+            ub[D(i, j)] = Bj[j] * p[i] if j < r[i] else 0
+            ub[Q(i, j)] = Bj[j] if j < r[i] else 0
+    if t_cap is not None:
+        ub[TT] = t_cap
+    if fixed:
+        for (i, j), v in fixed.items():
+            lb[D(i, j)] = ub[D(i, j)] = v
+    obj = np.zeros(nv)
+    if minimize_var is None:
+        obj[TT] = 1
+    else:
+        obj[D(*minimize_var)] = 1
+    integrality = np.ones(nv)
+    res = milp(obj, constraints=LinearConstraint(np.array(rows), lo, hi),
+               bounds=Bounds(lb, ub), integrality=integrality,
+               options={"mip_rel_gap": 0, "presolve": True})
+    if res.x is None:
+        return None
+    x = np.rint(res.x).astype(np.int64)
+    d = x[:G * R].reshape(G, R)
+    return d
+
+
+def solve_milp(Bj, p, c, r):
+    """t_hat* by HiGHS, then the lexicographically smallest d with objective <= t_hat*
+    by fixing d_ij to its minimum one variable at a time (reading Q12)."""
+    G, R = len(p), len(Bj)
+    d0 = _milp(Bj, p, c, r)
+    if d0 is None:
+        raise DispatchError(2, "Eq. 3 infeasible")
+    t_star = objective(d0, p, c)
+    fixed = {}
+    for i in range(G):
+        for j in range(R):
+            dm = _milp(Bj, p, c, r, t_cap=t_star, fixed=fixed, minimize_var=(i, j))
+            assert dm is not None
+            fixed[(i, j)] = int(dm[i, j])
+    d = np.zeros((G, R), dtype=np.int64)
+    for (i, j), v in fixed.items():
+        d[i, j] = v
+    check_eq3(d, Bj, p, r)
+    assert objective(d, p, c) == t_star
+    return d, t_star
+
+
+def solve_eq3(Bj, p, c, r, bruteforce_cap=200000):
+    try:
+        return solve_bruteforce(Bj, p, c, r, cap=bruteforce_cap)
+    except ValueError:
+        return solve_milp(Bj, p, c, r)
+
+
+# --------------------------------------------------------------------------- all
+def dispatch(groups, cost, seq_lens, seq_task, grid_step, grid_max, R, mode=0,
+             bruteforce_cap=200000) -> DispatchResult:
+    """The full per-step dispatch (steps 1-10 of the module docstring).
+
+    groups: list[Group] in (tp asc, M asc) order; cost: [G][U] ints, the cost of one
+    sequence padded to grid value u_k = (k+1)*grid_step.  mode 0 = balanced (Eq. 3),
+    mode 1 = length-based (Fig. 4(c): each bucket to the supporting group with the
+    smallest per-sequence GPU cost c_ij * n_i, ties to the earlier group)."""
+    seq_lens = np.asarray(seq_lens, dtype=np.int64)
+    seq_task = np.asarray(seq_task, dtype=np.int64)
+    n = len(seq_lens)
+    if n == 0:
+        raise DispatchError(1, "empty batch")
+    for a, b in zip(groups, groups[1:]):
+        if (a.tp, a.max_tokens) > (b.tp, b.max_tokens):
+            raise DispatchError(1, "groups must be ordered by (tp, max_tokens)")
+    counts = histogram(seq_lens, grid_step, grid_max)
+    bounds, _ = dynamic_buckets(counts, grid_step, R)
+    Rb = len(bounds)
+    seq_bucket = np.array([min(j for j in range(Rb) if bounds[j] >= l) for l in seq_lens.tolist()])
+    Bj = np.array([int((seq_bucket == j).sum()) for j in range(Rb)], dtype=np.int64)
+    # deployed groups only (p_i = 0 means not selected, Eq. 1 second constraint)
+    G = len(groups)
+    p = [g.replicas for g in groups]
+    r = [sum(1 for s in bounds if s <= g.max_tokens) if g.replicas > 0 else 0 for g in groups]
+    c = [[int(cost[i][s // grid_step - 1]) for s in bounds] for i in range(G)]
+    for j in range(Rb):
+        if Bj[j] > 0 and not any(j < r[i] for i in range(G)):
+            raise DispatchError(2, f"bucket {bounds[j]} unsupported: re-plan required")
+    live = [i for i in range(G) if p[i] > 0]
+    d = np.zeros((G, Rb), dtype=np.int64)
+    if mode == 0:
+        dl, _ = solve_eq3(Bj, [p[i] for i in live], [c[i] for i in live], [r[i] for i in live],
+                          bruteforce_cap)
+        for k, i in enumerate(live):
+            d[i] = dl[k]
+    elif mode == 1:
+        for j in range(Rb):
+            best = min((c[i][j] * groups[i].tp, i) for i in live if j < r[i])
+            d[best[1], j] = Bj[j]
+    else:
+        raise DispatchError(1, f"unknown mode {mode}")
+    check_eq3(d, Bj, p, r)
+    t_hat = objective(d, [max(x, 1) for x in p], c)
+
+    # 7. sequences of bucket j in ascending original index -> groups in order
+    seq_group = np.full(n, -1, dtype=np.int64)
+    for j in range(Rb):
+        idx = [k for k in range(n) if seq_bucket[k] == j]
+        pos = 0
+        for i in range(G):
+            for k in idx[pos:pos + d[i, j]]:
+                seq_group[k] = i
+            pos += int(d[i, j])
+    # 8. round-robin within a group
+    rbase = np.concatenate([[0], np.cumsum(p)]).astype(np.int64)
+    seq_replica = np.full(n, -1, dtype=np.int64)
+    running = [0] * int(rbase[-1])
+    for i in range(G):
+        for j in range(Rb):
+            idx = [k for k in range(n) if seq_bucket[k] == j and seq_group[k] == i]
+            if not idx:
+                continue
+            reps = list(range(rbase[i], rbase[i + 1]))
+            start = min(range(p[i]), key=lambda q: (running[reps[q]], q))
+            for m, k in enumerate(idx):
+                rep = reps[(start + m) % p[i]]
+                seq_replica[k] = rep
+                running[rep] += c[i][j]
+    # 9-10. chunks and packing order
+    seq_chunk = np.full(n, -1, dtype=np.int64)
+    pack_order = np.full(n, -1, dtype=np.int64)
+    for i in range(G):
+        for rep in range(rbase[i], rbase[i + 1]):
+            chunks = []   # (-cost, bucket, idx_in_bucket, [seqs])
+            for j in range(Rb):
+                idx = [k for k in range(n) if seq_replica[k] == rep and seq_bucket[k] == j]
+                if not idx:
+                    continue
+                b = groups[i].max_tokens // bounds[j]
+                assert b >= 1
+                for ci, s0 in enumerate(range(0, len(idx), b)):
+                    part = idx[s0:s0 + b]
+                    assert len(part) * bounds[j] <= groups[i].max_tokens
+                    chunks.append((-len(part) * c[i][j], j, ci, part))
+            chunks.sort(key=lambda x: (x[0], x[1], x[2]))
+            for cix, ch in enumerate(chunks):
+                order = sorted(ch[3], key=lambda k: (int(seq_task[k]), k))
+                for pos, k in enumerate(order):
+                    seq_chunk[k] = cix
+                    pack_order[k] = pos
+    replica_cost = np.array(running, dtype=np.int64)
+    # every sequence lands on a replica whose limit covers its padded length
+    for k in range(n):
+        i = int(np.searchsorted(rbase, seq_replica[k], side="right") - 1)
+        assert bounds[seq_bucket[k]] <= groups[i].max_tokens
+        assert seq_lens[k] <= groups[i].max_tokens
+    return DispatchResult(bounds, d, seq_bucket, seq_replica, seq_chunk, pack_order,
+                          replica_cost, int(t_hat), r)
