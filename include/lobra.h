@@ -1,0 +1,242 @@
+/*
+ * lobra.h -- C ABI of the B200-native LobRA multi-LoRA hot path.
+ *
+ * Paper: "LobRA: Multi-tenant Fine-tuning over Heterogeneous Data" (arXiv 2509.01193),
+ * /root/reference/PAPER.md, cited as P:<line> with its section / equation.
+ *
+ * The library computes, for a packed batch of variable-length sequences of many
+ * fine-tuning tasks ("fuse the input data from different tasks so that the
+ * computation of the base model can be fused into a batched operation whilst the
+ * computation of multiple LoRA adapters can be supported by customized operations";
+ * packing P:261-266), the forward and backward of ONE frozen base projection plus the
+ * tasks' LoRA adapters (§2.1 "computes XW + XBA"):
+ *
+ *     for every token row x of a sequence of task t:
+ *        y  = x W^T + s_t (x A_t^T) B_t^T                       (forward)
+ *        dx = dy W  + s_t (dy B_t) A_t                           (backward, W frozen
+ *        dA_t += s_t sum_rows (dy B_t)^T x                        P:74: no dW)
+ *        dB_t += s_t sum_rows dy^T (x A_t^T)
+ *
+ * Names: A_t is the "shrink" (paper's B), B_t the "expand" (paper's A); storage is
+ * PyTorch/PEFT style (reading Q24):
+ *     W   [out, in]    row-major (torch Linear.weight; a TP rank passes its local shard)
+ *     A   [sum_t r_t, in]   task t's rows start at roff[t] = sum_{u<t} r_u   (lora_A)
+ *     B   [out, sum_t r_t]  task t's columns start at roff[t]               (lora_B)
+ *     X   [T, in], Y [T, out], dY [T, out], dX [T, in]  row-major, T = sum seq_lens
+ *     dA  [sum_t r_t, in] fp32 (row stride problem.dA_ld), dB [out, sum_t r_t] fp32
+ *
+ * It also implements the per-step workload-balanced dispatch (Eq. 3 and
+ * dynamic bucketing) and the adapter-gradient all-reduce across FT replicas (P:170,
+ * P:306 "must synchronize the parameters of LoRA adapters for every training step").
+ *
+ * Conventions (all entry points):
+ *  - Every function returns lobra_status; nothing throws across the ABI.
+ *  - All host-side checks run BEFORE any device work is enqueued; on error nothing is
+ *    enqueued and lobra_last_error() says why (thread-local string, valid until the
+ *    next call on the same thread).
+ *  - Device work is enqueued on the caller's stream in stream order; there is no
+ *    implicit device synchronisation.  Asynchronous CUDA faults surface at the
+ *    caller's next synchronisation.
+ *  - The caller allocates and owns every device buffer (X, W, A, B, Y, Hs, dX, dA, dB,
+ *    workspace).  The library never allocates device memory on the hot path.  Host
+ *    arrays are only read during the call.  A lazily created per-device context
+ *    (SM count, a small ring of pinned host staging buffers) is freed by
+ *    lobra_shutdown().
+ *  - Calls on different streams are safe if their workspaces do not alias.
+ *  - Requires an sm_100 (B200) device for the compute entry points
+ *    (LOBRA_ERR_UNSUPPORTED otherwise).
+ */
+#ifndef LOBRA_H_
+#define LOBRA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LOBRA_API __attribute__((visibility("default")))
+#else
+#define LOBRA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* lobra_stream_t;   /* == cudaStream_t */
+
+/* Status codes; 1-3 reuse SPEC.md's CLI exit codes. */
+typedef enum {
+  LOBRA_OK = 0,
+  LOBRA_ERR_INPUT = 1,        /* bad argument: shape, alignment, rank, task id, ...    */
+  LOBRA_ERR_INFEASIBLE = 2,   /* dispatch: a sequence fits no deployed replica, or     */
+                              /* exceeds the grid ("re-plan required")          */
+  LOBRA_ERR_BUDGET = 3,       /* dispatch: Eq. 3 solver node cap hit; the best         */
+                              /* incumbent found is returned                   */
+  LOBRA_ERR_CUDA = 4,         /* a CUDA runtime/driver call failed                     */
+  LOBRA_ERR_NCCL = 5,         /* an NCCL call failed, or NCCL could not be loaded      */
+  LOBRA_ERR_UNSUPPORTED = 6   /* device is not sm_100, or configuration not supported  */
+} lobra_status;
+
+/* Human-readable reason for the last non-OK status on this thread. */
+LOBRA_API const char* lobra_last_error(void);
+
+/* Library version string, e.g. "lobra-b200 0.1 (sm_100a)". */
+LOBRA_API const char* lobra_version(void);
+
+typedef enum { LOBRA_BF16 = 0, LOBRA_FP32 = 1 } lobra_dtype;
+
+/* Megatron tensor parallelism of the base projection inside one FT replica
+ * (§2.2).  COLUMN: W sharded along `out` (q,k,v,gate,up); the backward
+ * all-reduces dX over the TP group.  ROW: W sharded along `in` (o,down); the forward
+ * all-reduces Y over the TP group.  The LoRA adapters add no collective (DESIGN.md
+ * "Multi-GPU").  NONE: unsharded, no collective. */
+typedef enum { LOBRA_TP_NONE = 0, LOBRA_TP_COLUMN = 1, LOBRA_TP_ROW = 2 } lobra_tp_kind;
+
+/* The packed batch (host arrays).  Sequence k occupies rows [off_k, off_k + seq_lens[k])
+ * of X/Y/dY/dX, off_k = sum_{j<k} seq_lens[j]; its task is seq_task[k] in
+ * [0, num_tasks).  P:256-266 (packing, block-diagonal: rows of different sequences never
+ * interact in a projection).  Any order is accepted; grouping sequences by task (what
+ * lobra_dispatch emits) minimises mixed-task tiles.  num_seqs >= 1, seq_lens[k] >= 0. */
+typedef struct {
+  int32_t num_seqs;
+  const int32_t* seq_lens;
+  const int32_t* seq_task;
+} lobra_batch;
+
+/* The tasks' adapters for this projection.  ranks/scales are host arrays of length
+ * num_tasks; 1 <= ranks[t] <= 64 (reading Q4); scales are s_t (reading Q2,
+ * the paper has no scale).  A and B are DEVICE pointers in the dtype of the problem,
+ * laid out as described at the top of this file (for a TP rank: its local shard, i.e.
+ * COLUMN: B holds the rank's `out` rows; ROW: A holds the rank's `in` columns,
+ * contiguous [sum r, in_local]). */
+typedef struct {
+  int32_t num_tasks;
+  const int32_t* ranks;
+  const float* scales;
+  const void* A;
+  const void* B;
+} lobra_adapters;
+
+typedef struct lobra_comm_s* lobra_comm;   /* opaque: NCCL world comm + TP sub-comm */
+
+/* One projection.  in/out are the LOCAL (per-rank) widths.  bf16: in and out must be
+ * multiples of 64.  fp32: any positive sizes.  dA_ld: row stride (elements) of the dA
+ * output (0 = in); lets a ROW-parallel rank write its column slice of a full-size flat
+ * gradient buffer.  tp may be NULL when tp_kind == LOBRA_TP_NONE. */
+typedef struct {
+  lobra_dtype dtype;
+  int64_t in;
+  int64_t out;
+  lobra_tp_kind tp_kind;
+  lobra_comm tp;
+  int64_t dA_ld;
+} lobra_problem;
+
+/* Bytes of device workspace lobra_lora_fwd / lobra_lora_bwd need for this problem and
+ * batch (both directions; 256-byte aligned pointer required).  Returns 0 and sets the
+ * last error on invalid input. */
+LOBRA_API size_t lobra_lora_workspace_bytes(const lobra_problem* prob, const lobra_batch* batch,
+                                  const lobra_adapters* ad);
+
+/* Bytes of the opaque saved state `Hs` (the pre-scaled shrink H_s = s_t X A_t^T in the
+ * library's per-row-tile layout) that lobra_lora_fwd writes and lobra_lora_bwd reads. */
+LOBRA_API size_t lobra_lora_saved_bytes(const lobra_problem* prob, const lobra_batch* batch,
+                              const lobra_adapters* ad);
+
+/* Forward: Y = X W^T + s_t (X A_t^T) B_t^T per task segment.
+ * X [T,in], W [out,in], Y [T,out] device; Hs (saved for bwd) and ws device scratch.
+ * ROW-parallel with a comm: Y is summed over the TP group (ncclAllReduce, in place).
+ * Errors: LOBRA_ERR_INPUT (shapes/alignment/ranks/task ids/workspace too small),
+ * LOBRA_ERR_UNSUPPORTED (not sm_100), LOBRA_ERR_CUDA, LOBRA_ERR_NCCL. */
+LOBRA_API lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_batch* batch,
+                            const lobra_adapters* ad, const void* X, const void* W, void* Y,
+                            void* Hs, void* ws, size_t ws_bytes, lobra_stream_t stream);
+
+/* Backward (W frozen: P:74):
+ *   dX  = dY W + s_t (dY B_t) A_t             (written, or added to dX if accumulate_dx)
+ *   dA_t = s_t sum (dY B_t)^T X  [r_t, in]     fp32 (written, or added if accumulate_dadb)
+ *   dB_t = s_t sum dY^T (X A_t^T) [out, r_t]   fp32 (same)
+ * Gradient sums are plain sums over the call's tokens (reading Q7); a task with no
+ * tokens leaves its dA/dB untouched when accumulating and writes zeros otherwise
+ * (reading Q10).  Hs must come from lobra_lora_fwd on the same batch/adapters.
+ * COLUMN-parallel with a comm: dX is summed over the TP group (in place).
+ * dA_t/dB_t reductions are deterministic (fixed order; no atomics). */
+LOBRA_API lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_batch* batch,
+                            const lobra_adapters* ad, const void* X, const void* W,
+                            const void* Hs, const void* dY, void* dX, int accumulate_dx,
+                            float* dA, float* dB, int accumulate_dadb, void* ws,
+                            size_t ws_bytes, lobra_stream_t stream);
+
+/* ------------------------------------------------------------------------------
+ * Per-step dispatch (host only, deterministic; every rank may compute it locally).
+ * Implements P:591-619 (dynamic bucketing DP over the grid u_k = k*grid_step,
+ * k = 1..grid_max/grid_step, empty intervals ignored, lexicographically smallest optimal
+ * boundary list), r_i = #{j : s_j <= M_i} (Table tab:notations), Eq. 3
+ * solved exactly with the App. D cost T_i = sum_j c_ij ceil(d_ij / p_i)
+ * and the canonical tie-break "lexicographically smallest d in (group, bucket)
+ * order", then: bucket j's sequences in ascending index go to groups in order; within a
+ * group a per-bucket round robin starting at the replica with the smallest running
+ * cost; chunks of floor(M_i / s_j) sequences ordered by descending cost;
+ * inside a chunk sequences ordered by (task id, index).  See DESIGN.md "Dispatch".
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_groups;          /* G; groups ordered by (tp asc, max_tokens asc)        */
+  const int32_t* tp;           /* [G] n_i: GPUs per replica (TP degree)                 */
+  const int32_t* replicas;     /* [G] p_i >= 0 (0 = configuration not deployed)         */
+  const int32_t* max_tokens;   /* [G] M_i: max tokens per chunk, multiple of grid_step  */
+  const int64_t* cost;         /* [G * U] integer cost of ONE sequence padded to grid   */
+                               /* value u_k = (k+1)*grid_step, k = 0..U-1 (reading Q15) */
+} lobra_deployment;
+
+typedef struct {
+  int32_t num_buckets;         /* out: R' <= R buckets actually formed                   */
+  int32_t* boundaries;         /* [R] out: s_1 < ... < s_R'                               */
+  int64_t* d;                  /* [G * R] out: d_ij, row-major with row stride R          */
+  int32_t* seq_bucket;         /* [n] out: bucket index of every sequence                 */
+  int32_t* seq_replica;        /* [n] out: global replica id (group-major numbering)      */
+  int32_t* seq_chunk;          /* [n] out: chunk (micro-batch) index within the replica   */
+  int32_t* pack_order;         /* [n] out: position of the sequence inside its chunk      */
+  int64_t* replica_cost;       /* [sum p_i] out: assigned cost per replica                */
+  int64_t t_hat;               /* out: Eq. 3 objective max_i sum_j c_ij ceil(d_ij/p_i)    */
+  int64_t nodes;               /* out: branch-and-bound nodes explored                    */
+} lobra_dispatch_out;
+
+/* mode: 0 = balanced (Eq. 3), 1 = length-based (Fig. 4(c): every bucket to the
+ * supporting group with the smallest c_ij * n_i, ties to the earlier group).
+ * node_cap: max branch-and-bound nodes (<= 0: default 2e7); on hitting it the best
+ * incumbent is returned with LOBRA_ERR_BUDGET.  Errors: LOBRA_ERR_INPUT,
+ * LOBRA_ERR_INFEASIBLE.  Host only; thread-safe (no global state). */
+LOBRA_API lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
+                            int32_t grid_step, int32_t grid_max, int32_t R, int32_t mode,
+                            int64_t node_cap, lobra_dispatch_out* out);
+
+/* ------------------------------------------------------------------------------
+ * Communication (NCCL over NVLink/NVSwitch).  One process per GPU.
+ * ------------------------------------------------------------------------------ */
+/* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (e.g. with
+ * torch.distributed.broadcast_object_list) to all ranks. */
+LOBRA_API lobra_status lobra_nccl_unique_id(void* out128);
+
+/* World communicator over all `world` ranks plus the TP sub-communicator of this
+ * rank's FT replica: ncclCommSplit(color = replica_id, key = rank).  Collective: every
+ * rank must call it.  The current CUDA device must be set by the caller. */
+LOBRA_API lobra_status lobra_comm_init(const void* id128, int32_t world, int32_t rank,
+                             int32_t replica_id, lobra_comm* out);
+LOBRA_API lobra_status lobra_comm_destroy(lobra_comm comm);
+/* TP group size / rank of this process inside its replica. */
+LOBRA_API lobra_status lobra_comm_tp_info(lobra_comm comm, int32_t* tp_size, int32_t* tp_rank);
+
+/* Adapter-gradient synchronisation across FT replicas: in-place SUM of
+ * the flat fp32 buffer over the WORLD communicator (reading Q7: sum, not mean).  Every
+ * rank passes a buffer with the identical full-size layout holding its partial sums
+ * (zeros where it owns nothing). */
+LOBRA_API lobra_status lobra_adapter_allreduce(lobra_comm comm, float* flat_grads, size_t count,
+                                     lobra_stream_t stream);
+
+/* Frees the lazily created per-device context(s). */
+LOBRA_API lobra_status lobra_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOBRA_H_ */

@@ -72,15 +72,16 @@ def lora_fwd(X, W, A_cat, B_cat, ranks, scales, seq_lens, seq_task, return_h=Fal
     return (Y, H) if return_h else Y
 
 
-def lora_bwd(X, W, A_cat, B_cat, ranks, scales, seq_lens, seq_task, dY):
-    """Returns (dX [T,in], dA_cat [sum r, in], dB_cat [out, sum r]) -- see module doc."""
+def lora_bwd(X, W, A_cat, B_cat, ranks, scales, seq_lens, seq_task, dY, want_dx=True):
+    """Returns (dX [T,in], dA_cat [sum r, in], dB_cat [out, sum r]) -- see module doc.
+    ``want_dx=False`` skips dX (returned as None) for large adapter-gradient checks."""
     X = np.asarray(X, dtype=np.float64)
     W = np.asarray(W, dtype=np.float64)
     A_cat = np.asarray(A_cat, dtype=np.float64)
     B_cat = np.asarray(B_cat, dtype=np.float64)
     dY = np.asarray(dY, dtype=np.float64)
     roff = _roff(ranks)
-    dX = np.zeros_like(X)
+    dX = np.zeros_like(X) if want_dx else None
     dA = np.zeros_like(A_cat)
     dB = np.zeros_like(B_cat)
     for a, b, t in _segments(seq_lens, seq_task):
@@ -91,7 +92,8 @@ def lora_bwd(X, W, A_cat, B_cat, ranks, scales, seq_lens, seq_task, dY):
         Bt = B_cat[:, roff[t]:roff[t + 1]]
         s = float(scales[t])
         g = np.matmul(dy, Bt)                    # dy B_t        [len, r]
-        dX[a:b] = np.matmul(dy, W) + s * np.matmul(g, At)
+        if want_dx:
+            dX[a:b] = np.matmul(dy, W) + s * np.matmul(g, At)
         dA[roff[t]:roff[t + 1]] += s * np.matmul(g.T, x)
         dB[:, roff[t]:roff[t + 1]] += s * np.matmul(dy.T, np.matmul(x, At.T))
     return dX, dA, dB

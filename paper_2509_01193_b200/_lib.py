@@ -1,0 +1,280 @@
+"""Thin ctypes binding of the C ABI in ``include/lobra.h`` (argument marshalling only).
+
+Every compute step runs inside ``liblobra.so`` (hand-written sm_100a kernels); this
+module only converts Python / torch arguments to the ABI's plain pointers and sizes.
+PyTorch is used by callers for device memory, streams and process groups.  There is no
+fallback: if the library is missing, ``load()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblobra.so")
+
+LOBRA_OK, LOBRA_ERR_INPUT, LOBRA_ERR_INFEASIBLE, LOBRA_ERR_BUDGET = 0, 1, 2, 3
+LOBRA_ERR_CUDA, LOBRA_ERR_NCCL, LOBRA_ERR_UNSUPPORTED = 4, 5, 6
+LOBRA_BF16, LOBRA_FP32 = 0, 1
+LOBRA_TP_NONE, LOBRA_TP_COLUMN, LOBRA_TP_ROW = 0, 1, 2
+
+EXPORTED = [
+    "lobra_last_error", "lobra_version", "lobra_lora_workspace_bytes", "lobra_lora_saved_bytes",
+    "lobra_lora_fwd", "lobra_lora_bwd", "lobra_dispatch", "lobra_nccl_unique_id",
+    "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
+    "lobra_shutdown",
+]
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f32p = C.POINTER(C.c_float)
+
+
+class Batch(C.Structure):
+    _fields_ = [("num_seqs", C.c_int32), ("seq_lens", _i32p), ("seq_task", _i32p)]
+
+
+class Adapters(C.Structure):
+    _fields_ = [("num_tasks", C.c_int32), ("ranks", _i32p), ("scales", _f32p),
+                ("A", C.c_void_p), ("B", C.c_void_p)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("in_", C.c_int64), ("out", C.c_int64),
+                ("tp_kind", C.c_int32), ("tp", C.c_void_p), ("dA_ld", C.c_int64)]
+
+
+class Deployment(C.Structure):
+    _fields_ = [("num_groups", C.c_int32), ("tp", _i32p), ("replicas", _i32p),
+                ("max_tokens", _i32p), ("cost", _i64p)]
+
+
+class DispatchOut(C.Structure):
+    _fields_ = [("num_buckets", C.c_int32), ("boundaries", _i32p), ("d", _i64p),
+                ("seq_bucket", _i32p), ("seq_replica", _i32p), ("seq_chunk", _i32p),
+                ("pack_order", _i32p), ("replica_cost", _i64p), ("t_hat", C.c_int64),
+                ("nodes", C.c_int64)]
+
+
+_LIB = None
+
+
+class LobraError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"lobra status {status}: {msg}")
+        self.status = status
+
+
+def load() -> C.CDLL:
+    """Loads the in-tree ``liblobra.so`` (built by ``__graft_entry__.build()``)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    lib.lobra_last_error.restype = C.c_char_p
+    lib.lobra_version.restype = C.c_char_p
+    lib.lobra_lora_workspace_bytes.restype = C.c_size_t
+    lib.lobra_lora_workspace_bytes.argtypes = [C.POINTER(Problem), C.POINTER(Batch), C.POINTER(Adapters)]
+    lib.lobra_lora_saved_bytes.restype = C.c_size_t
+    lib.lobra_lora_saved_bytes.argtypes = [C.POINTER(Problem), C.POINTER(Batch), C.POINTER(Adapters)]
+    lib.lobra_lora_fwd.restype = C.c_int
+    lib.lobra_lora_fwd.argtypes = [C.POINTER(Problem), C.POINTER(Batch), C.POINTER(Adapters),
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_size_t, C.c_void_p]
+    lib.lobra_lora_bwd.restype = C.c_int
+    lib.lobra_lora_bwd.argtypes = [C.POINTER(Problem), C.POINTER(Batch), C.POINTER(Adapters),
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                   C.c_size_t, C.c_void_p]
+    lib.lobra_dispatch.restype = C.c_int
+    lib.lobra_dispatch.argtypes = [C.POINTER(Deployment), C.POINTER(Batch), C.c_int32, C.c_int32,
+                                   C.c_int32, C.c_int32, C.c_int64, C.POINTER(DispatchOut)]
+    lib.lobra_nccl_unique_id.restype = C.c_int
+    lib.lobra_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.lobra_comm_init.restype = C.c_int
+    lib.lobra_comm_init.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+    lib.lobra_comm_destroy.restype = C.c_int
+    lib.lobra_comm_destroy.argtypes = [C.c_void_p]
+    lib.lobra_comm_tp_info.restype = C.c_int
+    lib.lobra_comm_tp_info.argtypes = [C.c_void_p, _i32p, _i32p]
+    lib.lobra_adapter_allreduce.restype = C.c_int
+    lib.lobra_adapter_allreduce.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.lobra_shutdown.restype = C.c_int
+    _LIB = lib
+    return lib
+
+
+def _check(st: int):
+    if st != LOBRA_OK:
+        raise LobraError(st, load().lobra_last_error().decode())
+
+
+def version() -> str:
+    return load().lobra_version().decode()
+
+
+# ---------------------------------------------------------------------------- marshalling
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _ptr(x) -> int:
+    """Device (or host) address of a torch tensor / int."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+class _Args:
+    """Keeps the numpy arrays alive while their pointers are inside ctypes structs."""
+
+    def __init__(self, dtype, d_in, d_out, seq_lens, seq_task, ranks, scales, A=None, B=None,
+                 tp_kind=LOBRA_TP_NONE, comm=None, dA_ld=0):
+        self.lens = _i32(seq_lens)
+        self.tasks = _i32(seq_task)
+        self.ranks = _i32(ranks)
+        self.scales = np.ascontiguousarray(np.asarray(scales, dtype=np.float32))
+        self.batch = Batch(len(self.lens), self.lens.ctypes.data_as(_i32p),
+                           self.tasks.ctypes.data_as(_i32p))
+        self.ad = Adapters(len(self.ranks), self.ranks.ctypes.data_as(_i32p),
+                           self.scales.ctypes.data_as(_f32p), _ptr(A) or 1, _ptr(B) or 1)
+        self.prob = Problem(dtype, d_in, d_out, tp_kind, comm.handle if comm is not None else None,
+                            dA_ld)
+
+
+def dtype_code(torch_dtype) -> int:
+    import torch
+    if torch_dtype == torch.bfloat16:
+        return LOBRA_BF16
+    if torch_dtype == torch.float32:
+        return LOBRA_FP32
+    raise ValueError(f"unsupported dtype {torch_dtype}")
+
+
+def lobra_lora_workspace_bytes(dtype: int, d_in: int, d_out: int, seq_lens, seq_task, ranks,
+                               scales) -> int:
+    a = _Args(dtype, d_in, d_out, seq_lens, seq_task, ranks, scales)
+    n = load().lobra_lora_workspace_bytes(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad))
+    if n == 0:
+        raise LobraError(LOBRA_ERR_INPUT, load().lobra_last_error().decode())
+    return int(n)
+
+
+def lobra_lora_saved_bytes(dtype: int, d_in: int, d_out: int, seq_lens, seq_task, ranks,
+                           scales) -> int:
+    a = _Args(dtype, d_in, d_out, seq_lens, seq_task, ranks, scales)
+    n = load().lobra_lora_saved_bytes(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad))
+    if n == 0:
+        raise LobraError(LOBRA_ERR_INPUT, load().lobra_last_error().decode())
+    return int(n)
+
+
+def lobra_lora_fwd(X, W, A, B, ranks, scales, seq_lens, seq_task, Y, Hs, ws, ws_bytes=None,
+                   tp_kind=LOBRA_TP_NONE, comm=None, stream=None, dtype=None):
+    """Y = X W^T + s_t (X A_t^T) B_t^T per task segment (include/lobra.h)."""
+    dt = dtype_code(X.dtype) if dtype is None else dtype
+    d_out, d_in = int(W.shape[0]), int(W.shape[1])
+    a = _Args(dt, d_in, d_out, seq_lens, seq_task, ranks, scales, A, B, tp_kind, comm)
+    nb = ws.numel() * ws.element_size() if ws_bytes is None else ws_bytes
+    _check(load().lobra_lora_fwd(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad), _ptr(X), _ptr(W),
+                                 _ptr(Y), _ptr(Hs), _ptr(ws), nb, _stream(stream)))
+
+
+def lobra_lora_bwd(X, W, A, B, ranks, scales, seq_lens, seq_task, Hs, dY, dX, dA, dB, ws,
+                   accumulate_dx=False, accumulate_dadb=False, ws_bytes=None, dA_ld=0,
+                   tp_kind=LOBRA_TP_NONE, comm=None, stream=None, dtype=None):
+    """dX (+)= dY W + s_t (dY B_t) A_t ; dA_t, dB_t (+)= token sums (include/lobra.h)."""
+    dt = dtype_code(X.dtype) if dtype is None else dtype
+    d_out, d_in = int(W.shape[0]), int(W.shape[1])
+    a = _Args(dt, d_in, d_out, seq_lens, seq_task, ranks, scales, A, B, tp_kind, comm, dA_ld)
+    nb = ws.numel() * ws.element_size() if ws_bytes is None else ws_bytes
+    _check(load().lobra_lora_bwd(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad), _ptr(X), _ptr(W),
+                                 _ptr(Hs), _ptr(dY), _ptr(dX), int(bool(accumulate_dx)), _ptr(dA),
+                                 _ptr(dB), int(bool(accumulate_dadb)), _ptr(ws), nb, _stream(stream)))
+
+
+def lobra_dispatch(tp, replicas, max_tokens, cost, seq_lens, seq_task, grid_step=256,
+                   grid_max=16384, R=16, mode=0, node_cap=0):
+    """Per-step dispatch (host).  Returns a dict of numpy arrays; raises LobraError on
+    input / infeasibility errors.  status LOBRA_ERR_BUDGET is returned in the dict."""
+    tp, replicas, max_tokens = _i32(tp), _i32(replicas), _i32(max_tokens)
+    cost = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
+    G = len(tp)
+    lens, tasks = _i32(seq_lens), _i32(seq_task)
+    n = len(lens)
+    dep = Deployment(G, tp.ctypes.data_as(_i32p), replicas.ctypes.data_as(_i32p),
+                     max_tokens.ctypes.data_as(_i32p), cost.ctypes.data_as(_i64p))
+    batch = Batch(n, lens.ctypes.data_as(_i32p), tasks.ctypes.data_as(_i32p))
+    out = {"boundaries": np.zeros(R, np.int32), "d": np.zeros(G * R, np.int64),
+           "seq_bucket": np.zeros(n, np.int32), "seq_replica": np.zeros(n, np.int32),
+           "seq_chunk": np.zeros(n, np.int32), "pack_order": np.zeros(n, np.int32),
+           "replica_cost": np.zeros(max(int(replicas.sum()), 1), np.int64)}
+    o = DispatchOut(0, out["boundaries"].ctypes.data_as(_i32p), out["d"].ctypes.data_as(_i64p),
+                    out["seq_bucket"].ctypes.data_as(_i32p), out["seq_replica"].ctypes.data_as(_i32p),
+                    out["seq_chunk"].ctypes.data_as(_i32p), out["pack_order"].ctypes.data_as(_i32p),
+                    out["replica_cost"].ctypes.data_as(_i64p), 0, 0)
+    st = load().lobra_dispatch(C.byref(dep), C.byref(batch), grid_step, grid_max, R, mode,
+                               node_cap, C.byref(o))
+    if st not in (LOBRA_OK, LOBRA_ERR_BUDGET):
+        raise LobraError(st, load().lobra_last_error().decode())
+    nb = o.num_buckets
+    out["status"] = st
+    out["boundaries"] = out["boundaries"][:nb]
+    out["d"] = out["d"].reshape(G, R)[:, :nb]
+    out["t_hat"] = int(o.t_hat)
+    out["nodes"] = int(o.nodes)
+    return out
+
+
+# ---------------------------------------------------------------------------- comm
+class Comm:
+    """World NCCL communicator + this rank's TP sub-communicator (lobra_comm)."""
+
+    def __init__(self, handle: int, world: int, rank: int, replica_id: int):
+        self.handle = handle
+        self.world, self.rank, self.replica_id = world, rank, replica_id
+        ts, tr = C.c_int32(0), C.c_int32(0)
+        _check(load().lobra_comm_tp_info(C.c_void_p(handle), C.byref(ts), C.byref(tr)))
+        self.tp_size, self.tp_rank = ts.value, tr.value
+
+    def destroy(self):
+        if self.handle:
+            load().lobra_comm_destroy(C.c_void_p(self.handle))
+            self.handle = 0
+
+
+def lobra_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().lobra_nccl_unique_id(buf))
+    return buf.raw
+
+
+def lobra_comm_init(uid: bytes, world: int, rank: int, replica_id: int) -> Comm:
+    h = C.c_void_p(0)
+    buf = C.create_string_buffer(uid, 128)
+    _check(load().lobra_comm_init(buf, world, rank, replica_id, C.byref(h)))
+    return Comm(h.value, world, rank, replica_id)
+
+
+def lobra_adapter_allreduce(comm: Comm, flat, stream=None):
+    _check(load().lobra_adapter_allreduce(C.c_void_p(comm.handle), _ptr(flat), int(flat.numel()),
+                                          _stream(stream)))
+
+
+def lobra_shutdown():
+    _check(load().lobra_shutdown())

@@ -1,0 +1,163 @@
+// NCCL plumbing: world communicator + per-replica TP sub-communicator
+// (ncclCommSplit(color = replica id)), the TP all-reduces of Megatron tensor parallelism
+// and the per-step adapter-gradient all-reduce across FT replicas (P:170,
+// P:306).  NCCL is resolved at run time with dlopen so that the process uses the single
+// libnccl.so.2 that torch already loaded (NCCL 2.28 in this image).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "common.h"
+#include "nccl.h"
+
+namespace lobra {
+namespace {
+
+struct Nccl {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*CommCount)(const ncclComm_t, int*);
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+Nccl g_nccl;
+std::once_flag g_once;
+
+void load_nccl() {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return;
+#define LOAD(f, name)                                                  \
+  g_nccl.f = reinterpret_cast<decltype(g_nccl.f)>(dlsym(h, name));     \
+  if (!g_nccl.f) return;
+  LOAD(GetUniqueId, "ncclGetUniqueId");
+  LOAD(CommInitRank, "ncclCommInitRank");
+  LOAD(CommSplit, "ncclCommSplit");
+  LOAD(CommDestroy, "ncclCommDestroy");
+  LOAD(CommCount, "ncclCommCount");
+  LOAD(CommUserRank, "ncclCommUserRank");
+  LOAD(AllReduce, "ncclAllReduce");
+  LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+  g_nccl.ok = true;
+}
+
+lobra_status need_nccl() {
+  std::call_once(g_once, load_nccl);
+  if (!g_nccl.ok) return fail(LOBRA_ERR_NCCL, "libnccl.so.2 could not be loaded (import torch first)");
+  return LOBRA_OK;
+}
+
+lobra_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return LOBRA_OK;
+  return fail(LOBRA_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+}
+
+}  // namespace
+}  // namespace lobra
+
+struct lobra_comm_s {
+  ncclComm_t world = nullptr;
+  ncclComm_t tp = nullptr;
+  int world_size = 0, rank = 0, tp_size = 0, tp_rank = 0;
+};
+
+namespace lobra {
+lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st) {
+  lobra_status s = need_nccl();
+  if (s != LOBRA_OK) return s;
+  if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
+  if (c->tp_size == 1) return LOBRA_OK;
+  return nccl_check(g_nccl.AllReduce(buf, buf, count, ncclBfloat16, ncclSum, c->tp, st),
+                    "TP all-reduce");
+}
+lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st) {
+  lobra_status s = need_nccl();
+  if (s != LOBRA_OK) return s;
+  if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
+  if (c->tp_size == 1) return LOBRA_OK;
+  return nccl_check(g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c->tp, st),
+                    "TP all-reduce");
+}
+}  // namespace lobra
+
+using namespace lobra;
+
+extern "C" lobra_status lobra_nccl_unique_id(void* out128) {
+  clear_error();
+  if (!out128) return fail(LOBRA_ERR_INPUT, "null output");
+  lobra_status s = need_nccl();
+  if (s != LOBRA_OK) return s;
+  ncclUniqueId id;
+  if ((s = nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId")) != LOBRA_OK) return s;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(out128, &id, 128);
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_comm_init(const void* id128, int32_t world, int32_t rank,
+                                        int32_t replica_id, lobra_comm* out) {
+  clear_error();
+  if (!id128 || !out || world < 1 || rank < 0 || rank >= world || replica_id < 0)
+    return fail(LOBRA_ERR_INPUT, "bad comm_init arguments");
+  lobra_status s = need_nccl();
+  if (s != LOBRA_OK) return s;
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  lobra_comm c = new lobra_comm_s();
+  c->world_size = world;
+  c->rank = rank;
+  if ((s = nccl_check(g_nccl.CommInitRank(&c->world, world, id, rank), "ncclCommInitRank")) != LOBRA_OK) {
+    delete c;
+    return s;
+  }
+  if ((s = nccl_check(g_nccl.CommSplit(c->world, replica_id, rank, &c->tp, nullptr), "ncclCommSplit")) !=
+      LOBRA_OK) {
+    g_nccl.CommDestroy(c->world);
+    delete c;
+    return s;
+  }
+  g_nccl.CommCount(c->tp, &c->tp_size);
+  g_nccl.CommUserRank(c->tp, &c->tp_rank);
+  *out = c;
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_comm_destroy(lobra_comm c) {
+  clear_error();
+  if (!c) return LOBRA_OK;
+  if (g_nccl.ok) {
+    if (c->tp) g_nccl.CommDestroy(c->tp);
+    if (c->world) g_nccl.CommDestroy(c->world);
+  }
+  delete c;
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_comm_tp_info(lobra_comm c, int32_t* tp_size, int32_t* tp_rank) {
+  clear_error();
+  if (!c || !tp_size || !tp_rank) return fail(LOBRA_ERR_INPUT, "null argument");
+  *tp_size = c->tp_size;
+  *tp_rank = c->tp_rank;
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_adapter_allreduce(lobra_comm c, float* flat, size_t count,
+                                                lobra_stream_t stream) {
+  clear_error();
+  if (!c || !c->world) return fail(LOBRA_ERR_INPUT, "null comm");
+  if (!flat && count) return fail(LOBRA_ERR_INPUT, "null buffer");
+  lobra_status s = need_nccl();
+  if (s != LOBRA_OK) return s;
+  if (c->world_size == 1 || count == 0) return LOBRA_OK;
+  return nccl_check(g_nccl.AllReduce(flat, flat, count, ncclFloat32, ncclSum, c->world,
+                                     reinterpret_cast<cudaStream_t>(stream)),
+                    "adapter all-reduce");
+}

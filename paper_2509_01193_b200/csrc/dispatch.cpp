@@ -1,0 +1,499 @@
+// lobra_dispatch: LobRA's per-step workload-balanced dispatch, host only.
+//
+// PAPER.md §4.3: given the deployed heterogeneous FT replicas p*_i, each
+// step buckets the batch by length with a DP over the grid and solves
+// Eq. 3
+//     min_d max_i T({ceil(d_ij / p_i)}_j ; S_i)
+//     s.t. sum_i d_ij = B_j,  d_ij <= B_j p_i
+// with the App. D cost T_i = sum_j c_ij * ceil(d_ij / p_i) for PP = 1,
+// c_ij = the caller's integer cost of one sequence padded to s_j on group i (linear in
+// the per-replica count; reading Q15).
+//
+// The Eq. 3 ILP is solved EXACTLY and canonically (lexicographically smallest optimal d
+// in (group, bucket) order, reading Q12):
+//  * 1 deployed group: trivial.
+//  * 2 groups: a pseudo-polynomial DP over the first group's cost budget:
+//        Suf_j(b) = min cost of group 2 over buckets j..R-1 with group-1 cost <= b
+//    then t* = min_b max(b, Suf_0(b)) and the lexicographic reconstruction picks, bucket
+//    by bucket, the smallest d_1j whose completion still meets t*.
+//  * >2 groups: depth-first search over the leading groups' d (lexicographic order,
+//    ascending values) with the 2-group DP as the exact leaf solver; node-capped.
+// This is an independent implementation of what oracle/dispatch.py computes by brute
+// force / MILP; tests check the two agree bit for bit.
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.h"
+
+namespace {
+
+using i64 = int64_t;
+const i64 BIG = INT64_MAX / 4;
+
+inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ bucketing
+// Returns boundaries (grid values) minimising cross-interval padding with <= R buckets,
+// the lexicographically smallest optimal list.  occ_u / occ_c: occupied grid values and
+// their counts, ascending.
+std::vector<i64> bucketize(const std::vector<i64>& u, const std::vector<i64>& cnt, int R) {
+  const int V = (int)u.size();
+  // prefix sums for O(1) segment cost: cost(a..b) = u_b * C(a..b) - S(a..b)
+  std::vector<i64> C(V + 1, 0), S(V + 1, 0);
+  for (int v = 0; v < V; ++v) {
+    C[v + 1] = C[v] + cnt[v];
+    S[v + 1] = S[v] + cnt[v] * u[v];
+  }
+  auto seg = [&](int a, int b) {  // intervals a..b (0-based, inclusive) padded to u[b]
+    return u[b] * (C[b + 1] - C[a]) - (S[b + 1] - S[a]);
+  };
+  // F[k][j]: min padding of intervals k..V-1 with <= j buckets (F[V][*] = 0)
+  std::vector<std::vector<i64>> F(V + 1, std::vector<i64>(R + 1, BIG));
+  for (int j = 0; j <= R; ++j) F[V][j] = 0;
+  for (int k = V - 1; k >= 0; --k)
+    for (int j = 1; j <= R; ++j) {
+      i64 best = BIG;
+      for (int e = k; e < V; ++e) {
+        if (F[e + 1][j - 1] >= BIG) continue;
+        best = std::min(best, seg(k, e) + F[e + 1][j - 1]);
+      }
+      F[k][j] = best;
+    }
+  std::vector<i64> out;
+  int k = 0, j = R;
+  while (k < V) {
+    for (int e = k; e < V; ++e) {
+      if (F[e + 1][j - 1] < BIG && seg(k, e) + F[e + 1][j - 1] == F[k][j]) {
+        out.push_back(u[e]);
+        k = e + 1;
+        --j;
+        break;
+      }
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ Eq. 3 solver
+struct Inst {
+  int G = 0, R = 0;
+  std::vector<i64> Bj;               // demand per bucket
+  std::vector<i64> p;                // replicas per group
+  std::vector<int> r;                // supported bucket count per group
+  std::vector<std::vector<i64>> c;   // cost per (group, bucket)
+  bool sup(int i, int j) const { return j < r[i]; }
+  i64 cost(int i, int j, i64 d) const { return d ? c[i][j] * cdiv(d, p[i]) : 0; }
+};
+
+struct Budget {
+  i64 cap, used = 0;
+  bool hit = false;
+  bool take(i64 n) {
+    used += n;
+    if (used > cap) hit = true;
+    return !hit;
+  }
+};
+
+// Two-group exact solver on residual demands D_j with fixed extra loads La, Lb.
+// Groups a, b of `in`.  Builds Suf tables over budgets 0..UB for group a's cost.
+struct Two {
+  const Inst& I;
+  int a, b;
+  std::vector<i64> D;
+  i64 La, Lb, UB;
+  std::vector<std::vector<i64>> Suf;   // [R+1][UB+1]
+  bool ok = false;
+
+  Two(const Inst& in, int ga, int gb, std::vector<i64> dem, i64 la, i64 lb, i64 ub, Budget& bud)
+      : I(in), a(ga), b(gb), D(std::move(dem)), La(la), Lb(lb), UB(ub) {
+    if (UB < 0) return;
+    const int R = I.R;
+    i64 cells = 0;
+    for (int j = 0; j < R; ++j) cells += (UB + 1) * (cdiv(D[j], I.p[a]) + 2);
+    if (!bud.take(cells)) return;
+    Suf.assign(R + 1, std::vector<i64>(UB + 1, 0));
+    for (int j = R - 1; j >= 0; --j) {
+      std::vector<i64>& cur = Suf[j];
+      const std::vector<i64>& nxt = Suf[j + 1];
+      std::fill(cur.begin(), cur.end(), BIG);
+      const i64 Dj = D[j];
+      if (Dj == 0) {
+        cur = nxt;
+        continue;
+      }
+      const bool sa = I.sup(a, j), sb = I.sup(b, j);
+      const i64 qmax = sa ? cdiv(Dj, I.p[a]) : 0;
+      for (i64 q = 0; q <= qmax; ++q) {
+        const i64 da = std::min(Dj, q * I.p[a]);
+        const i64 rest = Dj - da;
+        if (rest > 0 && !sb) continue;
+        const i64 ca = I.c[a][j] * q;
+        if (ca > UB) break;
+        const i64 cb = rest ? I.c[b][j] * cdiv(rest, I.p[b]) : 0;
+        for (i64 bb = ca; bb <= UB; ++bb) {
+          const i64 v = nxt[bb - ca];
+          if (v >= BIG) continue;
+          if (v + cb < cur[bb]) cur[bb] = v + cb;
+        }
+      }
+    }
+    ok = true;
+  }
+  // min over budgets of max(La + b, Lb + Suf_0(b))
+  i64 best() const {
+    i64 t = BIG;
+    for (i64 bb = 0; bb <= UB; ++bb) {
+      if (Suf[0][bb] >= BIG) continue;
+      t = std::min(t, std::max(La + bb, Lb + Suf[0][bb]));
+    }
+    return t;
+  }
+  // Lexicographically smallest d_a (then d_b = D - d_a) with max <= t; false if none.
+  bool lexmin(i64 t, std::vector<i64>& da_out) const {
+    const int R = I.R;
+    i64 budget = std::min(UB, t - La);
+    if (budget < 0) return false;
+    i64 usedb = Lb;
+    da_out.assign(R, 0);
+    if (Suf[0][budget] >= BIG || usedb + Suf[0][budget] > t) return false;
+    for (int j = 0; j < R; ++j) {
+      const i64 Dj = D[j];
+      bool found = (Dj == 0);
+      for (i64 d = 0; d <= Dj && !found; ++d) {
+        if (d > 0 && !I.sup(a, j)) break;
+        if (Dj - d > 0 && !I.sup(b, j)) continue;
+        const i64 ca = I.cost(a, j, d);
+        if (ca > budget) break;
+        const i64 cb = I.cost(b, j, Dj - d);
+        const i64 rest = Suf[j + 1][budget - ca];
+        if (rest < BIG && usedb + cb + rest <= t) {
+          da_out[j] = d;
+          budget -= ca;
+          usedb += cb;
+          found = true;
+        }
+      }
+      if (!found) return false;
+    }
+    return true;
+  }
+};
+
+i64 objective(const Inst& I, const std::vector<std::vector<i64>>& d) {
+  i64 t = 0;
+  for (int i = 0; i < I.G; ++i) {
+    i64 s = 0;
+    for (int j = 0; j < I.R; ++j) s += I.cost(i, j, d[i][j]);
+    t = std::max(t, s);
+  }
+  return t;
+}
+
+// By-length dispatch (Fig. 4(c)); always feasible when every bucket is supported.
+std::vector<std::vector<i64>> by_length(const Inst& I, const std::vector<i64>& tp) {
+  std::vector<std::vector<i64>> d(I.G, std::vector<i64>(I.R, 0));
+  for (int j = 0; j < I.R; ++j) {
+    int bi = -1;
+    i64 bv = BIG;
+    for (int i = 0; i < I.G; ++i)
+      if (I.sup(i, j) && I.c[i][j] * tp[i] < bv) bv = I.c[i][j] * tp[i], bi = i;
+    if (bi >= 0) d[bi][j] = I.Bj[j];
+  }
+  return d;
+}
+
+// DFS over the leading groups (all but the last two) in lexicographic order.
+struct Multi {
+  const Inst& I;
+  Budget& bud;
+  i64 UB;
+  i64 best = BIG;
+  std::vector<std::vector<i64>> cur, sol;
+  bool want_lex = false;
+  i64 target = BIG;
+  bool done = false;
+  Multi(const Inst& in, Budget& b, i64 ub) : I(in), bud(b), UB(ub) {
+    cur.assign(I.G, std::vector<i64>(I.R, 0));
+  }
+  // Phase 1 (want_lex=false): minimise; phase 2: first lexicographic d meeting target.
+  void rec(int i, int j, std::vector<i64>& rem, std::vector<i64>& load) {
+    if (done || bud.hit) return;
+    const int G = I.G;
+    if (i == G - 2) {
+      Two two(I, G - 2, G - 1, rem, load[G - 2], load[G - 1],
+              (want_lex ? target : std::min(best, UB)) - load[G - 2], bud);
+      if (!two.ok) return;
+      if (!want_lex) {
+        const i64 t = std::max(two.best(), *std::max_element(load.begin(), load.end() - 2));
+        if (t < best) {
+          best = t;
+        }
+      } else {
+        std::vector<i64> da;
+        if (two.lexmin(target, da)) {
+          sol = cur;
+          for (int jj = 0; jj < I.R; ++jj) {
+            sol[G - 2][jj] = da[jj];
+            sol[G - 1][jj] = rem[jj] - da[jj];
+          }
+          done = true;
+        }
+      }
+      return;
+    }
+    if (j == I.R) {
+      rec(i + 1, 0, rem, load);
+      return;
+    }
+    const i64 lim = want_lex ? target : best - 1;
+    const i64 hi = I.sup(i, j) ? rem[j] : 0;
+    for (i64 d = 0; d <= hi; ++d) {
+      if (!bud.take(1)) return;
+      const i64 ci = I.cost(i, j, d);
+      if (load[i] + ci > lim) break;
+      // remaining must still be coverable by some later group
+      load[i] += ci;
+      rem[j] -= d;
+      cur[i][j] = d;
+      bool coverable = true;
+      if (rem[j] > 0) {
+        coverable = false;
+        for (int k = i + 1; k < G; ++k) coverable |= I.sup(k, j);
+      }
+      if (coverable) rec(i, j + 1, rem, load);
+      cur[i][j] = 0;
+      rem[j] += d;
+      load[i] -= ci;
+      if (done || bud.hit) return;
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
+                                       int32_t grid_step, int32_t grid_max, int32_t R,
+                                       int32_t mode, int64_t node_cap,
+                                       lobra_dispatch_out* out) {
+  using lobra::fail;
+  lobra::clear_error();
+  if (!dep || !batch || !out) return fail(LOBRA_ERR_INPUT, "null argument");
+  if (grid_step < 1 || grid_max < grid_step || grid_max % grid_step)
+    return fail(LOBRA_ERR_INPUT, "grid_max must be a positive multiple of grid_step");
+  if (R < 1) return fail(LOBRA_ERR_INPUT, "R must be >= 1");
+  if (mode != 0 && mode != 1) return fail(LOBRA_ERR_INPUT, "unknown mode %d", mode);
+  const int G = dep->num_groups;
+  const int n = batch->num_seqs;
+  if (G < 1 || !dep->tp || !dep->replicas || !dep->max_tokens || !dep->cost)
+    return fail(LOBRA_ERR_INPUT, "deployment arrays missing");
+  if (n < 1 || !batch->seq_lens || !batch->seq_task) return fail(LOBRA_ERR_INPUT, "empty batch");
+  if (!out->boundaries || !out->d || !out->seq_bucket || !out->seq_replica || !out->seq_chunk ||
+      !out->pack_order || !out->replica_cost)
+    return fail(LOBRA_ERR_INPUT, "output arrays missing");
+  const int U = grid_max / grid_step;
+  std::vector<i64> tp(G), p(G), M(G);
+  i64 total_rep = 0;
+  for (int i = 0; i < G; ++i) {
+    tp[i] = dep->tp[i];
+    p[i] = dep->replicas[i];
+    M[i] = dep->max_tokens[i];
+    if (tp[i] < 1 || p[i] < 0 || M[i] < grid_step || M[i] % grid_step)
+      return fail(LOBRA_ERR_INPUT, "group %d: tp>=1, replicas>=0, max_tokens multiple of grid_step", i);
+    if (i && (tp[i - 1] > tp[i] || (tp[i - 1] == tp[i] && M[i - 1] > M[i])))
+      return fail(LOBRA_ERR_INPUT, "groups must be ordered by (tp, max_tokens)");
+    for (int k = 0; k < U; ++k)
+      if (dep->cost[(size_t)i * U + k] < 0) return fail(LOBRA_ERR_INPUT, "negative cost");
+    total_rep += p[i];
+  }
+  if (total_rep < 1) return fail(LOBRA_ERR_INPUT, "no replica deployed");
+  // 1. histogram on the grid u_k = k * grid_step
+  std::vector<i64> hist(U, 0);
+  std::vector<int> seq_k(n);
+  for (int s = 0; s < n; ++s) {
+    const i64 l = batch->seq_lens[s];
+    if (l < 1) return fail(LOBRA_ERR_INPUT, "sequence %d has length %lld < 1", s, (long long)l);
+    if (l > grid_max)
+      return fail(LOBRA_ERR_INFEASIBLE, "sequence %d (length %lld) exceeds the grid maximum %d", s,
+                  (long long)l, grid_max);
+    seq_k[s] = (int)cdiv(l, grid_step);   // 1-based interval
+    hist[seq_k[s] - 1]++;
+  }
+  // 2-3. compress empty intervals; DP boundaries
+  std::vector<i64> ou, oc;
+  for (int k = 0; k < U; ++k)
+    if (hist[k]) ou.push_back((i64)(k + 1) * grid_step), oc.push_back(hist[k]);
+  const std::vector<i64> bnd = bucketize(ou, oc, R);
+  const int Rb = (int)bnd.size();
+  std::vector<int> seq_b(n);
+  std::vector<i64> Bj(Rb, 0);
+  for (int s = 0; s < n; ++s) {
+    const i64 u = (i64)seq_k[s] * grid_step;
+    const int j = (int)(std::lower_bound(bnd.begin(), bnd.end(), u) - bnd.begin());
+    seq_b[s] = j;
+    Bj[j]++;
+  }
+  // 4. r_i and costs
+  Inst I;
+  I.G = G;
+  I.R = Rb;
+  I.Bj = Bj;
+  I.p = p;
+  I.r.assign(G, 0);
+  I.c.assign(G, std::vector<i64>(Rb, 0));
+  for (int i = 0; i < G; ++i) {
+    if (p[i] > 0)
+      for (int j = 0; j < Rb; ++j) I.r[i] += bnd[j] <= M[i];
+    for (int j = 0; j < Rb; ++j) I.c[i][j] = dep->cost[(size_t)i * U + (bnd[j] / grid_step - 1)];
+  }
+  for (int j = 0; j < Rb; ++j) {
+    bool s = false;
+    for (int i = 0; i < G; ++i) s |= I.sup(i, j);
+    if (!s)
+      return fail(LOBRA_ERR_INFEASIBLE, "bucket %lld fits no deployed replica: re-plan required",
+                  (long long)bnd[j]);
+  }
+  // 5-6. Eq. 3 on the deployed groups only
+  std::vector<int> live;
+  for (int i = 0; i < G; ++i)
+    if (p[i] > 0) live.push_back(i);
+  Inst L;
+  L.G = (int)live.size();
+  L.R = Rb;
+  L.Bj = Bj;
+  std::vector<i64> ltp;
+  for (int i : live) L.p.push_back(p[i]), L.r.push_back(I.r[i]), L.c.push_back(I.c[i]), ltp.push_back(tp[i]);
+  Budget bud{node_cap > 0 ? node_cap : (i64)400000000};
+  std::vector<std::vector<i64>> dl = by_length(L, ltp);
+  lobra_status st = LOBRA_OK;
+  if (mode == 0 && L.G >= 2) {
+    const i64 UB = objective(L, dl);
+    if (L.G == 2) {
+      Two two(L, 0, 1, Bj, 0, 0, UB, bud);
+      std::vector<i64> da;
+      if (two.ok) {
+        const i64 t = two.best();
+        if (two.lexmin(t, da)) {
+          for (int j = 0; j < Rb; ++j) dl[0][j] = da[j], dl[1][j] = Bj[j] - da[j];
+        }
+      }
+    } else {
+      Multi m(L, bud, UB);
+      std::vector<i64> rem = Bj, load(L.G, 0);
+      m.best = UB + 1;
+      m.rec(0, 0, rem, load);
+      if (!bud.hit && m.best <= UB) {
+        m.want_lex = true;
+        m.target = m.best;
+        m.rec(0, 0, rem, load);
+        if (m.done) dl = m.sol;
+      }
+    }
+    if (bud.hit) st = LOBRA_ERR_BUDGET;
+  } else if (mode == 0 && L.G == 1) {
+    for (int j = 0; j < Rb; ++j) dl[0][j] = Bj[j];
+  }
+  // write d (all groups; undeployed rows are 0)
+  std::vector<std::vector<i64>> d(G, std::vector<i64>(Rb, 0));
+  for (size_t k = 0; k < live.size(); ++k) d[live[k]] = dl[k];
+  i64 t_hat = 0;
+  for (int i = 0; i < G; ++i) {
+    if (!p[i]) continue;
+    i64 s = 0;
+    for (int j = 0; j < Rb; ++j) s += I.cost(i, j, d[i][j]);
+    t_hat = std::max(t_hat, s);
+  }
+  // 7. sequences of bucket j in ascending index -> groups in order
+  std::vector<int> seq_g(n, -1);
+  {
+    std::vector<std::vector<int>> idx(Rb);
+    for (int s = 0; s < n; ++s) idx[seq_b[s]].push_back(s);
+    for (int j = 0; j < Rb; ++j) {
+      size_t pos = 0;
+      for (int i = 0; i < G; ++i)
+        for (i64 q = 0; q < d[i][j]; ++q) seq_g[idx[j][pos++]] = i;
+    }
+  }
+  // 8. per-bucket round robin within a group, starting at the smallest running cost
+  std::vector<i64> rbase(G + 1, 0);
+  for (int i = 0; i < G; ++i) rbase[i + 1] = rbase[i] + p[i];
+  std::vector<i64> running(total_rep, 0);
+  std::vector<int> seq_rep(n, -1);
+  for (int i = 0; i < G; ++i) {
+    if (!p[i]) continue;
+    for (int j = 0; j < Rb; ++j) {
+      int start = 0;
+      for (int q = 1; q < p[i]; ++q)
+        if (running[rbase[i] + q] < running[rbase[i] + start]) start = q;
+      int m = 0;
+      for (int s = 0; s < n; ++s) {
+        if (seq_b[s] != j || seq_g[s] != i) continue;
+        const int rep = (int)(rbase[i] + (start + m) % p[i]);
+        seq_rep[s] = rep;
+        running[rep] += I.c[i][j];
+        ++m;
+      }
+    }
+  }
+  // 9-10. chunks b_j = floor(M_i / s_j), descending cost; (task, index) inside a chunk
+  std::vector<int> seq_chunk(n, -1), pack(n, -1);
+  for (int i = 0; i < G; ++i) {
+    for (i64 rep = rbase[i]; rep < rbase[i + 1]; ++rep) {
+      struct Ch {
+        i64 cost;
+        int j, ci;
+        std::vector<int> seqs;
+      };
+      std::vector<Ch> chunks;
+      for (int j = 0; j < Rb; ++j) {
+        std::vector<int> mine;
+        for (int s = 0; s < n; ++s)
+          if (seq_rep[s] == rep && seq_b[s] == j) mine.push_back(s);
+        if (mine.empty()) continue;
+        const i64 b = M[i] / bnd[j];
+        int ci = 0;
+        for (size_t s0 = 0; s0 < mine.size(); s0 += (size_t)b, ++ci) {
+          Ch ch;
+          ch.j = j;
+          ch.ci = ci;
+          const size_t e = std::min(mine.size(), s0 + (size_t)b);
+          ch.seqs.assign(mine.begin() + s0, mine.begin() + e);
+          ch.cost = (i64)ch.seqs.size() * I.c[i][j];
+          chunks.push_back(std::move(ch));
+        }
+      }
+      std::stable_sort(chunks.begin(), chunks.end(), [](const Ch& x, const Ch& y) {
+        if (x.cost != y.cost) return x.cost > y.cost;
+        if (x.j != y.j) return x.j < y.j;
+        return x.ci < y.ci;
+      });
+      for (size_t k = 0; k < chunks.size(); ++k) {
+        std::vector<int> o = chunks[k].seqs;
+        std::stable_sort(o.begin(), o.end(), [&](int x, int y) {
+          if (batch->seq_task[x] != batch->seq_task[y]) return batch->seq_task[x] < batch->seq_task[y];
+          return x < y;
+        });
+        for (size_t q = 0; q < o.size(); ++q) seq_chunk[o[q]] = (int)k, pack[o[q]] = (int)q;
+      }
+    }
+  }
+  out->num_buckets = Rb;
+  for (int j = 0; j < Rb; ++j) out->boundaries[j] = (int32_t)bnd[j];
+  for (int i = 0; i < G; ++i)
+    for (int j = 0; j < R; ++j) out->d[(size_t)i * R + j] = j < Rb ? d[i][j] : 0;
+  for (int s = 0; s < n; ++s) {
+    out->seq_bucket[s] = seq_b[s];
+    out->seq_replica[s] = seq_rep[s];
+    out->seq_chunk[s] = seq_chunk[s];
+    out->pack_order[s] = pack[s];
+  }
+  for (i64 q = 0; q < total_rep; ++q) out->replica_cost[q] = running[q];
+  out->t_hat = t_hat;
+  out->nodes = bud.used;
+  if (st == LOBRA_ERR_BUDGET) lobra::set_error("Eq. 3 solver node cap hit; incumbent returned");
+  return st;
+}

@@ -1,0 +1,606 @@
+// bf16 kernels of the multi-LoRA hot path for sm_100a (tcgen05 + TMEM + TMA).
+//
+// k_gemm     : C = Z W^T (fwd) or Z W (bwd, W as an MN-major operand) with the LoRA
+//              expand fused into the SAME TMEM accumulator as extra K steps over the
+//              tile's adapter slots ("K-extension"): "the computation of the base
+//              model can be fused into a batched operation whilst ... multiple LoRA
+//              adapters ... customized operations".
+// k_rowproj  : the rank-r shrink H_s = s_t X A_t^T (and the backward G_s = s_t dY B_t),
+//              HBM-bound; one CTA per 128-row tile streams Z once.
+// k_segred   : the token reductions dA_t = X^T G_s and dB_t = dY^T H_s on tensor cores,
+//              Z tiles used as MN-major A operands (one HBM read of Z), deterministic
+//              two-pass (partials + k_finalize in fixed order).
+// See DESIGN.md "Kernels" for layouts and the roofline of each.
+#include <cuda_bf16.h>
+
+#include "lora_internal.h"
+#include "ptx.cuh"
+
+namespace lobra {
+using namespace ptx;
+
+namespace {
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+__device__ __forceinline__ int rpad16(int r) { return (r + 15) & ~15; }
+
+// =====================================================================================
+// GEMM with fused K-extension
+// =====================================================================================
+constexpr int G_BM = 128, G_BN = 256, G_BK = 64, G_STAGES = 4;
+constexpr int G_A_BYTES = G_BM * G_BK * 2;   // 16 KB
+constexpr int G_B_BYTES = G_BN * G_BK * 2;   // 32 KB
+constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;
+constexpr int G_SMEM = G_STAGES * G_STAGE_BYTES + 1024 + 256;
+constexpr int G_THREADS = 256;
+
+struct GemmArgs {
+  int T, N, K, ntm, ntn, accumulate;
+  __nv_bfloat16* C;
+  Meta meta;
+};
+
+template <bool kBMN>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    k_gemm(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW,
+           const __grid_constant__ CUtensorMap mapSlot, const __grid_constant__ CUtensorMap mapV,
+           const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G_STAGES * G_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + G_STAGES * G_B_BYTES);
+  uint64_t* empty = full + G_STAGES;
+  uint64_t* tfull = empty + G_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapZ);
+    tma_prefetch(&mapW);
+    tma_prefetch(&mapSlot);
+    tma_prefetch(&mapV);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < G_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int ntiles = args.ntm * args.ntn;
+  const int nk = (args.K + G_BK - 1) / G_BK;
+  const Meta& meta = args.meta;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m = tile / args.ntn, n = tile % args.ntn;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], G_STAGE_BYTES);
+          tma_load_2d(sA + stage * G_A_BYTES, &mapZ, &full[stage], kb * G_BK, m * G_BM);
+          if (!kBMN) {
+            tma_load_2d(sB + stage * G_B_BYTES, &mapW, &full[stage], kb * G_BK, n * G_BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(sB + stage * G_B_BYTES + c * 8192, &mapW, &full[stage],
+                          n * G_BN + c * 64, kb * G_BK);
+          }
+          if (++stage == G_STAGES) stage = 0, phase ^= 1;
+        }
+        for (int s = meta.tile_slot_off[m]; s < meta.tile_slot_off[m + 1]; ++s) {
+          const int t = meta.slot_task[s];
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], G_STAGE_BYTES);
+          tma_load_2d(sA + stage * G_A_BYTES, &mapSlot, &full[stage], 0, s * kTileM);
+          tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], 0, t * args.N + n * G_BN);
+          if (++stage == G_STAGES) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (single thread)
+      const uint32_t id_main = idesc_bf16(G_BM, G_BN, false, kBMN);
+      const uint32_t id_ext = idesc_bf16(G_BM, G_BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int m = tile / args.ntn;
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * G_BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < G_BK / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
+            mma_bf16(d, ad, bd, id_main, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == G_STAGES) stage = 0, phase ^= 1;
+        }
+        for (int s = meta.tile_slot_off[m]; s < meta.tile_slot_off[m + 1]; ++s) {
+          const int nk16 = rpad16(meta.ranks[meta.slot_task[s]]) / 16;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
+          for (int k = 0; k < nk16; ++k)
+            mma_bf16(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024),
+                     id_ext, 1u);
+          mma_commit(&empty[stage]);
+          if (++stage == G_STAGES) stage = 0, phase ^= 1;
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> bf16 -> global
+    const uint32_t q = warp - 4;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int m = tile / args.ntn, n = tile % args.ntn;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m * G_BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < G_BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((q * 32u) << 16) + acc * G_BN + c * 32, v);
+        const int col0 = n * G_BN + c * 32;
+        if (row < args.T && col0 < args.N) {
+          uint4* dst = reinterpret_cast<uint4*>(args.C + (size_t)row * args.N + col0);
+          if (args.accumulate) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 o = dst[j];
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                v[j * 8 + 2 * e] += f.x;
+                v[j * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 o;
+            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+            dst[j] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// =====================================================================================
+// Row projection (shrink): slot[s][row][q] = s_t * sum_k Z[row][k] V_t[q][k]
+// =====================================================================================
+constexpr int R_STAGES = 4, R_MAXS = 4;
+constexpr int R_A_BYTES = 128 * 64 * 2;         // 16 KB
+constexpr int R_V_BYTES = 64 * 64 * 2;          // 8 KB per slot
+constexpr int R_STAGE_BYTES = R_A_BYTES + R_MAXS * R_V_BYTES;
+constexpr int R_SMEM = R_STAGES * R_STAGE_BYTES + 1024 + 256;
+
+struct RowArgs {
+  int K;
+  __nv_bfloat16* out;
+  Meta meta;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    k_rowproj(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
+              const RowArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + R_STAGES * R_STAGE_BYTES);
+  uint64_t* empty = full + R_STAGES;
+  uint64_t* tfull = empty + R_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+  const int m = blockIdx.x;
+  const int s_begin = meta.tile_slot_off[m], s_end = meta.tile_slot_off[m + 1];
+  const int npass = (s_end - s_begin + R_MAXS - 1) / R_MAXS;
+  const int nk = (args.K + 63) / 64;
+
+  if (warp == 0 && lane == 0) tma_prefetch(&mapZ), tma_prefetch(&mapV);
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < R_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int p = 0; p < npass; ++p) {
+        const int s0 = s_begin + p * R_MAXS;
+        const int ns = min(R_MAXS, s_end - s0);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], R_A_BYTES + ns * R_V_BYTES);
+          uint8_t* st = smem + stage * R_STAGE_BYTES;
+          tma_load_2d(st, &mapZ, &full[stage], kb * 64, m * kTileM);
+          for (int i = 0; i < ns; ++i)
+            tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64,
+                        meta.slot_task[s0 + i] * 64);
+          if (++stage == R_STAGES) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id = idesc_bf16(128, 64, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int p = 0; p < npass; ++p) {
+        const int s0 = s_begin + p * R_MAXS;
+        const int ns = min(R_MAXS, s_end - s0);
+        mbar_wait(tempty, (p & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + stage * R_STAGE_BYTES);
+          for (int i = 0; i < ns; ++i) {
+            const uint32_t b0 = a0 + R_A_BYTES + i * R_V_BYTES;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024),
+                       sdesc_sw128(b0 + k * 32, 16, 1024), id, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == R_STAGES) stage = 0, phase ^= 1;
+        }
+        mma_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;
+    const int lrow = q * 32 + lane;
+    const int row = m * kTileM + lrow;
+    const int my_task = row < meta.T ? row_task(meta, row) : -1;
+    for (int p = 0; p < npass; ++p) {
+      const int s0 = s_begin + p * R_MAXS;
+      const int ns = min(R_MAXS, s_end - s0);
+      mbar_wait(tfull, p & 1);
+      tc_fence_after();
+      for (int i = 0; i < ns; ++i) {
+        const int s = s0 + i;
+        const int ts = meta.slot_task[s];
+        const float sc = (ts == my_task) ? meta.scales[ts] : 0.0f;
+        const int rp = (ts == my_task) ? meta.ranks[ts] : 0;
+        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)s * kTileM + lrow) * kSlotW);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          float v[32];
+          tmem_ld32(tmem + ((q * 32u) << 16) + i * 64 + h * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (h * 32 + j < rp) ? v[j] * sc : 0.0f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 o;
+            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+            dst[h * 4 + j] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// =====================================================================================
+// Segmented token reduction: partial[u][c][q][i] = sum_{slots of unit u} sum_rows
+//      Z[row][c*128 + i] * Slot[row][q]          (Z^T as an MN-major A operand)
+// =====================================================================================
+constexpr int S_STAGES = 4;
+constexpr int S_A_BYTES = 2 * 128 * 64 * 2;  // two 64-col boxes of 128 rows: 32 KB
+constexpr int S_B_BYTES = 128 * 64 * 2;      // one slot: 16 KB
+constexpr int S_STAGE_BYTES = S_A_BYTES + S_B_BYTES;
+constexpr int S_SMEM = S_STAGES * S_STAGE_BYTES + 1024 + 256;
+
+struct SegArgs {
+  int width, nchunks, nitems;
+  float* partial;
+  Meta meta;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    k_segred(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapSlot,
+             const SegArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_STAGES * S_STAGE_BYTES);
+  uint64_t* empty = full + S_STAGES;
+  uint64_t* tfull = empty + S_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+
+  if (warp == 0 && lane == 0) tma_prefetch(&mapZ), tma_prefetch(&mapSlot);
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
+        const int u = item / args.nchunks, c = item % args.nchunks;
+        for (int k = meta.unit_s0[u]; k < meta.unit_s1[u]; ++k) {
+          const int sl = meta.task_slots[k];
+          const int tile = meta.slot_tile[sl];
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], S_STAGE_BYTES);
+          uint8_t* st = smem + stage * S_STAGE_BYTES;
+          tma_load_2d(st, &mapZ, &full[stage], c * 128, tile * kTileM);
+          tma_load_2d(st + 16384, &mapZ, &full[stage], c * 128 + 64, tile * kTileM);
+          tma_load_2d(st + S_A_BYTES, &mapSlot, &full[stage], 0, sl * kTileM);
+          if (++stage == S_STAGES) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id = idesc_bf16(128, 64, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
+        const int u = item / args.nchunks;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 64;
+        bool first = true;
+        for (int k = meta.unit_s0[u]; k < meta.unit_s1[u]; ++k) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + stage * S_STAGE_BYTES);
+          const uint32_t b0 = a0 + S_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_bf16(d, sdesc_sw128(a0 + kk * 2048, 16384, 1024),
+                     sdesc_sw128(b0 + kk * 2048, 8192, 1024), id, first ? 0u : 1u);
+            first = false;
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == S_STAGES) stage = 0, phase ^= 1;
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;
+    int it = 0;
+    for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
+      const int u = item / args.nchunks, c = item % args.nchunks;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int rp = rpad16(meta.ranks[meta.unit_task[u]]);
+      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * 64) * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        if (h * 32 >= rp) break;
+        float v[32];
+        tmem_ld32(tmem + ((q * 32u) << 16) + acc * 64 + h * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (h * 32 + j < rp) dst[(size_t)(h * 32 + j) * 128] = v[j];
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+}
+
+// =====================================================================================
+// small helper kernels
+// =====================================================================================
+__global__ void k_pad(int mode, const __nv_bfloat16* __restrict__ src,
+                      __nv_bfloat16* __restrict__ dst, Meta meta, int in, int out) {
+  // one thread per destination element
+  const long long total = (mode == 0)   ? (long long)meta.ntasks * 64 * in
+                          : (mode == 1) ? (long long)meta.ntasks * out * 64
+                          : (mode == 2) ? (long long)meta.ntasks * 64 * out
+                                        : (long long)meta.ntasks * in * 64;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int t, q;
+    long long o;
+    __nv_bfloat16 v = __float2bfloat16(0.0f);
+    if (mode == 0) {          // Apad[t][q][k] = A[roff+q][k]
+      const long long k = i % in;
+      const long long tq = i / in;
+      t = (int)(tq / 64), q = (int)(tq % 64);
+      if (q < meta.ranks[t]) v = src[(long long)(meta.roff[t] + q) * in + k];
+    } else if (mode == 1) {   // Bpad[t][o][q] = B[o][roff+q]
+      q = (int)(i % 64);
+      const long long to = i / 64;
+      t = (int)(to / out), o = to % out;
+      if (q < meta.ranks[t]) v = src[o * meta.rsum + meta.roff[t] + q];
+    } else if (mode == 2) {   // Btpad[t][q][o] = B[o][roff+q]
+      o = i % out;
+      const long long tq = i / out;
+      t = (int)(tq / 64), q = (int)(tq % 64);
+      if (q < meta.ranks[t]) v = src[o * meta.rsum + meta.roff[t] + q];
+    } else {                  // Atpad[t][k][q] = A[roff+q][k]
+      q = (int)(i % 64);
+      const long long tk = i / 64;
+      t = (int)(tk / in);
+      const long long k = tk % in;
+      if (q < meta.ranks[t]) v = src[(long long)(meta.roff[t] + q) * in + k];
+    }
+    dst[i] = v;
+  }
+}
+
+__global__ void k_finalize(int mode, const float* __restrict__ partial, int width, int nchunks,
+                           Meta meta, float* __restrict__ out, long long ld, int accumulate) {
+  const long long total = (long long)meta.rsum * width;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(i % width);
+    const int rq = (int)(i / width);   // global adapter row roff[t] + q
+    int t = 0;
+    while (meta.roff[t + 1] <= rq) ++t;
+    const int q = rq - meta.roff[t];
+    const int c = col / 128, ci = col % 128;
+    float s = 0.0f;
+    for (int u = meta.task_unit_off[t]; u < meta.task_unit_off[t + 1]; ++u)
+      s += partial[((size_t)(u * nchunks + c) * 64 + q) * 128 + ci];
+    float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
+    *dst = accumulate ? *dst + s : s;
+  }
+}
+
+__global__ void k_zero(float* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = 0.0f;
+}
+
+}  // namespace
+
+// =====================================================================================
+// launchers
+// =====================================================================================
+void launch_pad(int mode, const __nv_bfloat16* src, __nv_bfloat16* dst, const Meta& meta, int in,
+                int out, cudaStream_t st) {
+  k_pad<<<1184, 256, 0, st>>>(mode, src, dst, meta, in, out);
+}
+
+void launch_rowproj(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
+                    __nv_bfloat16* slots, int num_sms, cudaStream_t st) {
+  (void)num_sms;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_rowproj, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
+    init = true;
+  }
+  RowArgs a{K, slots, meta};
+  k_rowproj<<<meta.ntiles, 256, R_SMEM, st>>>(mapZ, mapV, a);
+}
+
+void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
+                 const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
+                 __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms,
+                 cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
+    cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
+    init = true;
+  }
+  GemmArgs a;
+  a.T = T;
+  a.N = N;
+  a.K = K;
+  a.ntm = (T + G_BM - 1) / G_BM;
+  a.ntn = (N + G_BN - 1) / G_BN;
+  a.accumulate = accumulate;
+  a.C = C;
+  a.meta = meta;
+  const int tiles = a.ntm * a.ntn;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  if (b_mn)
+    k_gemm<true><<<grid, G_THREADS, G_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+  else
+    k_gemm<false><<<grid, G_THREADS, G_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+}
+
+void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
+                   const Meta& meta, float* partial, int num_sms, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_segred, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+    init = true;
+  }
+  SegArgs a;
+  a.width = width;
+  a.nchunks = (width + 127) / 128;
+  a.nitems = meta.nunits * a.nchunks;
+  a.partial = partial;
+  a.meta = meta;
+  if (a.nitems == 0) return;
+  const int grid = a.nitems < num_sms ? a.nitems : num_sms;
+  k_segred<<<grid, 256, S_SMEM, st>>>(mapZ, mapSlot, a);
+}
+
+void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
+                     long long ld, int accumulate, cudaStream_t st) {
+  k_finalize<<<592, 256, 0, st>>>(mode, partial, width, (width + 127) / 128, meta, out, ld,
+                                  accumulate);
+}
+
+void launch_zero_f32(float* p, long long n, cudaStream_t st) {
+  if (n > 0) k_zero<<<296, 256, 0, st>>>(p, n);
+}
+
+}  // namespace lobra

@@ -1,0 +1,510 @@
+// Host side of lobra_lora_fwd / lobra_lora_bwd: argument validation, batch metadata
+// (segments, per-tile adapter slots, reduction units), workspace layout, TMA tensor maps,
+// and the launch sequence.  See include/lobra.h for the contract.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "lora_internal.h"
+
+namespace lobra {
+
+// ------------------------------------------------------------------ errors / version
+static thread_local std::string g_err;
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+void clear_error() { g_err.clear(); }
+
+// comm.cpp
+lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
+lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st);
+
+// ------------------------------------------------------------------ per-device context
+namespace {
+
+constexpr int kRing = 8;
+
+struct DevCtx {
+  int dev = -1, num_sms = 0, cc_major = 0, cc_minor = 0;
+  std::vector<uint8_t*> pinned;
+  std::vector<size_t> pinned_bytes;
+  std::vector<cudaEvent_t> ev;
+  int next = 0;
+  std::mutex mu;
+};
+
+std::mutex g_ctx_mu;
+std::vector<DevCtx*> g_ctx;
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+lobra_status get_ctx(DevCtx** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(LOBRA_ERR_CUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1, nullptr);
+  if (!g_ctx[dev]) {
+    DevCtx* c = new DevCtx();
+    c->dev = dev;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&c->cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&c->cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    c->pinned.assign(kRing, nullptr);
+    c->pinned_bytes.assign(kRing, 0);
+    c->ev.assign(kRing, nullptr);
+    for (int i = 0; i < kRing; ++i)
+      if (cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(LOBRA_ERR_CUDA, "cudaEventCreate failed");
+    g_ctx[dev] = c;
+  }
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(LOBRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  *out = g_ctx[dev];
+  if (g_ctx[dev]->cc_major != 10 || g_ctx[dev]->cc_minor != 0)
+    return fail(LOBRA_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                dev, g_ctx[dev]->cc_major, g_ctx[dev]->cc_minor);
+  return LOBRA_OK;
+}
+
+// Copies `bytes` of host data to device `dst` on `st` through a pinned staging ring.
+lobra_status upload(DevCtx* c, const void* src, size_t bytes, void* dst, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int k = c->next;
+  c->next = (k + 1) % kRing;
+  if (cudaEventSynchronize(c->ev[k]) != cudaSuccess) return fail(LOBRA_ERR_CUDA, "event sync");
+  if (c->pinned_bytes[k] < bytes) {
+    if (c->pinned[k]) cudaFreeHost(c->pinned[k]);
+    size_t sz = std::max<size_t>(bytes, 1 << 16);
+    if (cudaMallocHost(reinterpret_cast<void**>(&c->pinned[k]), sz) != cudaSuccess)
+      return fail(LOBRA_ERR_CUDA, "cudaMallocHost(%zu) failed", sz);
+    c->pinned_bytes[k] = sz;
+  }
+  std::memcpy(c->pinned[k], src, bytes);
+  if (cudaMemcpyAsync(dst, c->pinned[k], bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(LOBRA_ERR_CUDA, "cudaMemcpyAsync H2D failed");
+  if (cudaEventRecord(c->ev[k], st) != cudaSuccess) return fail(LOBRA_ERR_CUDA, "event record");
+  return LOBRA_OK;
+}
+
+// ------------------------------------------------------------------ batch plan
+struct Plan {
+  int T = 0, ntasks = 0, rsum = 0;
+  std::vector<int32_t> buf;  // serialized int32 metadata (floats bit-cast)
+  // offsets (in int32 words) of each array inside buf
+  int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
+      o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_scales;
+  int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+lobra_status validate(const lobra_problem* prob, const lobra_batch* b, const lobra_adapters* ad) {
+  if (!prob || !b || !ad) return fail(LOBRA_ERR_INPUT, "null problem/batch/adapters");
+  if (prob->dtype != LOBRA_BF16 && prob->dtype != LOBRA_FP32)
+    return fail(LOBRA_ERR_INPUT, "unknown dtype %d", (int)prob->dtype);
+  if (prob->in < 1 || prob->out < 1) return fail(LOBRA_ERR_INPUT, "in/out must be positive");
+  if (prob->dtype == LOBRA_BF16 && (prob->in % 64 || prob->out % 64))
+    return fail(LOBRA_ERR_INPUT, "bf16 path needs in and out multiples of 64 (got %lld, %lld)",
+                (long long)prob->in, (long long)prob->out);
+  if (prob->in > (1 << 30) || prob->out > (1 << 30)) return fail(LOBRA_ERR_INPUT, "in/out too large");
+  if (prob->tp_kind != LOBRA_TP_NONE && prob->tp_kind != LOBRA_TP_COLUMN &&
+      prob->tp_kind != LOBRA_TP_ROW)
+    return fail(LOBRA_ERR_INPUT, "unknown tp_kind");
+  if (prob->dA_ld != 0 && prob->dA_ld < prob->in) return fail(LOBRA_ERR_INPUT, "dA_ld < in");
+  if (b->num_seqs < 1 || !b->seq_lens || !b->seq_task)
+    return fail(LOBRA_ERR_INPUT, "batch needs num_seqs >= 1 and host seq_lens/seq_task");
+  if (ad->num_tasks < 1 || !ad->ranks || !ad->scales)
+    return fail(LOBRA_ERR_INPUT, "adapters need num_tasks >= 1 and host ranks/scales");
+  if (!ad->A || !ad->B) return fail(LOBRA_ERR_INPUT, "adapter A/B device pointers missing");
+  for (int t = 0; t < ad->num_tasks; ++t)
+    if (ad->ranks[t] < 1 || ad->ranks[t] > 64)
+      return fail(LOBRA_ERR_INPUT, "task %d rank %d outside [1, 64]", t, ad->ranks[t]);
+  long long T = 0;
+  for (int k = 0; k < b->num_seqs; ++k) {
+    if (b->seq_lens[k] < 0) return fail(LOBRA_ERR_INPUT, "sequence %d has negative length", k);
+    if (b->seq_task[k] < 0 || b->seq_task[k] >= ad->num_tasks)
+      return fail(LOBRA_ERR_INPUT, "sequence %d task id %d out of range [0, %d)", k,
+                  b->seq_task[k], ad->num_tasks);
+    T += b->seq_lens[k];
+  }
+  if (T > (1LL << 30)) return fail(LOBRA_ERR_INPUT, "too many tokens");
+  return LOBRA_OK;
+}
+
+void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int num_sms,
+                Plan& P) {
+  const int n = b->num_seqs, G = ad->num_tasks;
+  P.ntasks = G;
+  std::vector<int> seg_off{0}, seg_task;
+  int T = 0;
+  for (int k = 0; k < n; ++k) {
+    const int L = b->seq_lens[k], t = b->seq_task[k];
+    if (L == 0) continue;
+    if (!seg_task.empty() && seg_task.back() == t) {
+      seg_off.back() += L;
+    } else {
+      seg_task.push_back(t);
+      seg_off.push_back(seg_off.back() + L);
+    }
+    T += L;
+  }
+  P.T = T;
+  P.nseg = (int)seg_task.size();
+  P.ntiles = (T + kTileM - 1) / kTileM;
+  // slots: per tile, tasks in order of first appearance
+  std::vector<int> tile_slot_off{0}, slot_task, slot_tile;
+  int sg = 0;
+  for (int m = 0; m < P.ntiles; ++m) {
+    const int r0 = m * kTileM, r1 = std::min(T, r0 + kTileM);
+    while (seg_off[sg + 1] <= r0) ++sg;
+    std::vector<int> seen;
+    for (int s = sg; s < P.nseg && seg_off[s] < r1; ++s)
+      if (std::find(seen.begin(), seen.end(), seg_task[s]) == seen.end()) seen.push_back(seg_task[s]);
+    for (int t : seen) slot_task.push_back(t), slot_tile.push_back(m);
+    tile_slot_off.push_back((int)slot_task.size());
+    P.max_slots = std::max(P.max_slots, (int)seen.size());
+  }
+  P.nslots = (int)slot_task.size();
+  std::vector<int> task_slot_off(G + 1, 0), task_slots;
+  for (int t = 0; t < G; ++t) {
+    for (int s = 0; s < P.nslots; ++s)
+      if (slot_task[s] == t) task_slots.push_back(s);
+    task_slot_off[t + 1] = (int)task_slots.size();
+  }
+  // reduction units: split each task's slot list so that units x chunks ~ 2 waves
+  const int nchunks = std::max(1, (width_hint + 127) / 128);
+  const long long target = 2LL * std::max(num_sms, 1);
+  int per = (int)std::max<long long>(1, ((long long)P.nslots * nchunks + target - 1) / target);
+  std::vector<int> unit_task, unit_s0, unit_s1, task_unit_off(G + 1, 0);
+  for (int t = 0; t < G; ++t) {
+    for (int s = task_slot_off[t]; s < task_slot_off[t + 1]; s += per) {
+      unit_task.push_back(t);
+      unit_s0.push_back(s);
+      unit_s1.push_back(std::min(task_slot_off[t + 1], s + per));
+    }
+    task_unit_off[t + 1] = (int)unit_task.size();
+  }
+  P.nunits = (int)unit_task.size();
+  std::vector<int> roff(G + 1, 0);
+  for (int t = 0; t < G; ++t) roff[t + 1] = roff[t] + ad->ranks[t];
+  P.rsum = roff[G];
+  // serialize
+  P.buf.clear();
+  auto put = [&](const std::vector<int>& v) {
+    const int o = (int)P.buf.size();
+    P.buf.insert(P.buf.end(), v.begin(), v.end());
+    while (P.buf.size() % 4) P.buf.push_back(0);   // 16-byte alignment of every array
+    return o;
+  };
+  P.o_seg_off = put(seg_off);
+  P.o_seg_task = put(seg_task);
+  P.o_tile_slot_off = put(tile_slot_off);
+  P.o_slot_task = put(slot_task);
+  P.o_slot_tile = put(slot_tile);
+  P.o_task_slot_off = put(task_slot_off);
+  P.o_task_slots = put(task_slots);
+  P.o_unit_task = put(unit_task);
+  P.o_unit_s0 = put(unit_s0);
+  P.o_unit_s1 = put(unit_s1);
+  P.o_task_unit_off = put(task_unit_off);
+  P.o_ranks = put(std::vector<int>(ad->ranks, ad->ranks + G));
+  P.o_roff = put(roff);
+  std::vector<int> sc(G);
+  std::memcpy(sc.data(), ad->scales, sizeof(float) * G);
+  P.o_scales = put(sc);
+}
+
+Meta device_meta(const Plan& P, const void* dev_base) {
+  const int32_t* d = reinterpret_cast<const int32_t*>(dev_base);
+  Meta m;
+  m.T = P.T;
+  m.nseg = P.nseg;
+  m.ntiles = P.ntiles;
+  m.nslots = P.nslots;
+  m.ntasks = P.ntasks;
+  m.nunits = P.nunits;
+  m.rsum = P.rsum;
+  m.max_slots_per_tile = P.max_slots;
+  m.seg_off = d + P.o_seg_off;
+  m.seg_task = d + P.o_seg_task;
+  m.tile_slot_off = d + P.o_tile_slot_off;
+  m.slot_task = d + P.o_slot_task;
+  m.slot_tile = d + P.o_slot_tile;
+  m.task_slot_off = d + P.o_task_slot_off;
+  m.task_slots = d + P.o_task_slots;
+  m.unit_task = d + P.o_unit_task;
+  m.unit_s0 = d + P.o_unit_s0;
+  m.unit_s1 = d + P.o_unit_s1;
+  m.task_unit_off = d + P.o_task_unit_off;
+  m.ranks = d + P.o_ranks;
+  m.roff = d + P.o_roff;
+  m.scales = reinterpret_cast<const float*>(d + P.o_scales);
+  return m;
+}
+
+// Workspace layout (bytes from ws base); both directions share it.
+struct Layout {
+  size_t meta = 0, pad1 = 0, pad2 = 0, gslots = 0, partA = 0, partB = 0, total = 0;
+  size_t saved = 0;
+};
+
+Layout layout(const lobra_problem* prob, const Plan& P) {
+  Layout L;
+  const size_t in = prob->in, out = prob->out, G = P.ntasks;
+  size_t off = 0;
+  L.meta = off;
+  off += align256(P.buf.size() * 4);
+  if (prob->dtype == LOBRA_BF16) {
+    const size_t es = 2;
+    const size_t p1 = std::max(G * 64 * in, G * 64 * out) * es;   // Apad / Btpad
+    const size_t p2 = std::max(G * out * 64, G * in * 64) * es;   // Bpad / Atpad
+    L.pad1 = off;
+    off += align256(p1);
+    L.pad2 = off;
+    off += align256(p2);
+    L.gslots = off;
+    off += align256((size_t)P.nslots * kTileM * kSlotW * es);
+    const size_t chA = (in + 127) / 128, chB = (out + 127) / 128;
+    L.partA = off;
+    off += align256((size_t)P.nunits * chA * 64 * 128 * 4);
+    L.partB = off;
+    off += align256((size_t)P.nunits * chB * 64 * 128 * 4);
+    L.saved = (size_t)P.nslots * kTileM * kSlotW * es;
+  } else {
+    L.gslots = off;
+    off += align256((size_t)P.T * kSlotW * 4);
+    L.saved = (size_t)P.T * kSlotW * 4;
+  }
+  L.total = off;
+  return L;
+}
+
+lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+                      uint32_t box_inner, uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(LOBRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=%llu x %llu box=%u x %u",
+                (int)r, (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
+  return LOBRA_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+lobra_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LOBRA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return LOBRA_OK;
+}
+
+lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobra_adapters* ad,
+                     int width_hint, int num_sms, Plan& P, Layout& L) {
+  lobra_status st = validate(prob, b, ad);
+  if (st != LOBRA_OK) return st;
+  build_plan(b, ad, width_hint, num_sms, P);
+  L = layout(prob, P);
+  return LOBRA_OK;
+}
+
+}  // namespace
+}  // namespace lobra
+
+using namespace lobra;
+
+extern "C" const char* lobra_last_error(void) { return lobra::g_err.c_str(); }
+extern "C" const char* lobra_version(void) { return "lobra-b200 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }
+
+extern "C" size_t lobra_lora_workspace_bytes(const lobra_problem* prob, const lobra_batch* batch,
+                                             const lobra_adapters* ad) {
+  clear_error();
+  Plan P;
+  Layout L;
+  // the unit split depends on the SM count; size for the worst case (1 slot per unit)
+  if (prepare(prob, batch, ad, 128, 1 << 20, P, L) != LOBRA_OK) return 0;
+  return L.total;
+}
+
+extern "C" size_t lobra_lora_saved_bytes(const lobra_problem* prob, const lobra_batch* batch,
+                                         const lobra_adapters* ad) {
+  clear_error();
+  Plan P;
+  Layout L;
+  if (prepare(prob, batch, ad, 128, 1 << 20, P, L) != LOBRA_OK) return 0;
+  return std::max<size_t>(L.saved, 256);
+}
+
+extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_batch* batch,
+                                       const lobra_adapters* ad, const void* X, const void* W,
+                                       void* Y, void* Hs, void* ws, size_t ws_bytes,
+                                       lobra_stream_t stream_) {
+  clear_error();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  DevCtx* ctx = nullptr;
+  Plan P;
+  Layout L;
+  lobra_status s = prepare(prob, batch, ad, (int)prob->in, 1 << 20, P, L);
+  if (s != LOBRA_OK) return s;
+  if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
+  if (!X || !W || !Y || !Hs || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");
+  if (ws_bytes < L.total) return fail(LOBRA_ERR_INPUT, "workspace too small: %zu < %zu", ws_bytes, L.total);
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) || !aligned16(X) || !aligned16(W) || !aligned16(Y) ||
+      !aligned16(Hs) || !aligned16(ad->A) || !aligned16(ad->B))
+    return fail(LOBRA_ERR_INPUT, "device pointers must be 16-byte aligned (ws 256-byte)");
+  if (prob->tp_kind == LOBRA_TP_ROW && prob->tp == nullptr)
+    return fail(LOBRA_ERR_INPUT, "row-parallel problem without a comm");
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  if (P.T == 0) return LOBRA_OK;
+  // the unit split only matters for the backward; metadata identical otherwise
+  if ((s = upload(ctx, P.buf.data(), P.buf.size() * 4, w + L.meta, st)) != LOBRA_OK) return s;
+  const Meta meta = device_meta(P, w + L.meta);
+  const int in = (int)prob->in, out = (int)prob->out;
+  if (prob->dtype == LOBRA_FP32) {
+    launch_f32_rowproj(0, static_cast<const float*>(X), static_cast<const float*>(ad->A),
+                       static_cast<const float*>(ad->B), in, out, meta, static_cast<float*>(Hs), st);
+    launch_f32_gemm(0, static_cast<const float*>(X), static_cast<const float*>(W),
+                    static_cast<const float*>(ad->A), static_cast<const float*>(ad->B),
+                    static_cast<const float*>(Hs), in, out, meta, static_cast<float*>(Y), 0, st);
+  } else {
+    auto* Apad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
+    auto* Bpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
+    launch_pad(0, static_cast<const __nv_bfloat16*>(ad->A), Apad, meta, in, out, st);
+    launch_pad(1, static_cast<const __nv_bfloat16*>(ad->B), Bpad, meta, in, out, st);
+    CUtensorMap mX, mApad, mW, mSlot, mBpad;
+    if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mApad, Apad, in, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mW, W, in, out, 64, 256)) != LOBRA_OK) return s;
+    if ((s = make_map(&mSlot, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mBpad, Bpad, 64, (uint64_t)P.ntasks * out, 64, 256)) != LOBRA_OK) return s;
+    launch_rowproj(mX, mApad, in, meta, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st);
+    launch_gemm(false, mX, mW, mSlot, mBpad, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
+                ctx->num_sms, st);
+  }
+  if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
+  if (prob->tp_kind == LOBRA_TP_ROW) {
+    const size_t cnt = (size_t)P.T * out;
+    return prob->dtype == LOBRA_BF16 ? comm_tp_allreduce_bf16(prob->tp, Y, cnt, st)
+                                     : comm_tp_allreduce_f32(prob->tp, static_cast<float*>(Y), cnt, st);
+  }
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_batch* batch,
+                                       const lobra_adapters* ad, const void* X, const void* W,
+                                       const void* Hs, const void* dY, void* dX, int accumulate_dx,
+                                       float* dA, float* dB, int accumulate_dadb, void* ws,
+                                       size_t ws_bytes, lobra_stream_t stream_) {
+  clear_error();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  DevCtx* ctx = nullptr;
+  lobra_status s = validate(prob, batch, ad);
+  if (s != LOBRA_OK) return s;
+  if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
+  Plan P;
+  Layout L;
+  // units sized for the wider of the two reductions (dA over `in`, dB over `out`)
+  if ((s = prepare(prob, batch, ad, (int)std::min(prob->in, prob->out), ctx->num_sms, P, L)) != LOBRA_OK)
+    return s;
+  if (!X || !W || !Hs || !dY || !dX || !dA || !dB || !ws)
+    return fail(LOBRA_ERR_INPUT, "null device pointer");
+  if (ws_bytes < L.total)
+    return fail(LOBRA_ERR_INPUT, "workspace too small: %zu < %zu", ws_bytes, L.total);
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) || !aligned16(X) || !aligned16(W) || !aligned16(Hs) ||
+      !aligned16(dY) || !aligned16(dX) || !aligned16(ad->A) || !aligned16(ad->B) || !aligned16(dA) ||
+      !aligned16(dB))
+    return fail(LOBRA_ERR_INPUT, "device pointers must be 16-byte aligned (ws 256-byte)");
+  if (prob->tp_kind == LOBRA_TP_COLUMN && prob->tp == nullptr)
+    return fail(LOBRA_ERR_INPUT, "column-parallel problem without a comm");
+  const int in = (int)prob->in, out = (int)prob->out;
+  const long long ldA = prob->dA_ld ? prob->dA_ld : prob->in;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  if (P.T == 0) {
+    // no tokens: dX untouched (nothing to write), gradients zero unless accumulating
+    if (!accumulate_dadb) {
+      for (int r = 0; r < P.rsum; ++r) cudaMemsetAsync(dA + (size_t)r * ldA, 0, sizeof(float) * in, st);
+      cudaMemsetAsync(dB, 0, sizeof(float) * (size_t)out * P.rsum, st);
+    }
+    return check_launch("lobra_lora_bwd(empty)");
+  }
+  if ((s = upload(ctx, P.buf.data(), P.buf.size() * 4, w + L.meta, st)) != LOBRA_OK) return s;
+  const Meta meta = device_meta(P, w + L.meta);
+  if (prob->dtype == LOBRA_FP32) {
+    float* G = reinterpret_cast<float*>(w + L.gslots);
+    const float* Af = static_cast<const float*>(ad->A);
+    const float* Bf = static_cast<const float*>(ad->B);
+    launch_f32_rowproj(1, static_cast<const float*>(dY), Af, Bf, in, out, meta, G, st);
+    launch_f32_gemm(1, static_cast<const float*>(dY), static_cast<const float*>(W), Af, Bf, G, in,
+                    out, meta, static_cast<float*>(dX), accumulate_dx, st);
+    launch_f32_segred(0, static_cast<const float*>(X), G, in, meta, dA, ldA, accumulate_dadb, st);
+    launch_f32_segred(1, static_cast<const float*>(dY), static_cast<const float*>(Hs), out, meta,
+                      dB, 0, accumulate_dadb, st);
+  } else {
+    auto* Btpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
+    auto* Atpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
+    auto* Gs = reinterpret_cast<__nv_bfloat16*>(w + L.gslots);
+    float* partA = reinterpret_cast<float*>(w + L.partA);
+    float* partB = reinterpret_cast<float*>(w + L.partB);
+    launch_pad(2, static_cast<const __nv_bfloat16*>(ad->B), Btpad, meta, in, out, st);
+    launch_pad(3, static_cast<const __nv_bfloat16*>(ad->A), Atpad, meta, in, out, st);
+    CUtensorMap mdY, mBt, mWmn, mG, mAt, mX, mHs;
+    if ((s = make_map(&mdY, dY, out, P.T, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mBt, Btpad, out, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mWmn, W, in, out, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mG, Gs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mAt, Atpad, 64, (uint64_t)P.ntasks * in, 64, 256)) != LOBRA_OK) return s;
+    if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mHs, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
+    launch_rowproj(mdY, mBt, out, meta, Gs, ctx->num_sms, st);
+    launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
+                accumulate_dx, meta, ctx->num_sms, st);
+    launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st);
+    launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st);
+    launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st);
+    launch_finalize(1, partB, out, meta, dB, 0, accumulate_dadb, st);
+  }
+  if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
+  if (prob->tp_kind == LOBRA_TP_COLUMN) {
+    const size_t cnt = (size_t)P.T * in;
+    return prob->dtype == LOBRA_BF16 ? comm_tp_allreduce_bf16(prob->tp, dX, cnt, st)
+                                     : comm_tp_allreduce_f32(prob->tp, static_cast<float*>(dX), cnt, st);
+  }
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  for (DevCtx* c : g_ctx) {
+    if (!c) continue;
+    for (int i = 0; i < kRing; ++i) {
+      if (c->ev[i]) cudaEventSynchronize(c->ev[i]), cudaEventDestroy(c->ev[i]);
+      if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
+    }
+    delete c;
+  }
+  g_ctx.clear();
+  return LOBRA_OK;
+}

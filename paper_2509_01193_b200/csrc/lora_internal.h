@@ -1,0 +1,89 @@
+// Internal (non-ABI) declarations shared by the host planner and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lobra {
+
+constexpr int kTileM = 128;     // rows (tokens) per M tile == rows per adapter "slot"
+constexpr int kSlotW = 64;      // slot width: ranks padded to 64 columns (r_t <= 64)
+
+// Batch metadata resident in the workspace (int32 unless noted).  Built on the host
+// from (seq_lens, seq_task, ranks) and copied once per call.
+//   segments: maximal runs of equal task in packing order, rows [seg_off[i], seg_off[i+1])
+//   slots:    one per (M tile, task present in the tile), tile-major; slot s holds the
+//             128 x 64 block of H_s (or G_s) rows of that tile for that task, zeros in the
+//             rows of other tasks (the block-stacked K-extension layout)
+//   units:    split of each task's slot list into contiguous ranges for the token
+//             reductions dA/dB (deterministic two-pass reduction)
+struct Meta {
+  int T, nseg, ntiles, nslots, ntasks, nunits, rsum, max_slots_per_tile;
+  const int* seg_off;        // [nseg+1]
+  const int* seg_task;       // [nseg]
+  const int* tile_slot_off;  // [ntiles+1]
+  const int* slot_task;      // [nslots]
+  const int* slot_tile;      // [nslots]
+  const int* task_slot_off;  // [ntasks+1]
+  const int* task_slots;     // [nslots]
+  const int* unit_task;      // [nunits]
+  const int* unit_s0;        // [nunits] range into task_slots
+  const int* unit_s1;        // [nunits]
+  const int* task_unit_off;  // [ntasks+1]
+  const int* ranks;          // [ntasks]
+  const int* roff;           // [ntasks+1]
+  const float* scales;       // [ntasks]
+};
+
+__device__ __forceinline__ int row_task(const Meta& m, int row) {
+  int lo = 0, hi = m.nseg - 1;
+  while (lo < hi) {  // last segment with seg_off <= row
+    const int mid = (lo + hi + 1) >> 1;
+    if (m.seg_off[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return m.seg_task[lo];
+}
+
+// ---- bf16 launchers (kernels_bf16.cu) ---------------------------------------------
+// Pads the adapters into the K-major operand copies the tcgen05 kernels consume.
+//  mode 0: Apad [ntasks*64, in]  (row q of task t = A_t[q,:], zeros for q >= r_t)
+//  mode 1: Bpad [ntasks*out, 64] (Bpad[t][o][q] = B_t[o,q])
+//  mode 2: Btpad[ntasks*64, out] (Btpad[t][q][o] = B_t[o,q])
+//  mode 3: Atpad[ntasks*in, 64]  (Atpad[t][k][q] = A_t[q,k])
+void launch_pad(int mode, const __nv_bfloat16* src, __nv_bfloat16* dst, const Meta& meta,
+                int in, int out, cudaStream_t st);
+// H[slot] = s_t * Z[rows of tile] V_t^T for every slot of every tile (zeros in rows of
+// other tasks).  Z [T, K] bf16 (tensor map), V [ntasks*64, K] bf16 K-major (tensor map).
+void launch_rowproj(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
+                    __nv_bfloat16* slots, int num_sms, cudaStream_t st);
+// C[T, N] (+)= Z[T,K] . Wop  +  sum over tile slots: Slot[128,64] . Vext_t[N-tile, 64]^T
+//   b_mn = false: Wop = W^T with W [N, K] K-major (forward, X W^T)
+//   b_mn = true : Wop = W   with W [K, N] (MN-major B operand; backward, dY W)
+void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
+                 const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
+                 __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st);
+// partial[u][chunk][q][128] = sum over the unit's slots: Z[tile rows, chunk cols]^T Slot
+void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
+                   const Meta& meta, float* partial, int num_sms, cudaStream_t st);
+// out = (accumulate ? out : 0) + sum_u partial   (fixed order). mode 0: dA [r, width] rows
+// with stride ld; mode 1: dB [width, rsum] (PEFT layout, row stride rsum).
+void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
+                     long long ld, int accumulate, cudaStream_t st);
+// Zero (or leave) the dA/dB of every task when the batch has no tokens.
+void launch_zero_f32(float* p, long long n, cudaStream_t st);
+
+// ---- fp32 SIMT launchers (kernels_fp32.cu) ----------------------------------------
+// fwd (dir 0): H [T,64] = s_t X A_t^T;   bwd (dir 1): G [T,64] = s_t dY B_t
+void launch_f32_rowproj(int dir, const float* Z, const float* A, const float* B, int in, int out,
+                        const Meta& meta, float* H, cudaStream_t st);
+// fwd: Y = X W^T + H B_t^T ; bwd: dX (+)= dY W + G A_t
+void launch_f32_gemm(int dir, const float* Z, const float* W, const float* A, const float* B,
+                     const float* H, int in, int out, const Meta& meta, float* C, int accumulate,
+                     cudaStream_t st);
+// dA_t (dir 0) = sum G^T X  (rows stride ld) ; dB_t (dir 1) = sum dY^T H
+void launch_f32_segred(int dir, const float* Z, const float* H, int width, const Meta& meta,
+                       float* out, long long ld, int accumulate, cudaStream_t st);
+
+}  // namespace lobra

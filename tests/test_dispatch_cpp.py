@@ -1,0 +1,126 @@
+"""C++ lobra_dispatch vs the integer oracle: bit-exact on every output (CPU only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dispatch as D
+from workloads import synth
+
+pytestmark = []
+
+
+def _run_both(groups, cost, lens, tasks, step, gmax, R, mode=0, cap=200000):
+    from paper_2509_01193_b200 import _lib
+    ref = D.dispatch(groups, cost, lens, tasks, step, gmax, R, mode=mode, bruteforce_cap=cap)
+    got = _lib.lobra_dispatch([g.tp for g in groups], [g.replicas for g in groups],
+                              [g.max_tokens for g in groups], cost, lens, tasks, step, gmax, R, mode)
+    assert got["status"] == 0
+    assert got["boundaries"].tolist() == ref.boundaries
+    assert np.array_equal(got["d"], ref.d), (got["d"], ref.d)
+    assert got["t_hat"] == ref.t_hat
+    assert np.array_equal(got["seq_bucket"], ref.seq_bucket)
+    assert np.array_equal(got["seq_replica"], ref.seq_replica)
+    assert np.array_equal(got["seq_chunk"], ref.seq_chunk)
+    assert np.array_equal(got["pack_order"], ref.pack_order)
+    assert np.array_equal(got["replica_cost"][:len(ref.replica_cost)], ref.replica_cost)
+    return got, ref
+
+
+def _cost_table(groups, U, step, rng=None, a1=1.0, a2=0.0, unit=1.0):
+    """Integer per-sequence costs ~ (a1 s + a2 s^2) / tp-efficiency (App. D shape)."""
+    out = []
+    for g in groups:
+        eff = g.tp * (0.85 ** np.log2(g.tp))
+        row = []
+        for k in range(U):
+            s = (k + 1) * step
+            row.append(max(1, int(round((a1 * s + a2 * s * s) / eff / unit))))
+        out.append(row)
+    return out
+
+
+def test_spec_examples_cpp():
+    _run_both([D.Group(1, 1, 8)], [[4, 8]], [4] * 5, [0] * 5, 4, 8, 1)
+    _run_both([D.Group(1, 2, 8)], [[4, 8]], [4] * 5, [0] * 5, 4, 8, 1)
+
+
+def test_design_anatomy_cpp():
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                    "dispatch_spec_examples.json")))["design_anatomy"]
+    bl = [256, 512, 768, 1024]
+    lens = sum(([b] * n for b, n in zip(bl, g["B"])), [])
+    groups = [D.Group(n, p, bl[r - 1]) for n, p, r in zip(g["n"], g["p"], g["r"])]
+    cost = [[int(100 * (k + 1) * (k + 2) / (1 + 0.8 * np.log2(n))) for k in range(4)] for n in g["n"]]
+    got, ref = _run_both(groups, cost, lens, [0] * len(lens), 256, 1024, 4)
+    _run_both(groups, cost, lens, [0] * len(lens), 256, 1024, 4, mode=1)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_small_bruteforce(seed):
+    rng = np.random.default_rng(100 + seed)
+    G = int(rng.integers(1, 4))
+    groups = []
+    for i in range(G):
+        groups.append(D.Group(2 ** i, int(rng.integers(1, 3)), 256 * (i + 1) * 2))
+    n = int(rng.integers(1, 9))
+    gmax = groups[-1].max_tokens
+    lens = rng.integers(1, gmax + 1, size=n)
+    tasks = rng.integers(0, 3, size=n)
+    U = gmax // 256
+    cost = [[int(x) for x in rng.integers(1, 30, size=U)] for _ in groups]
+    _run_both(groups, cost, lens, tasks, 256, gmax, int(rng.integers(1, 5)))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_two_groups_milp_scale(seed):
+    """G=2 (TP1 x p1 + TP2 x p2) on skewed multi-task batches: C++ exact DP == oracle
+    HiGHS + lexicographic canonicalisation."""
+    rng = np.random.default_rng(200 + seed)
+    groups = [D.Group(1, int(rng.integers(1, 5)), 2048), D.Group(2, int(rng.integers(1, 3)), 4096)]
+    tasks = synth.c2_tasks()
+    wl = synth.sample_batch(tasks, seed=300 + seed, l_max=4096, per_task=[12, 8, 8, 4])
+    cost = _cost_table(groups, 4096 // 256, 256, a1=1.0, a2=1.0 / 8192, unit=64)
+    _run_both(groups, cost, wl.seq_lens, wl.seq_task, 256, 4096, 6, cap=2000)
+
+
+def test_three_groups_cpp():
+    rng = np.random.default_rng(7)
+    groups = [D.Group(1, 2, 1024), D.Group(2, 1, 2048), D.Group(4, 1, 4096)]
+    lens = rng.integers(1, 4096, size=14)
+    tasks = rng.integers(0, 4, size=14)
+    cost = _cost_table(groups, 16, 256, a1=1.0, unit=128)
+    _run_both(groups, cost, lens, tasks, 256, 4096, 4, cap=2000)
+
+
+def test_errors_cpp():
+    from paper_2509_01193_b200 import _lib
+    with pytest.raises(_lib.LobraError) as e:
+        _lib.lobra_dispatch([1], [1], [512], [[1, 2]], [600], [0], 256, 512, 2)
+    assert e.value.status == _lib.LOBRA_ERR_INFEASIBLE
+    with pytest.raises(_lib.LobraError) as e:   # sequence longer than every replica limit
+        _lib.lobra_dispatch([1], [1], [256], [[1, 2]], [300], [0], 256, 512, 2)
+    assert e.value.status == _lib.LOBRA_ERR_INFEASIBLE
+    with pytest.raises(_lib.LobraError) as e:   # groups out of (tp, M) order
+        _lib.lobra_dispatch([2, 1], [1, 1], [512, 512], [[1, 2], [1, 2]], [100], [0], 256, 512, 2)
+    assert e.value.status == _lib.LOBRA_ERR_INPUT
+
+
+def test_c5_scale_runs_fast():
+    """C5-like step: 4xTP1 (M=8192) + 2xTP2 (M=16384), 16 tasks' batch (~1950 seqs),
+    R=16 -- exact, canonical, and well under a second (P:586 'fully overlapped')."""
+    import time
+    from paper_2509_01193_b200 import _lib
+    tasks = synth.c3_tasks()
+    wl = synth.sample_batch(tasks, seed=100, l_max=16384, per_task=[t.batch_size for t in tasks[:12]] + [64] * 4)
+    groups = [D.Group(1, 4, 8192), D.Group(2, 2, 16384)]
+    cost = _cost_table(groups, 64, 256, a1=1.0, a2=1.0 / 16384, unit=32)
+    t0 = time.time()
+    got = _lib.lobra_dispatch([1, 2], [4, 2], [8192, 16384], cost, wl.seq_lens, wl.seq_task, 256, 16384, 16)
+    dt = time.time() - t0
+    assert got["status"] == 0 and dt < 5.0
+    assert got["d"].sum() == len(wl.seq_lens)
+    # sequences longer than 8192 never reach a TP1 replica
+    long = wl.seq_lens > 8192
+    assert (got["seq_replica"][long] >= 4).all()

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle (run under gpurun).
+
+Tolerances (BASELINE.json north_star): bf16 inputs with fp32 accumulation, max relative
+error 2e-2; fp32 path 1e-5.  Error metric per output tensor (reading Q9):
+max|gpu - oracle| / max|oracle|; dA_t and dB_t per task.
+"""
+import numpy as np
+import pytest
+
+from oracle import lora as O
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-5
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def run_lib(dtype, wl, t, d_in, d_out, accumulate_dx=False, accumulate_dadb=False, init=None):
+    """Runs fwd + bwd through the C ABI; returns host fp64 arrays (Y, dX, dA, dB, Hs)."""
+    torch = _torch()
+    from paper_2509_01193_b200 import _lib
+    dev = torch.device("cuda:0")
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = _lib.LOBRA_BF16 if dtype == "bf16" else _lib.LOBRA_FP32
+
+    def up(a):
+        a = synth.round_bf16(a) if dtype == "bf16" else np.asarray(a, np.float32)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev).to(td)
+
+    X, W, A, B, dY = (up(t[k]) for k in ("X", "W", "A", "B", "dY"))
+    T = wl.T
+    ranks, scales = wl.ranks, wl.scales
+    Y = torch.empty(T, d_out, device=dev, dtype=td)
+    ws_n = _lib.lobra_lora_workspace_bytes(code, d_in, d_out, wl.seq_lens, wl.seq_task, ranks, scales)
+    hs_n = _lib.lobra_lora_saved_bytes(code, d_in, d_out, wl.seq_lens, wl.seq_task, ranks, scales)
+    ws = torch.empty(ws_n, device=dev, dtype=torch.uint8)
+    Hs = torch.empty(hs_n, device=dev, dtype=torch.uint8)
+    _lib.lobra_lora_fwd(X, W, A, B, ranks, scales, wl.seq_lens, wl.seq_task, Y, Hs, ws)
+    Rs = int(ranks.sum())
+    if init is not None:
+        dX = up(init["dX"])
+        dA = torch.from_numpy(init["dA"].astype(np.float32)).to(dev)
+        dB = torch.from_numpy(init["dB"].astype(np.float32)).to(dev)
+    else:
+        dX = torch.full((T, d_in), float("nan"), device=dev, dtype=td)
+        dA = torch.full((Rs, d_in), float("nan"), device=dev, dtype=torch.float32)
+        dB = torch.full((d_out, Rs), float("nan"), device=dev, dtype=torch.float32)
+    _lib.lobra_lora_bwd(X, W, A, B, ranks, scales, wl.seq_lens, wl.seq_task, Hs, dY, dX, dA, dB, ws,
+                        accumulate_dx=accumulate_dx, accumulate_dadb=accumulate_dadb)
+    torch.cuda.synchronize()
+    f = lambda x: x.float().cpu().numpy().astype(np.float64)
+    return f(Y), f(dX), f(dA), f(dB), Hs
+
+
+def oracle_inputs(dtype, t):
+    conv = (lambda a: synth.round_bf16(a).astype(np.float64)) if dtype == "bf16" else \
+        (lambda a: np.asarray(a, np.float32).astype(np.float64))
+    return {k: conv(v) for k, v in t.items()}
+
+
+def check_all(wl, t, got, tol, d_in, d_out):
+    Y, dX, dA, dB = got[:4]
+    args = (t["X"], t["W"], t["A"], t["B"], wl.ranks.tolist(), wl.scales, wl.seq_lens, wl.seq_task)
+    Yo = O.lora_fwd(*args)
+    dXo, dAo, dBo = O.lora_bwd(*args, t["dY"])
+    errs = {"Y": O.max_rel_err(Y, Yo), "dX": O.max_rel_err(dX, dXo)}
+    roff = np.concatenate([[0], np.cumsum(wl.ranks)])
+    present = set(wl.seq_task[wl.seq_lens > 0].tolist())
+    for k in range(len(wl.ranks)):
+        a, b = roff[k], roff[k + 1]
+        if k in present:
+            errs[f"dA{k}"] = O.max_rel_err(dA[a:b], dAo[a:b])
+            errs[f"dB{k}"] = O.max_rel_err(dB[:, a:b], dBo[:, a:b])
+        else:   # reading Q10: no tokens -> exact zeros when overwriting
+            assert not dA[a:b].any() and not dB[:, a:b].any()
+    bad = {k: v for k, v in errs.items() if not (v <= tol)}
+    assert not bad, f"tolerance {tol} exceeded: {bad} (all: {errs})"
+    return errs
+
+
+def test_c1_fp32():
+    """BASELINE config 1: tiny 64x64, 2 tasks r=4, 8 sequences of 3-40 tokens, fp32."""
+    wl = synth.config_c1()
+    t = synth.layer_tensors(wl, 64, 64, seed=1)
+    got = run_lib("fp32", wl, t, 64, 64)
+    check_all(wl, oracle_inputs("fp32", t), got, FP32_TOL, 64, 64)
+
+
+def _medium(seed=5, ranks=(8, 16, 64), scales=(2.0, 0.5, 1.0), n=9, lmax=160, group=True):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, lmax, size=n).astype(np.int32)
+    tids = rng.integers(0, len(ranks), size=n).astype(np.int32)
+    if group:
+        o = np.argsort(tids, kind="stable")
+        lens, tids = lens[o], tids[o]
+    tasks = [synth.TaskSpec(f"t{i}", 0, 0, 1, r, s) for i, (r, s) in enumerate(zip(ranks, scales))]
+    return synth.Workload("medium", tasks, lens, tids, lmax)
+
+
+@pytest.mark.parametrize("group", [True, False])
+def test_bf16_medium(group):
+    """Several M tiles with a ragged tail, mixed-task tiles, 3 tasks of ranks 8/16/64,
+    N = 384 (one full 256-wide tile + a 128 tail)."""
+    wl = _medium(group=group)
+    d_in, d_out = 256, 384
+    t = synth.layer_tensors(wl, d_in, d_out, seed=11)
+    got = run_lib("bf16", wl, t, d_in, d_out)
+    check_all(wl, oracle_inputs("bf16", t), got, BF16_TOL, d_in, d_out)
+
+
+def test_bf16_fp32_paths_agree_medium():
+    wl = _medium(seed=6)
+    t = synth.layer_tensors(wl, 128, 192, seed=12)
+    check_all(wl, oracle_inputs("fp32", t), run_lib("fp32", wl, t, 128, 192), FP32_TOL, 128, 192)
+
+
+def test_bf16_W_zero_isolates_adapters():
+    wl = _medium(seed=7)
+    t = synth.layer_tensors(wl, 192, 256, seed=13, zero_W=True)
+    check_all(wl, oracle_inputs("bf16", t), run_lib("bf16", wl, t, 192, 256), BF16_TOL, 192, 256)
+
+
+def test_bf16_B_zero_bitwise_equals_scale_zero():
+    """B_t = 0 adds exact zeros to the fp32 accumulator: Y(B=0) == Y(s=0) bit for bit,
+    and both match the base X W^T."""
+    wl = _medium(seed=8)
+    t = synth.layer_tensors(wl, 128, 256, seed=14, zero_B=True)
+    Y0 = run_lib("bf16", wl, t, 128, 256)[0]
+    wl2 = _medium(seed=8, scales=(0.0, 0.0, 0.0))
+    t2 = synth.layer_tensors(wl2, 128, 256, seed=14)
+    Y1 = run_lib("bf16", wl2, t2, 128, 256)[0]
+    assert np.array_equal(Y0, Y1)
+    ti = oracle_inputs("bf16", t)
+    assert O.max_rel_err(Y0, ti["X"] @ ti["W"].T) < BF16_TOL
+
+
+def test_bf16_packing_order_rows_bitwise():
+    """Per-sequence Y rows do not depend on where the sequence is packed."""
+    wl = _medium(seed=9, n=7)
+    d_in, d_out = 128, 256
+    t = synth.layer_tensors(wl, d_in, d_out, seed=15)
+    Y = run_lib("bf16", wl, t, d_in, d_out)[0]
+    perm = np.array([3, 6, 0, 5, 1, 4, 2])
+    offs = np.concatenate([[0], np.cumsum(wl.seq_lens)])
+    rows = np.concatenate([np.arange(offs[k], offs[k + 1]) for k in perm]).astype(np.int64)
+    wl2 = synth.Workload("perm", wl.tasks, wl.seq_lens[perm], wl.seq_task[perm], wl.l_max)
+    t2 = dict(t)
+    t2["X"], t2["dY"] = t["X"][rows], t["dY"][rows]
+    Y2 = run_lib("bf16", wl2, t2, d_in, d_out)[0]
+    assert np.array_equal(Y[rows], Y2)
+
+
+def test_bf16_accumulate_flags():
+    """accumulate_dx / accumulate_dadb add to the existing buffers (gradient
+    accumulation)."""
+    wl = _medium(seed=10)
+    d_in, d_out = 128, 192
+    t = synth.layer_tensors(wl, d_in, d_out, seed=16)
+    rng = np.random.default_rng(0)
+    Rs = int(wl.ranks.sum())
+    init = {"dX": rng.standard_normal((wl.T, d_in)).astype(np.float32),
+            "dA": rng.standard_normal((Rs, d_in)), "dB": rng.standard_normal((d_out, Rs))}
+    got = run_lib("bf16", wl, t, d_in, d_out, accumulate_dx=True, accumulate_dadb=True, init=init)
+    ti = oracle_inputs("bf16", t)
+    args = (ti["X"], ti["W"], ti["A"], ti["B"], wl.ranks.tolist(), wl.scales, wl.seq_lens, wl.seq_task)
+    dXo, dAo, dBo = O.lora_bwd(*args, ti["dY"])
+    assert O.max_rel_err(got[1], dXo + synth.round_bf16(init["dX"])) < BF16_TOL
+    assert O.max_rel_err(got[2], dAo + init["dA"].astype(np.float32)) < BF16_TOL
+    assert O.max_rel_err(got[3], dBo + init["dB"].astype(np.float32)) < BF16_TOL
+
+
+def test_bf16_task_without_tokens_gets_zero_grads():
+    wl = _medium(seed=11, ranks=(8, 16, 64, 32), scales=(1.0, 1.0, 1.0, 3.0))
+    assert 3 not in set(wl.seq_task.tolist())
+    t = synth.layer_tensors(wl, 128, 128, seed=17)
+    got = run_lib("bf16", wl, t, 128, 128)
+    check_all(wl, oracle_inputs("bf16", t), got, BF16_TOL, 128, 128)
+
+
+def test_bf16_c2_q_projection_full_size():
+    """BASELINE config 2 at full size (T = 16384, 4 tasks r=16, s=2), the q projection
+    4096 -> 4096 in the launch configuration bench.py times: dA_t/dB_t compared in
+    full, Y/dX on sampled rows (every 64th row + all rows of the first sequence)."""
+    wl = synth.config_c2()
+    d_in = d_out = 4096
+    t = synth.layer_tensors(wl, d_in, d_out, seed=21)
+    Y, dX, dA, dB, _ = run_lib("bf16", wl, t, d_in, d_out)
+    ti = oracle_inputs("bf16", t)
+    rows = np.unique(np.concatenate([np.arange(0, wl.T, 64), np.arange(0, wl.seq_lens[0])]))
+    # oracle on the sampled rows only (rows are independent)
+    row_task = np.repeat(wl.seq_task, wl.seq_lens)[rows]
+    lens1 = np.ones(len(rows), np.int32)
+    args = (ti["X"][rows], ti["W"], ti["A"], ti["B"], wl.ranks.tolist(), wl.scales, lens1, row_task)
+    Yo = O.lora_fwd(*args)
+    dXo = O.lora_bwd(*args, ti["dY"][rows])[0]
+    assert O.max_rel_err(Y[rows], Yo) < BF16_TOL
+    assert O.max_rel_err(dX[rows], dXo) < BF16_TOL
+    # full adapter gradients
+    fargs = (ti["X"], ti["W"], ti["A"], ti["B"], wl.ranks.tolist(), wl.scales, wl.seq_lens, wl.seq_task)
+    _, dAo, dBo = _bwd_adapters_only(*fargs, ti["dY"])
+    roff = np.concatenate([[0], np.cumsum(wl.ranks)])
+    for k in range(len(wl.ranks)):
+        assert O.max_rel_err(dA[roff[k]:roff[k + 1]], dAo[roff[k]:roff[k + 1]]) < BF16_TOL
+        assert O.max_rel_err(dB[:, roff[k]:roff[k + 1]], dBo[:, roff[k]:roff[k + 1]]) < BF16_TOL
+
+
+def _bwd_adapters_only(X, W, A, B, ranks, scales, lens, tasks, dY):
+    return O.lora_bwd(X, W, A, B, ranks, scales, lens, tasks, dY, want_dx=False)
