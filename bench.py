@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the LobRA multi-LoRA hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lobra|reference]
+
+One STEP = one pass of the whole hot path over one batch:
+per-step dispatch on the host (a7: bucketing DP + exact Eq. 3 + chunking), then for
+every micro-batch of this rank's replica the forward and backward of all seven
+Llama-2-7B projections with every task's adapters (a0-a5, TP collectives a6), then the
+adapter-gradient all-reduce across replicas (a8).
+
+N = 1: BASELINE config 2 (7B shapes, 4 tasks r=16 s=2, skewed lengths <= 4K, T = 16384
+packed, bf16) on 1 x TP1.  N > 1 (launched by torchrun, one rank per GPU): weak scaling,
+N x 16384 tokens of the same task mix per step, dispatched over heterogeneous replicas
+(2: 2xTP1; 4: 2xTP1 + 1xTP2; 8: 4xTP1 + 2xTP2; SURVEY.md §8(d) sweep).
+
+value = real tokens processed by all ranks / max-over-ranks device time.  Inputs are
+resident in HBM when the timed region starts; every projection input exceeds L2
+(>= 128 MiB per step-input vs 126 MB L2), so no explicit L2 flush is used.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "multi-LoRA fwd+bwd tokens/s/GPU at 1/2/4/8 B200; % of bf16 tensor peak"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+T_PER_GPU = 16384
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ plans
+def deployment_for(n_gpus: int):
+    """(tp, replicas, max_tokens) per group, ordered by (tp, M) -- SURVEY.md §8(d)."""
+    if n_gpus == 1:
+        return [(1, 1, 16384)]
+    if n_gpus == 2:
+        return [(1, 2, 16384)]
+    if n_gpus == 4:
+        return [(1, 2, 16384), (2, 1, 32768)]
+    if n_gpus == 8:
+        return [(1, 4, 16384), (2, 2, 32768)]
+    if n_gpus % 2 == 0:
+        return [(1, n_gpus - 2, 16384), (2, 1, 32768)]
+    return [(1, n_gpus, 16384)]
+
+
+def cost_table(groups, grid_step=256, grid_max=32768):
+    """Integer per-sequence cost c_i(u) on the grid (reading Q15): projections are
+    linear in tokens (App. D with a2 = 0 for projection-only layers); TP2 costs half
+    per token plus a communication penalty.  Units ~ 64 tokens."""
+    U = grid_max // grid_step
+    eff = {1: 1.0, 2: 0.89, 4: 0.75, 8: 0.6}
+    out = []
+    for tp, _, _ in groups:
+        out.append([max(1, int(round((k + 1) * grid_step / 64 / (tp * eff.get(tp, 0.5)))))
+                    for k in range(U)])
+    return out
+
+
+def replica_ranks(groups):
+    """Global replica id -> list of ranks (contiguous, group-major)."""
+    out, r = [], 0
+    for tp, p, _ in groups:
+        for _ in range(p):
+            out.append(list(range(r, r + tp)))
+            r += tp
+    return out
+
+
+# ------------------------------------------------------------------------------ oracle leg
+def oracle_tokens_per_s(wl, shapes, budget_tokens=2048, seed=7):
+    """The fp64 CPU oracle (test infrastructure) timed on the host cores on a bounded
+    sample of the workload: the first sequences of the batch totalling ~budget_tokens,
+    all seven projections forward + backward."""
+    from oracle import lora as O
+    from workloads import synth
+    lens, tasks, tot = [], [], 0
+    for L, t in zip(wl.seq_lens.tolist(), wl.seq_task.tolist()):
+        if tot >= budget_tokens:
+            break
+        L = min(L, budget_tokens - tot)
+        lens.append(L)
+        tasks.append(t)
+        tot += L
+    sub = synth.Workload("sample", wl.tasks, np.array(lens, np.int32), np.array(tasks, np.int32), wl.l_max)
+    data = []
+    for i, (_, d_in, d_out, _, _) in enumerate(shapes):
+        t = synth.layer_tensors(sub, d_in, d_out, seed=seed + i)
+        data.append({k: synth.round_bf16(v).astype(np.float64) for k, v in t.items()})
+    t0 = time.perf_counter()
+    for t in data:
+        args = (t["X"], t["W"], t["A"], t["B"], sub.ranks.tolist(), sub.scales, sub.seq_lens, sub.seq_task)
+        O.lora_fwd(*args)
+        O.lora_bwd(*args, t["dY"])
+    dt = time.perf_counter() - t0
+    threads = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 0) for i in threadpool_info()] + [1])
+    except Exception:
+        pass
+    return tot / dt, dt, tot, threads
+
+
+def run_reference(args):
+    """--impl reference: the oracle (as it stands) on the host cores, bounded samples of
+    the same workload; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2509_01193_b200.layer import LLAMA2_7B
+    from workloads import synth
+    wl = synth.config_c2()
+    budget = 512
+    times, toks = [], 0
+    for i in range(args.warmup + args.steps):
+        tps, dt, n, threads = oracle_tokens_per_s(wl, LLAMA2_7B, budget_tokens=budget, seed=100 + i)
+        if i >= args.warmup:
+            times.append(dt)
+            toks = n
+    tot = sum(times)
+    value = toks * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: Llama-2-7B 7 projections, 4 tasks r=16 s=2, lengths<=4K",
+                       "global_batch_tokens": toks, "parallelism": "host"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {toks} tokens of the C2 batch, 7 projections fwd+bwd, fp64 NumPy"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ main leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lobra", choices=["lobra", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="few steps, no e2e/cpu (for ncu)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_01193_b200 import _lib
+    from paper_2509_01193_b200.layer import LLAMA2_7B, LoraLayer, algorithmic_flops
+    from workloads import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = max(world, 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+
+    groups = deployment_for(n_gpus)
+    reps = replica_ranks(groups)
+    my_rep = next(i for i, rr in enumerate(reps) if rank in rr)
+    my_group = 0
+    acc = 0
+    for gi, (tp, p, _) in enumerate(groups):
+        if my_rep < acc + p:
+            my_group = gi
+            break
+        acc += p
+    tp_size = groups[my_group][0]
+    tp_rank = reps[my_rep].index(rank)
+    comm = None
+    if world > 1:
+        uid = [_lib.lobra_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = _lib.lobra_comm_init(uid[0], world, rank, my_rep)
+
+    tasks = synth.c2_tasks()
+    ranks = [t.rank for t in tasks]
+    scales = [t.scale for t in tasks]
+    layer = LoraLayer(LLAMA2_7B, ranks, scales, dev, torch.bfloat16, tp_size, tp_rank, comm, seed=1234)
+    max_tok = groups[my_group][2]
+    io = layer.alloc_io(max_tok, seed=99 + rank)
+
+    tp_list = [g[0] for g in groups]
+    rep_list = [g[1] for g in groups]
+    m_list = [g[2] for g in groups]
+    grid_step, grid_max = 256, max(m_list)
+    costs = cost_table(groups, grid_step, grid_max)
+
+    def make_batch(step: int):
+        """Global batch of the step: N x 16384 tokens of the C2 task mix (seeded)."""
+        if n_gpus == 1:
+            return synth.config_c2(seed=2 + step)
+        return synth.pack_tokens(tasks, T_PER_GPU * n_gpus, 4096, seed=1000 + step, name="C2xN")
+
+    n_batches = 4
+    batches = [make_batch(i) for i in range(n_batches)]
+
+    def plan(wl):
+        d = _lib.lobra_dispatch(tp_list, rep_list, m_list, costs, wl.seq_lens, wl.seq_task,
+                                grid_step, grid_max, 16, 0)
+        mine = np.nonzero(d["seq_replica"] == my_rep)[0]
+        chunks = []
+        for c in sorted(set(d["seq_chunk"][mine].tolist())):
+            idx = mine[d["seq_chunk"][mine] == c]
+            idx = idx[np.argsort(d["pack_order"][idx])]
+            chunks.append((wl.seq_lens[idx].astype(np.int32), wl.seq_task[idx].astype(np.int32)))
+        return chunks, int(wl.seq_lens.sum()), d
+
+    def run_step(chunks, stream=None):
+        if tp_size > 1:
+            layer.flat_grad.zero_()
+        for ci, (lens, tsk) in enumerate(chunks):
+            T = int(lens.sum())
+            layer.forward(lens, tsk, io, T, stream=stream)
+            layer.backward(lens, tsk, io, T, accumulate_dadb=(ci > 0 or tp_size > 1), stream=stream)
+        layer.sync_adapter_grads(stream=stream)
+
+    plans = [plan(b) for b in batches]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        run_step(plans[i % n_batches][0])
+    barrier()
+
+    peaks, peak_src = load_peaks()
+    sampler = ClockSampler(local) if rank == 0 or world > 1 else None
+    if sampler and rank == 0:
+        sampler.start()
+    _lib.lobra_profile_enable(True)
+    _lib.lobra_profile_read(reset=True)
+    l0 = _lib.lobra_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens = 0
+    tokens_local = 0
+    disp_ms = []
+    barrier()
+    e0.record(stream)
+    for i in range(args.steps):
+        # a7: the dispatch of this step runs on the host while the GPU works on the
+        # previously enqueued step ("fully overlapped")
+        t0 = time.perf_counter()
+        chunks, tok, _ = plan(batches[(args.warmup + i) % n_batches])
+        disp_ms.append(1000 * (time.perf_counter() - t0))
+        run_step(chunks)
+        tokens += tok
+        tokens_local += sum(int(c[0].sum()) for c in chunks)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1)
+    launches = _lib.lobra_launch_count() - l0
+    prof = _lib.lobra_profile_read(reset=True)
+    _lib.lobra_profile_enable(False)
+    clocks = sampler.stop() if (sampler and rank == 0) else None
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    else:
+        ms_total = ms_local
+    ms_step = ms_total / args.steps
+    value = tokens / (ms_total / 1000.0)
+
+    # ---- roofline of the dominant kernel (device time share inside the timed region)
+    T_step_local = tokens_local / args.steps
+    # algorithmic FLOPs per GEMM class over the timed region (this rank's shards)
+    fl_fwd = fl_bwd = 0.0
+    nt = np.zeros(len(ranks))
+    for i in range(args.steps):
+        for lens, tsk in plan(batches[(args.warmup + i) % n_batches])[0]:
+            for L, t in zip(lens.tolist(), tsk.tolist()):
+                nt[t] += L
+    tok_r = float((nt * np.array(ranks)).sum())
+    for p in layer.projs:
+        fl_fwd += 2.0 * nt.sum() * p.in_l * p.out_l + 2.0 * tok_r * p.out_l
+        fl_bwd += 2.0 * nt.sum() * p.in_l * p.out_l + 2.0 * tok_r * p.in_l
+    kern = {k: {"launches": c, "ms": ms} for k, (c, ms) in prof.items() if c}
+    dom = max(("gemm_fwd", "gemm_bwd"), key=lambda k: prof[k][1])
+    dom_fl = fl_fwd if dom == "gemm_fwd" else fl_bwd
+    dom_ms = prof[dom][1]
+    peak_t = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    achieved = dom_fl / (dom_ms / 1000.0) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("k_gemm_" + dom.split("_")[1])
+    roofline = {"bound": "tensor", "kernel": f"k_gemm ({dom})", "achieved": achieved, "peak": peak_t,
+                "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": traffic,
+                "peak_source": peak_src + " bf16_tflops_sustained (kernel timed inside a long step)",
+                "share_of_step": dom_ms / ms_local,
+                "flops_per_launch": dom_fl / max(prof[dom][0], 1),
+                "ms_per_launch": dom_ms / max(prof[dom][0], 1)}
+    flops_step = algorithmic_flops(LLAMA2_7B, int(tokens / args.steps), ranks)["total"]
+    step_tflops = flops_step / (ms_step / 1000.0) / 1e12
+
+    # ---- end to end through the public API with host buffers (pinned), rank-local
+    e2e = None
+    if not args.no_e2e and not args.profile_only:
+        host_x = {g: torch.empty(io["X"][g].shape, dtype=io["X"][g].dtype, pin_memory=True) for g in io["X"]}
+        host_dy = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in io["dY"].items()}
+        for g in host_x:
+            host_x[g].copy_(io["X"][g])
+        for k in host_dy:
+            host_dy[k].copy_(io["dY"][k])
+        host_grad = torch.empty(layer.flat_grad.shape, dtype=torch.float32, pin_memory=True)
+        ke = max(1, min(args.steps, 5))
+        h2d = d2h = 0
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        e2e_tokens = 0
+        for i in range(ke):
+            chunks, tok, _ = plan(batches[i % n_batches])
+            for lens, tsk in chunks:
+                T = int(lens.sum())
+                for g in host_x:
+                    io["X"][g][:T].copy_(host_x[g][:T], non_blocking=True)
+                    h2d += host_x[g][:T].numel() * 2
+                for k in host_dy:
+                    io["dY"][k][:T].copy_(host_dy[k][:T], non_blocking=True)
+                    h2d += host_dy[k][:T].numel() * 2
+                layer.forward(lens, tsk, io, T)
+                layer.backward(lens, tsk, io, T, accumulate_dadb=True)
+            layer.sync_adapter_grads()
+            host_grad.copy_(layer.flat_grad, non_blocking=True)
+            d2h += layer.flat_grad.numel() * 4
+            e2e_tokens += tok
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": e2e_tokens / (e_ms / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d // ke), "d2h_bytes_per_step": int(d2h // ke),
+               "steps": ke}
+
+    cpu = None
+    if rank == 0 and n_gpus == 1 and not args.no_cpu and not args.profile_only:
+        tps, dt, n, threads = oracle_tokens_per_s(batches[0], LLAMA2_7B, budget_tokens=2048)
+        cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {n} tokens of the C2 batch, 7 projections fwd+bwd, fp64 NumPy ({dt:.1f} s)"}
+
+    if rank == 0:
+        par = "+".join(f"{p}xTP{tp}" for tp, p, _ in groups)
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": n_gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded; lengths lognormal-fitted to the paper's dataset table)",
+                "config": {"workload": "C2: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
+                                       "4 tasks r=16 s=2, lengths<=4096 packed",
+                           "global_batch_tokens": int(tokens / args.steps), "seq_len_max": 4096,
+                           "parallelism": par, "l2": "inputs > L2 (each projection input >= 128 MiB)"},
+                "per_gpu": value / n_gpus,
+                "algorithmic_tflops": step_tflops,
+                "frac_of_bf16_peak": {"burst": step_tflops / float(peaks["bf16_tflops"]),
+                                      "sustained": step_tflops / peak_t, "nominal_2250": step_tflops / 2250.0},
+                "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+                "kernels": kern, "dispatch_ms_median": statistics.median(disp_ms) if disp_ms else None,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.destroy()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -233,6 +233,33 @@ LOBRA_API lobra_status lobra_comm_tp_info(lobra_comm comm, int32_t* tp_size, int
 LOBRA_API lobra_status lobra_adapter_allreduce(lobra_comm comm, float* flat_grads, size_t count,
                                      lobra_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * Tracing: per-kernel-class device times (CUDA events recorded on the launching
+ * stream around every kernel the library enqueues, only while enabled) and a launch
+ * counter (always on).  The paper's cost model is fitted from such single-layer
+ * profiles (App. D).
+ * ------------------------------------------------------------------------------ */
+enum {
+  LOBRA_K_GEMM_FWD = 0,   /* fused base GEMM + LoRA expand, forward            */
+  LOBRA_K_GEMM_BWD = 1,   /* fused dY W + G_s A_t, backward                     */
+  LOBRA_K_ROWPROJ = 2,    /* rank-r shrink H_s / G_s                            */
+  LOBRA_K_SEGRED = 3,     /* token reductions dA_t / dB_t (partials)            */
+  LOBRA_K_FINALIZE = 4,   /* fixed-order partial sums                           */
+  LOBRA_K_PAD = 5,        /* adapter operand packing                            */
+  LOBRA_K_FP32 = 6,       /* fp32 SIMT path kernels                             */
+  LOBRA_K_NUM = 8
+};
+typedef struct {
+  int64_t count[LOBRA_K_NUM];   /* launches per class since the last reset        */
+  double ms[LOBRA_K_NUM];       /* summed device milliseconds per class           */
+} lobra_profile;
+/* Enables/disables event timing of every launch (off by default). */
+LOBRA_API lobra_status lobra_profile_enable(int on);
+/* Synchronises the recorded events, fills `out`, and (if reset) clears the counters. */
+LOBRA_API lobra_status lobra_profile_read(lobra_profile* out, int reset);
+/* Total kernels launched by the library in this process (never reset). */
+LOBRA_API int64_t lobra_launch_count(void);
+
 /* Frees the lazily created per-device context(s). */
 LOBRA_API lobra_status lobra_shutdown(void);
 

@@ -24,8 +24,9 @@ EXPORTED = [
     "lobra_last_error", "lobra_version", "lobra_lora_workspace_bytes", "lobra_lora_saved_bytes",
     "lobra_lora_fwd", "lobra_lora_bwd", "lobra_dispatch", "lobra_nccl_unique_id",
     "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
-    "lobra_shutdown",
+    "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
 ]
+K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "other"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -56,6 +57,10 @@ class DispatchOut(C.Structure):
                 ("seq_bucket", _i32p), ("seq_replica", _i32p), ("seq_chunk", _i32p),
                 ("pack_order", _i32p), ("replica_cost", _i64p), ("t_hat", C.c_int64),
                 ("nodes", C.c_int64)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("count", C.c_int64 * 8), ("ms", C.c_double * 8)]
 
 
 _LIB = None
@@ -104,6 +109,11 @@ def load() -> C.CDLL:
     lib.lobra_adapter_allreduce.restype = C.c_int
     lib.lobra_adapter_allreduce.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
     lib.lobra_shutdown.restype = C.c_int
+    lib.lobra_profile_enable.restype = C.c_int
+    lib.lobra_profile_enable.argtypes = [C.c_int]
+    lib.lobra_profile_read.restype = C.c_int
+    lib.lobra_profile_read.argtypes = [C.POINTER(Profile), C.c_int]
+    lib.lobra_launch_count.restype = C.c_int64
     _LIB = lib
     return lib
 
@@ -278,3 +288,19 @@ def lobra_adapter_allreduce(comm: Comm, flat, stream=None):
 
 def lobra_shutdown():
     _check(load().lobra_shutdown())
+
+
+# ---------------------------------------------------------------------------- tracing
+def lobra_profile_enable(on: bool = True):
+    _check(load().lobra_profile_enable(int(bool(on))))
+
+
+def lobra_profile_read(reset: bool = True) -> dict:
+    """{kernel class: (launches, device ms)} since the last reset (synchronises)."""
+    p = Profile()
+    _check(load().lobra_profile_read(C.byref(p), int(bool(reset))))
+    return {K_NAMES[k]: (int(p.count[k]), float(p.ms[k])) for k in range(8)}
+
+
+def lobra_launch_count() -> int:
+    return int(load().lobra_launch_count())

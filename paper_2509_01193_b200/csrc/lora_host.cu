@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -31,6 +32,55 @@ void clear_error() { g_err.clear(); }
 // comm.cpp
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
 lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st);
+
+// ------------------------------------------------------------------ tracing
+namespace {
+std::atomic<int64_t> g_launches{0};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+struct ProfRec {
+  int kind;
+  cudaEvent_t e0, e1;
+};
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+int64_t g_prof_count[LOBRA_K_NUM] = {0};
+double g_prof_ms[LOBRA_K_NUM] = {0};
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one kernel launch: counts it and, while tracing is enabled, records events
+// on the launching stream around it.
+struct Prof {
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  Prof(int k, cudaStream_t s) : kind(k), st(s) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (g_prof_on) {
+      e0 = prof_event();
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~Prof() {
+    if (!e0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t e1 = prof_event();
+    cudaEventRecord(e1, st);
+    g_prof_recs.push_back({kind, e0, e1});
+  }
+};
+}  // namespace
 
 // ------------------------------------------------------------------ per-device context
 namespace {
@@ -384,25 +434,25 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
   const Meta meta = device_meta(P, w + L.meta);
   const int in = (int)prob->in, out = (int)prob->out;
   if (prob->dtype == LOBRA_FP32) {
-    launch_f32_rowproj(0, static_cast<const float*>(X), static_cast<const float*>(ad->A),
-                       static_cast<const float*>(ad->B), in, out, meta, static_cast<float*>(Hs), st);
-    launch_f32_gemm(0, static_cast<const float*>(X), static_cast<const float*>(W),
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_rowproj(0, static_cast<const float*>(X), static_cast<const float*>(ad->A),
+                       static_cast<const float*>(ad->B), in, out, meta, static_cast<float*>(Hs), st); }
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_gemm(0, static_cast<const float*>(X), static_cast<const float*>(W),
                     static_cast<const float*>(ad->A), static_cast<const float*>(ad->B),
-                    static_cast<const float*>(Hs), in, out, meta, static_cast<float*>(Y), 0, st);
+                    static_cast<const float*>(Hs), in, out, meta, static_cast<float*>(Y), 0, st); }
   } else {
     auto* Apad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
     auto* Bpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
-    launch_pad(0, static_cast<const __nv_bfloat16*>(ad->A), Apad, meta, in, out, st);
-    launch_pad(1, static_cast<const __nv_bfloat16*>(ad->B), Bpad, meta, in, out, st);
+    { Prof p_(LOBRA_K_PAD, st); launch_pad(0, static_cast<const __nv_bfloat16*>(ad->A), Apad, meta, in, out, st); }
+    { Prof p_(LOBRA_K_PAD, st); launch_pad(1, static_cast<const __nv_bfloat16*>(ad->B), Bpad, meta, in, out, st); }
     CUtensorMap mX, mApad, mW, mSlot, mBpad;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mApad, Apad, in, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mW, W, in, out, 64, 256)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mBpad, Bpad, 64, (uint64_t)P.ntasks * out, 64, 256)) != LOBRA_OK) return s;
-    launch_rowproj(mX, mApad, in, meta, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st);
-    launch_gemm(false, mX, mW, mSlot, mBpad, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
-                ctx->num_sms, st);
+    { Prof p_(LOBRA_K_ROWPROJ, st); launch_rowproj(mX, mApad, in, meta, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mBpad, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
+                ctx->num_sms, st); }
   }
   if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
   if (prob->tp_kind == LOBRA_TP_ROW) {
@@ -456,20 +506,20 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     float* G = reinterpret_cast<float*>(w + L.gslots);
     const float* Af = static_cast<const float*>(ad->A);
     const float* Bf = static_cast<const float*>(ad->B);
-    launch_f32_rowproj(1, static_cast<const float*>(dY), Af, Bf, in, out, meta, G, st);
-    launch_f32_gemm(1, static_cast<const float*>(dY), static_cast<const float*>(W), Af, Bf, G, in,
-                    out, meta, static_cast<float*>(dX), accumulate_dx, st);
-    launch_f32_segred(0, static_cast<const float*>(X), G, in, meta, dA, ldA, accumulate_dadb, st);
-    launch_f32_segred(1, static_cast<const float*>(dY), static_cast<const float*>(Hs), out, meta,
-                      dB, 0, accumulate_dadb, st);
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_rowproj(1, static_cast<const float*>(dY), Af, Bf, in, out, meta, G, st); }
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_gemm(1, static_cast<const float*>(dY), static_cast<const float*>(W), Af, Bf, G, in,
+                    out, meta, static_cast<float*>(dX), accumulate_dx, st); }
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_segred(0, static_cast<const float*>(X), G, in, meta, dA, ldA, accumulate_dadb, st); }
+    { Prof p_(LOBRA_K_FP32, st); launch_f32_segred(1, static_cast<const float*>(dY), static_cast<const float*>(Hs), out, meta,
+                      dB, 0, accumulate_dadb, st); }
   } else {
     auto* Btpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
     auto* Atpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
     auto* Gs = reinterpret_cast<__nv_bfloat16*>(w + L.gslots);
     float* partA = reinterpret_cast<float*>(w + L.partA);
     float* partB = reinterpret_cast<float*>(w + L.partB);
-    launch_pad(2, static_cast<const __nv_bfloat16*>(ad->B), Btpad, meta, in, out, st);
-    launch_pad(3, static_cast<const __nv_bfloat16*>(ad->A), Atpad, meta, in, out, st);
+    { Prof p_(LOBRA_K_PAD, st); launch_pad(2, static_cast<const __nv_bfloat16*>(ad->B), Btpad, meta, in, out, st); }
+    { Prof p_(LOBRA_K_PAD, st); launch_pad(3, static_cast<const __nv_bfloat16*>(ad->A), Atpad, meta, in, out, st); }
     CUtensorMap mdY, mBt, mWmn, mG, mAt, mX, mHs;
     if ((s = make_map(&mdY, dY, out, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mBt, Btpad, out, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
@@ -478,13 +528,13 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mAt, Atpad, 64, (uint64_t)P.ntasks * in, 64, 256)) != LOBRA_OK) return s;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mHs, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
-    launch_rowproj(mdY, mBt, out, meta, Gs, ctx->num_sms, st);
-    launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
-                accumulate_dx, meta, ctx->num_sms, st);
-    launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st);
-    launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st);
-    launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st);
-    launch_finalize(1, partB, out, meta, dB, 0, accumulate_dadb, st);
+    { Prof p_(LOBRA_K_ROWPROJ, st); launch_rowproj(mdY, mBt, out, meta, Gs, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
+                accumulate_dx, meta, ctx->num_sms, st); }
+    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st); }
+    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta, dB, 0, accumulate_dadb, st); }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
   if (prob->tp_kind == LOBRA_TP_COLUMN) {
@@ -494,6 +544,35 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
   }
   return LOBRA_OK;
 }
+
+extern "C" lobra_status lobra_profile_enable(int on) {
+  clear_error();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_profile_read(lobra_profile* out, int reset) {
+  clear_error();
+  if (!out) return fail(LOBRA_ERR_INPUT, "null output");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (const ProfRec& r : g_prof_recs) {
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) return fail(LOBRA_ERR_CUDA, "event sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    g_prof_ms[r.kind] += ms;
+    g_prof_count[r.kind] += 1;
+    g_prof_pool.push_back(r.e0);
+    g_prof_pool.push_back(r.e1);
+  }
+  g_prof_recs.clear();
+  for (int k = 0; k < LOBRA_K_NUM; ++k) out->count[k] = g_prof_count[k], out->ms[k] = g_prof_ms[k];
+  if (reset)
+    for (int k = 0; k < LOBRA_K_NUM; ++k) g_prof_count[k] = 0, g_prof_ms[k] = 0;
+  return LOBRA_OK;
+}
+
+extern "C" int64_t lobra_launch_count(void) { return g_launches.load(); }
 
 extern "C" lobra_status lobra_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_ctx_mu);

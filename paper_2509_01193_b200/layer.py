@@ -1,0 +1,196 @@
+"""One Llama-shaped decoder layer's seven LoRA projections driven through the C ABI.
+
+This is plumbing around ``liblobra.so``: PyTorch allocates device memory, every step of
+the hot path runs in the library's kernels (``lobra_lora_fwd`` / ``lobra_lora_bwd``).
+Projections: q, k, v, gate, up are column-parallel and o, down
+row-parallel under Megatron TP; every projection carries all tasks' adapters
+(reading Q3).
+
+Adapter gradients live in ONE flat fp32 buffer with the full-size layout on every rank
+(DESIGN.md "Multi-GPU"): per projection dA_full [sum r, in_full] then dB_full
+[out_full, sum r].  A TP rank writes only its partial sums into it (column rank: its dB
+rows, partial dA; row rank: its dA column slice via dA_ld, partial dB), so one world
+all-reduce (``lobra_adapter_allreduce``) yields the exact full gradients.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+# (name, in, out, tp kind, input group)
+LLAMA2_7B = [("q", 4096, 4096, "col", "attn"), ("k", 4096, 4096, "col", "attn"),
+             ("v", 4096, 4096, "col", "attn"), ("o", 4096, 4096, "row", "o_in"),
+             ("gate", 4096, 11008, "col", "mlp"), ("up", 4096, 11008, "col", "mlp"),
+             ("down", 11008, 4096, "row", "down_in")]
+LLAMA2_70B = [("q", 8192, 8192, "col", "attn"), ("k", 8192, 1024, "col", "attn"),
+              ("v", 8192, 1024, "col", "attn"), ("o", 8192, 8192, "row", "o_in"),
+              ("gate", 8192, 28672, "col", "mlp"), ("up", 8192, 28672, "col", "mlp"),
+              ("down", 28672, 8192, "row", "down_in")]
+
+
+def algorithmic_flops(shapes, T: int, ranks, tokens_per_task=None) -> dict:
+    """Algorithmic FLOPs of one fwd+bwd over T tokens: base
+    4*T*sum(in*out) (no dW: frozen base), LoRA 6*sum_t T_t r_t sum(in+out)."""
+    base = 4 * T * sum(i * o for _, i, o, *_ in shapes)
+    if tokens_per_task is None:
+        rt = T * float(np.mean(ranks))
+    else:
+        rt = float(sum(n * r for n, r in zip(tokens_per_task, ranks)))
+    lora = 6 * rt * sum(i + o for _, i, o, *_ in shapes)
+    return {"base": base, "lora": lora, "total": base + lora}
+
+
+@dataclass
+class _Proj:
+    name: str
+    d_in: int           # full widths
+    d_out: int
+    kind: str           # "col" | "row"
+    group: str
+    in_l: int           # local widths
+    out_l: int
+    W: torch.Tensor
+    A: torch.Tensor
+    B: torch.Tensor
+    dA_off: int         # element offsets into the flat gradient buffer
+    dB_off: int
+    Hs: torch.Tensor | None = None
+
+
+class LoraLayer:
+    def __init__(self, shapes, ranks, scales, device, dtype=torch.bfloat16, tp_size=1, tp_rank=0,
+                 comm=None, seed=0):
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.code = _lib.dtype_code(dtype)
+        self.ranks = np.asarray(ranks, np.int32)
+        self.scales = np.asarray(scales, np.float32)
+        self.rsum = int(self.ranks.sum())
+        self.tp_size, self.tp_rank, self.comm = tp_size, tp_rank, comm
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        self.projs = []
+        off = 0
+        for name, d_in, d_out, kind, group in shapes:
+            if kind == "col":
+                in_l, out_l = d_in, d_out // tp_size
+            else:
+                in_l, out_l = d_in // tp_size, d_out
+            assert in_l * (tp_size if kind == "row" else 1) == d_in
+            assert out_l * (tp_size if kind == "col" else 1) == d_out
+            # full-size random init (synthetic weights), then the rank's shard
+            W = self._randn((d_out, d_in), 1 / math.sqrt(d_in), g)
+            A = self._randn((self.rsum, d_in), 1 / math.sqrt(d_in), g)
+            Bparts = [self._randn((d_out, int(r)), 1 / math.sqrt(int(r)), g) for r in self.ranks]
+            B = torch.cat(Bparts, dim=1)
+            if kind == "col":
+                sl = slice(tp_rank * out_l, (tp_rank + 1) * out_l)
+                W, B = W[sl].contiguous(), B[sl].contiguous()
+            else:
+                sl = slice(tp_rank * in_l, (tp_rank + 1) * in_l)
+                W, A = W[:, sl].contiguous(), A[:, sl].contiguous()
+            dA_off = off
+            off += self.rsum * d_in
+            dB_off = off
+            off += d_out * self.rsum
+            self.projs.append(_Proj(name, d_in, d_out, kind, group, in_l, out_l, W, A, B, dA_off, dB_off))
+        self.flat_grad = torch.zeros(off, dtype=torch.float32, device=self.device)
+        self.ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    def _randn(self, shape, std, g):
+        return (torch.randn(shape, generator=g, device=self.device, dtype=torch.float32) * std).to(self.dtype)
+
+    # ------------------------------------------------------------------ buffers
+    def input_width(self, group: str) -> int:
+        for p in self.projs:
+            if p.group == group:
+                return p.in_l
+        raise KeyError(group)
+
+    def groups(self):
+        seen = []
+        for p in self.projs:
+            if p.group not in seen:
+                seen.append(p.group)
+        return seen
+
+    def alloc_io(self, T: int, seed: int = 1):
+        """Synthetic activations X per input group and upstream grads dY per projection
+        (values ~ N(0,1)); outputs Y / dX buffers."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        io = {"X": {}, "dY": {}, "Y": {}, "dX": {}}
+        for grp in self.groups():
+            w = self.input_width(grp)
+            io["X"][grp] = torch.randn((T, w), generator=g, device=self.device).to(self.dtype)
+            io["dX"][grp] = torch.empty((T, w), device=self.device, dtype=self.dtype)
+        for p in self.projs:
+            io["dY"][p.name] = torch.randn((T, p.out_l), generator=g, device=self.device).to(self.dtype)
+            io["Y"][p.name] = torch.empty((T, p.out_l), device=self.device, dtype=self.dtype)
+        return io
+
+    def _ensure(self, seq_lens, seq_task):
+        need = 0
+        for p in self.projs:
+            need = max(need, _lib.lobra_lora_workspace_bytes(self.code, p.in_l, p.out_l, seq_lens,
+                                                             seq_task, self.ranks, self.scales))
+            hs = _lib.lobra_lora_saved_bytes(self.code, p.in_l, p.out_l, seq_lens, seq_task,
+                                             self.ranks, self.scales)
+            if p.Hs is None or p.Hs.numel() < hs:
+                p.Hs = torch.empty(hs, dtype=torch.uint8, device=self.device)
+        if self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+
+    def _grads(self, p):
+        fg = self.flat_grad
+        dA = fg[p.dA_off:p.dA_off + self.rsum * p.d_in]
+        dB = fg[p.dB_off:p.dB_off + p.d_out * self.rsum]
+        dA_ld = 0
+        if p.kind == "row":   # this rank's column slice of dA_full
+            dA = dA[self.tp_rank * p.in_l:]
+            dA_ld = p.d_in
+        else:                 # this rank's rows of dB_full
+            dB = dB[self.tp_rank * p.out_l * self.rsum:]
+        return dA, dB, dA_ld
+
+    def _tp(self, p):
+        if self.tp_size == 1 or self.comm is None:
+            return _lib.LOBRA_TP_NONE, None
+        return (_lib.LOBRA_TP_COLUMN if p.kind == "col" else _lib.LOBRA_TP_ROW), self.comm
+
+    # ------------------------------------------------------------------ the hot path
+    def forward(self, seq_lens, seq_task, io, T: int, stream=None):
+        self._ensure(seq_lens, seq_task)
+        for p in self.projs:
+            kind, comm = self._tp(p)
+            X = io["X"][p.group][:T]
+            _lib.lobra_lora_fwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task,
+                                io["Y"][p.name][:T], p.Hs, self.ws, tp_kind=kind, comm=comm,
+                                stream=stream)
+
+    def backward(self, seq_lens, seq_task, io, T: int, accumulate_dadb: bool, stream=None):
+        """q/k/v (and gate/up) accumulate into one dX in the kernel epilogue
+        (accumulate_dx); for column-parallel TP only the LAST projection of a group asks
+        the library for the dX all-reduce, which then sums every projection's partial."""
+        last = {p.group: p.name for p in self.projs}
+        seen = set()
+        for p in self.projs:
+            kind, comm = self._tp(p)
+            if kind == _lib.LOBRA_TP_COLUMN and last[p.group] != p.name:
+                kind, comm = _lib.LOBRA_TP_NONE, None
+            dA, dB, dA_ld = self._grads(p)
+            _lib.lobra_lora_bwd(io["X"][p.group][:T], p.W, p.A, p.B, self.ranks, self.scales,
+                                seq_lens, seq_task, p.Hs, io["dY"][p.name][:T],
+                                io["dX"][p.group][:T], dA, dB, self.ws,
+                                accumulate_dx=p.group in seen, accumulate_dadb=accumulate_dadb,
+                                dA_ld=dA_ld, tp_kind=kind, comm=comm, stream=stream)
+            seen.add(p.group)
+
+    def sync_adapter_grads(self, stream=None):
+        if self.comm is not None and self.comm.world > 1:
+            _lib.lobra_adapter_allreduce(self.comm, self.flat_grad, stream=stream)
