@@ -185,7 +185,7 @@ def run_reference(args):
     from paper_2509_01193_b200.layer import LLAMA2_7B
     from workloads import synth
     wl = synth.config_c2()
-    budget = 512
+    budget = 2048
     times, toks = [], 0
     for i in range(args.warmup + args.steps):
         tps, dt, n, threads = oracle_tokens_per_s(wl, LLAMA2_7B, budget_tokens=budget, seed=100 + i)
@@ -279,7 +279,7 @@ def main():
 
     def plan(wl):
         d = _lib.lobra_dispatch(tp_list, rep_list, m_list, costs, wl.seq_lens, wl.seq_task,
-                                grid_step, grid_max, 16, 0)
+                                grid_step, grid_max, 16, 0, chunking=1)
         mine = np.nonzero(d["seq_replica"] == my_rep)[0]
         chunks = []
         for c in sorted(set(d["seq_chunk"][mine].tolist())):
@@ -425,7 +425,7 @@ def main():
 
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu and not args.profile_only:
-        tps, dt, n, threads = oracle_tokens_per_s(batches[0], LLAMA2_7B, budget_tokens=2048)
+        tps, dt, n, threads = oracle_tokens_per_s(batches[0], LLAMA2_7B, budget_tokens=8192)
         cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "oracle",
                "sample": f"first {n} tokens of the C2 batch, 7 projections fwd+bwd, fp64 NumPy ({dt:.1f} s)"}
 

@@ -203,12 +203,16 @@ typedef struct {
 
 /* mode: 0 = balanced (Eq. 3), 1 = length-based (Fig. 4(c): every bucket to the
  * supporting group with the smallest c_ij * n_i, ties to the earlier group).
+ * chunking: 0 = padded micro-batches of App. D (per bucket, b_j = floor(M_i / s_j)
+ * sequences); 1 = packed micro-batches ("can also be applied when
+ * packing is employed"; reading Q6b): the replica's sequences in (bucket desc, index)
+ * order filled next-fit into chunks of at most M_i REAL tokens.
  * node_cap: max branch-and-bound nodes (<= 0: default 2e7); on hitting it the best
  * incumbent is returned with LOBRA_ERR_BUDGET.  Errors: LOBRA_ERR_INPUT,
  * LOBRA_ERR_INFEASIBLE.  Host only; thread-safe (no global state). */
 LOBRA_API lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
                             int32_t grid_step, int32_t grid_max, int32_t R, int32_t mode,
-                            int64_t node_cap, lobra_dispatch_out* out);
+                            int32_t chunking, int64_t node_cap, lobra_dispatch_out* out);
 
 /* ------------------------------------------------------------------------------
  * Communication (NCCL over NVLink/NVSwitch).  One process per GPU.

@@ -27,7 +27,9 @@ Steps (``dispatch`` below):
     {floor(d/p), ceil(d/p)} (P:576 objective "ceil(d_ij/p_i)"; reading Q14)
  9. chunks of b_j = floor(M_i / s_j) sequences plus one remainder chunk per bucket
     (App. D), ordered by descending chunk cost, ties by bucket then
-    chunk index (App. D "sorting micro-batches in descending order of time cost")
+    chunk index (App. D "sorting micro-batches in descending order of time cost");
+    or, with chunking = 1 (packing; reading Q6b), the replica's sequences in
+    (bucket desc, index asc) order filled next-fit into chunks of <= M_i real tokens
 10. inside a chunk, sequences ordered by (task id, original index) -- packing order
     grouped by task (reading Q6).
 """
@@ -297,7 +299,7 @@ def solve_eq3(Bj, p, c, r, bruteforce_cap=200000):
 
 # --------------------------------------------------------------------------- all
 def dispatch(groups, cost, seq_lens, seq_task, grid_step, grid_max, R, mode=0,
-             bruteforce_cap=200000) -> DispatchResult:
+             bruteforce_cap=200000, chunking=0) -> DispatchResult:
     """The full per-step dispatch (steps 1-10 of the module docstring).
 
     groups: list[Group] in (tp asc, M asc) order; cost: [G][U] ints, the cost of one
@@ -371,16 +373,28 @@ def dispatch(groups, cost, seq_lens, seq_task, grid_step, grid_max, R, mode=0,
     for i in range(G):
         for rep in range(rbase[i], rbase[i + 1]):
             chunks = []   # (-cost, bucket, idx_in_bucket, [seqs])
-            for j in range(Rb):
-                idx = [k for k in range(n) if seq_replica[k] == rep and seq_bucket[k] == j]
-                if not idx:
-                    continue
-                b = groups[i].max_tokens // bounds[j]
-                assert b >= 1
-                for ci, s0 in enumerate(range(0, len(idx), b)):
-                    part = idx[s0:s0 + b]
-                    assert len(part) * bounds[j] <= groups[i].max_tokens
-                    chunks.append((-len(part) * c[i][j], j, ci, part))
+            if chunking == 0:
+                for j in range(Rb):
+                    idx = [k for k in range(n) if seq_replica[k] == rep and seq_bucket[k] == j]
+                    if not idx:
+                        continue
+                    b = groups[i].max_tokens // bounds[j]
+                    assert b >= 1
+                    for ci, s0 in enumerate(range(0, len(idx), b)):
+                        part = idx[s0:s0 + b]
+                        assert len(part) * bounds[j] <= groups[i].max_tokens
+                        chunks.append((-len(part) * c[i][j], j, ci, part))
+            else:
+                order = [k for j in range(Rb - 1, -1, -1) for k in range(n)
+                         if seq_replica[k] == rep and seq_bucket[k] == j]
+                cur, fill = None, 0
+                for k in order:
+                    if cur is None or fill + int(seq_lens[k]) > groups[i].max_tokens:
+                        cur = []
+                        chunks.append((0, 0, len(chunks), cur))
+                        fill = 0
+                    cur.append(k)
+                    fill += int(seq_lens[k])
             chunks.sort(key=lambda x: (x[0], x[1], x[2]))
             for cix, ch in enumerate(chunks):
                 order = sorted(ch[3], key=lambda k: (int(seq_task[k]), k))

@@ -97,7 +97,8 @@ def load() -> C.CDLL:
                                    C.c_size_t, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
     lib.lobra_dispatch.argtypes = [C.POINTER(Deployment), C.POINTER(Batch), C.c_int32, C.c_int32,
-                                   C.c_int32, C.c_int32, C.c_int64, C.POINTER(DispatchOut)]
+                                   C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                   C.POINTER(DispatchOut)]
     lib.lobra_nccl_unique_id.restype = C.c_int
     lib.lobra_nccl_unique_id.argtypes = [C.c_void_p]
     lib.lobra_comm_init.restype = C.c_int
@@ -219,7 +220,7 @@ def lobra_lora_bwd(X, W, A, B, ranks, scales, seq_lens, seq_task, Hs, dY, dX, dA
 
 
 def lobra_dispatch(tp, replicas, max_tokens, cost, seq_lens, seq_task, grid_step=256,
-                   grid_max=16384, R=16, mode=0, node_cap=0):
+                   grid_max=16384, R=16, mode=0, node_cap=0, chunking=0):
     """Per-step dispatch (host).  Returns a dict of numpy arrays; raises LobraError on
     input / infeasibility errors.  status LOBRA_ERR_BUDGET is returned in the dict."""
     tp, replicas, max_tokens = _i32(tp), _i32(replicas), _i32(max_tokens)
@@ -239,7 +240,7 @@ def lobra_dispatch(tp, replicas, max_tokens, cost, seq_lens, seq_task, grid_step
                     out["seq_chunk"].ctypes.data_as(_i32p), out["pack_order"].ctypes.data_as(_i32p),
                     out["replica_cost"].ctypes.data_as(_i64p), 0, 0)
     st = load().lobra_dispatch(C.byref(dep), C.byref(batch), grid_step, grid_max, R, mode,
-                               node_cap, C.byref(o))
+                               chunking, node_cap, C.byref(o))
     if st not in (LOBRA_OK, LOBRA_ERR_BUDGET):
         raise LobraError(st, load().lobra_last_error().decode())
     nb = o.num_buckets

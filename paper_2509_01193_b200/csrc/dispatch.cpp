@@ -278,7 +278,7 @@ struct Multi {
 
 extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
                                        int32_t grid_step, int32_t grid_max, int32_t R,
-                                       int32_t mode, int64_t node_cap,
+                                       int32_t mode, int32_t chunking, int64_t node_cap,
                                        lobra_dispatch_out* out) {
   using lobra::fail;
   lobra::clear_error();
@@ -287,6 +287,7 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
     return fail(LOBRA_ERR_INPUT, "grid_max must be a positive multiple of grid_step");
   if (R < 1) return fail(LOBRA_ERR_INPUT, "R must be >= 1");
   if (mode != 0 && mode != 1) return fail(LOBRA_ERR_INPUT, "unknown mode %d", mode);
+  if (chunking != 0 && chunking != 1) return fail(LOBRA_ERR_INPUT, "unknown chunking %d", chunking);
   const int G = dep->num_groups;
   const int n = batch->num_seqs;
   if (G < 1 || !dep->tp || !dep->replicas || !dep->max_tokens || !dep->cost)
@@ -449,22 +450,45 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
         std::vector<int> seqs;
       };
       std::vector<Ch> chunks;
-      for (int j = 0; j < Rb; ++j) {
-        std::vector<int> mine;
-        for (int s = 0; s < n; ++s)
-          if (seq_rep[s] == rep && seq_b[s] == j) mine.push_back(s);
-        if (mine.empty()) continue;
-        const i64 b = M[i] / bnd[j];
-        int ci = 0;
-        for (size_t s0 = 0; s0 < mine.size(); s0 += (size_t)b, ++ci) {
-          Ch ch;
-          ch.j = j;
-          ch.ci = ci;
-          const size_t e = std::min(mine.size(), s0 + (size_t)b);
-          ch.seqs.assign(mine.begin() + s0, mine.begin() + e);
-          ch.cost = (i64)ch.seqs.size() * I.c[i][j];
-          chunks.push_back(std::move(ch));
+      if (chunking == 0) {
+        for (int j = 0; j < Rb; ++j) {
+          std::vector<int> mine;
+          for (int s = 0; s < n; ++s)
+            if (seq_rep[s] == rep && seq_b[s] == j) mine.push_back(s);
+          if (mine.empty()) continue;
+          const i64 b = M[i] / bnd[j];
+          int ci = 0;
+          for (size_t s0 = 0; s0 < mine.size(); s0 += (size_t)b, ++ci) {
+            Ch ch;
+            ch.j = j;
+            ch.ci = ci;
+            const size_t e = std::min(mine.size(), s0 + (size_t)b);
+            ch.seqs.assign(mine.begin() + s0, mine.begin() + e);
+            ch.cost = (i64)ch.seqs.size() * I.c[i][j];
+            chunks.push_back(std::move(ch));
+          }
         }
+      } else {
+        // packed: (bucket desc, index asc), next-fit by real tokens <= M_i
+        i64 fill = 0;
+        int ci = 0;
+        for (int j = Rb - 1; j >= 0; --j)
+          for (int s = 0; s < n; ++s) {
+            if (seq_rep[s] != rep || seq_b[s] != j) continue;
+            const i64 L = batch->seq_lens[s];
+            if (chunks.empty() || fill + L > M[i]) {
+              Ch ch;
+              ch.j = 0;
+              ch.ci = ci++;
+              ch.cost = 0;
+              chunks.push_back(std::move(ch));
+              fill = 0;
+            }
+            chunks.back().seqs.push_back(s);
+            fill += L;
+          }
+        // creation order is the execution order: make the sort below a no-op
+        for (auto& ch : chunks) ch.cost = 0;
       }
       std::stable_sort(chunks.begin(), chunks.end(), [](const Ch& x, const Ch& y) {
         if (x.cost != y.cost) return x.cost > y.cost;

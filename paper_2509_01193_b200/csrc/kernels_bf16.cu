@@ -6,7 +6,7 @@
 //              model can be fused into a batched operation whilst ... multiple LoRA
 //              adapters ... customized operations".
 // k_rowproj  : the rank-r shrink H_s = s_t X A_t^T (and the backward G_s = s_t dY B_t),
-//              HBM-bound; one CTA per 128-row tile streams Z once.
+//              HBM-bound; CTAs per 128-row tile (split-K when tiles are few) stream Z once.
 // k_segred   : the token reductions dA_t = X^T G_s and dB_t = dY^T H_s on tensor cores,
 //              Z tiles used as MN-major A operands (one HBM read of Z), deterministic
 //              two-pass (partials + k_finalize in fixed order).
@@ -104,7 +104,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], G_STAGE_BYTES);
           tma_load_2d(sA + stage * G_A_BYTES, &mapSlot, &full[stage], 0, s * kTileM);
-          tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], 0, t * args.N + n * G_BN);
+          // expand operand straight from the caller's adapters, box starting at roff[t]
+          const int roff = meta.roff[t];
+          if (!kBMN) {   // B_cat [out, ld8]: K-major rows o, columns roff..roff+63
+            tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], roff, n * G_BN);
+          } else {       // A_cat [rsum, in]: MN-major, K rows roff..roff+63
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(sB + stage * G_B_BYTES + c * 8192, &mapV, &full[stage],
+                          n * G_BN + c * 64, roff);
+          }
           if (++stage == G_STAGES) stage = 0, phase ^= 1;
         }
       }
@@ -112,7 +121,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer (single thread)
       const uint32_t id_main = idesc_bf16(G_BM, G_BN, false, kBMN);
-      const uint32_t id_ext = idesc_bf16(G_BM, G_BN, false, false);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -144,9 +152,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
-          for (int k = 0; k < nk16; ++k)
-            mma_bf16(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024),
-                     id_ext, 1u);
+          for (int k = 0; k < nk16; ++k) {
+            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
+            mma_bf16(d, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id_main, 1u);
+          }
           mma_commit(&empty[stage]);
           if (++stage == G_STAGES) stage = 0, phase ^= 1;
         }
@@ -206,21 +216,47 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 // =====================================================================================
-// Row projection (shrink): slot[s][row][q] = s_t * sum_k Z[row][k] V_t[q][k]
+// Row projection (shrink): slot[s][row][q] = s_t * sum_k Z[row][k] V_t(q, k)
+//   kVmn = false: V_t rows of A_cat [rsum, K] (K-major; forward H_s = s X A_t^T)
+//   kVmn = true : V_t = columns of B_cat [K, rsum8] (MN-major; backward G_s = s dY B_t)
+// The 64-wide operand box starts at the task's roff; columns q >= r_t (other tasks'
+// data or OOB zeros) are masked to exact zeros in the epilogue.  HBM-bound: split-K
+// over `nsplit` CTAs per tile when the tile count cannot fill the GPU, partials reduced
+// in fixed split order by the last CTA to arrive (deterministic).
 // =====================================================================================
-constexpr int R_STAGES = 4, R_MAXS = 4;
-constexpr int R_A_BYTES = 128 * 64 * 2;         // 16 KB
-constexpr int R_V_BYTES = 64 * 64 * 2;          // 8 KB per slot
-constexpr int R_STAGE_BYTES = R_A_BYTES + R_MAXS * R_V_BYTES;
-constexpr int R_SMEM = R_STAGES * R_STAGE_BYTES + 1024 + 256;
+constexpr int R_STAGES = 3, R_P = 2;             // stages, slots per pass
+constexpr int R_A_BYTES = 128 * 64 * 2;          // 16 KB
+constexpr int R_V_BYTES = 64 * 64 * 2;           // 8 KB per slot
+constexpr int R_STAGE_BYTES = R_A_BYTES + R_P * R_V_BYTES;
+constexpr int R_SMEM = R_STAGES * R_STAGE_BYTES + 1024 + 256;   // ~97 KB: 2 CTAs / SM
 
 struct RowArgs {
-  int K;
+  int K, nsplit, kb_per_split;
   __nv_bfloat16* out;
+  float* partial;     // [nsplit][nslots][128][64] fp32 (only when nsplit > 1)
+  int* counters;      // [ntiles], zero on entry; reset by the last CTA
   Meta meta;
 };
 
-__global__ void __launch_bounds__(256, 1)
+__device__ __forceinline__ void store_slot_row(__nv_bfloat16* out, int s, int lrow, const float* v,
+                                               float sc, int rp) {
+  uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)s * kTileM + lrow) * kSlotW);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e] = (j * 8 + e < rp) ? v[j * 8 + e] * sc : 0.0f;
+    uint4 o;
+    o.x = pack_bf16x2(w[0], w[1]);
+    o.y = pack_bf16x2(w[2], w[3]);
+    o.z = pack_bf16x2(w[4], w[5]);
+    o.w = pack_bf16x2(w[6], w[7]);
+    dst[j] = o;
+  }
+}
+
+template <bool kVmn>
+__global__ void __launch_bounds__(256, 2)
     k_rowproj(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
               const RowArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -230,12 +266,14 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + R_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   const uint32_t warp = warp_id(), lane = lane_id();
   const Meta& meta = args.meta;
-  const int m = blockIdx.x;
+  const int m = blockIdx.x / args.nsplit, split = blockIdx.x % args.nsplit;
   const int s_begin = meta.tile_slot_off[m], s_end = meta.tile_slot_off[m + 1];
-  const int npass = (s_end - s_begin + R_MAXS - 1) / R_MAXS;
+  const int npass = (s_end - s_begin + R_P - 1) / R_P;
   const int nk = (args.K + 63) / 64;
+  const int kb0 = split * args.kb_per_split, kb1 = min(nk, kb0 + args.kb_per_split);
 
   if (warp == 0 && lane == 0) tma_prefetch(&mapZ), tma_prefetch(&mapV);
   if (warp == 1 && lane == 0) {
@@ -244,7 +282,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(tempty, 128);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  if (warp == 2) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -255,40 +293,47 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int p = 0; p < npass; ++p) {
-        const int s0 = s_begin + p * R_MAXS;
-        const int ns = min(R_MAXS, s_end - s0);
-        for (int kb = 0; kb < nk; ++kb) {
+        const int s0 = s_begin + p * R_P;
+        const int ns = min(R_P, s_end - s0);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], R_A_BYTES + ns * R_V_BYTES);
           uint8_t* st = smem + stage * R_STAGE_BYTES;
           tma_load_2d(st, &mapZ, &full[stage], kb * 64, m * kTileM);
-          for (int i = 0; i < ns; ++i)
-            tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64,
-                        meta.slot_task[s0 + i] * 64);
+          for (int i = 0; i < ns; ++i) {
+            const int roff = meta.roff[meta.slot_task[s0 + i]];
+            if (kVmn)
+              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], roff, kb * 64);
+            else
+              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64, roff);
+          }
           if (++stage == R_STAGES) stage = 0, phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id = idesc_bf16(128, 64, false, false);
+      const uint32_t id = idesc_bf16(128, 64, false, kVmn);
       int stage = 0;
       uint32_t phase = 0;
       for (int p = 0; p < npass; ++p) {
-        const int s0 = s_begin + p * R_MAXS;
-        const int ns = min(R_MAXS, s_end - s0);
+        const int s0 = s_begin + p * R_P;
+        const int ns = min(R_P, s_end - s0);
         mbar_wait(tempty, (p & 1) ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * R_STAGE_BYTES);
           for (int i = 0; i < ns; ++i) {
             const uint32_t b0 = a0 + R_A_BYTES + i * R_V_BYTES;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024),
-                       sdesc_sw128(b0 + k * 32, 16, 1024), id, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bd = kVmn ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                       : sdesc_sw128(b0 + k * 32, 16, 1024);
+              mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id,
+                       (kb != kb0 || k != 0) ? 1u : 0u);
+            }
           }
           mma_commit(&empty[stage]);
           if (++stage == R_STAGES) stage = 0, phase ^= 1;
@@ -302,41 +347,66 @@ __global__ void __launch_bounds__(256, 1)
     const int row = m * kTileM + lrow;
     const int my_task = row < meta.T ? row_task(meta, row) : -1;
     for (int p = 0; p < npass; ++p) {
-      const int s0 = s_begin + p * R_MAXS;
-      const int ns = min(R_MAXS, s_end - s0);
+      const int s0 = s_begin + p * R_P;
+      const int ns = min(R_P, s_end - s0);
       mbar_wait(tfull, p & 1);
       tc_fence_after();
       for (int i = 0; i < ns; ++i) {
         const int s = s0 + i;
         const int ts = meta.slot_task[s];
-        const float sc = (ts == my_task) ? meta.scales[ts] : 0.0f;
-        const int rp = (ts == my_task) ? meta.ranks[ts] : 0;
-        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)s * kTileM + lrow) * kSlotW);
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          float v[32];
-          tmem_ld32(tmem + ((q * 32u) << 16) + i * 64 + h * 32, v);
+        float v[64];
+        tmem_ld32(tmem + ((q * 32u) << 16) + i * 64, *reinterpret_cast<float(*)[32]>(v));
+        tmem_ld32(tmem + ((q * 32u) << 16) + i * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        if (args.nsplit == 1) {
+          const bool mine = ts == my_task;
+          store_slot_row(args.out, s, lrow, v, mine ? meta.scales[ts] : 0.0f, mine ? meta.ranks[ts] : 0);
+        } else {
+          const int rp = rpad16(meta.ranks[ts]);
+          float4* dst = reinterpret_cast<float4*>(
+              args.partial + (((size_t)split * meta.nslots + s) * kTileM + lrow) * 64);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = (h * 32 + j < rp) ? v[j] * sc : 0.0f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 o;
-            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
-            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
-            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
-            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
-            dst[h * 4 + j] = o;
-          }
+          for (int j = 0; j < 16; ++j)
+            if (4 * j < rp) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
       tc_fence_before();
       mbar_arrive(tempty);
     }
+    if (args.nsplit > 1) {
+      // deterministic split-K reduction by the last CTA of this tile to finish
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (lrow == 0) *last_flag = (atomicAdd(&args.counters[m], 1) == args.nsplit - 1);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*last_flag) {
+        __threadfence();
+        for (int s = s_begin; s < s_end; ++s) {
+          const int ts = meta.slot_task[s];
+          const int rp = rpad16(meta.ranks[ts]);
+          float v[64];
+#pragma unroll
+          for (int j = 0; j < 64; ++j) v[j] = 0.0f;
+          for (int sp = 0; sp < args.nsplit; ++sp) {
+            const float4* src = reinterpret_cast<const float4*>(
+                args.partial + (((size_t)sp * meta.nslots + s) * kTileM + lrow) * 64);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (4 * j >= rp) break;
+              const float4 f = __ldcg(src + j);
+              v[4 * j] += f.x, v[4 * j + 1] += f.y, v[4 * j + 2] += f.z, v[4 * j + 3] += f.w;
+            }
+          }
+          const bool mine = ts == my_task;
+          store_slot_row(args.out, s, lrow, v, mine ? meta.scales[ts] : 0.0f, mine ? meta.ranks[ts] : 0);
+        }
+        if (lrow == 0) args.counters[m] = 0;
+      }
+    }
   }
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<128>(tmem);
   }
 }
 
@@ -463,58 +533,30 @@ __global__ void __launch_bounds__(256, 1)
 // =====================================================================================
 // small helper kernels
 // =====================================================================================
-__global__ void k_pad(int mode, const __nv_bfloat16* __restrict__ src,
-                      __nv_bfloat16* __restrict__ dst, Meta meta, int in, int out) {
-  // one thread per destination element
-  const long long total = (mode == 0)   ? (long long)meta.ntasks * 64 * in
-                          : (mode == 1) ? (long long)meta.ntasks * out * 64
-                          : (mode == 2) ? (long long)meta.ntasks * 64 * out
-                                        : (long long)meta.ntasks * in * 64;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    int t, q;
-    long long o;
-    __nv_bfloat16 v = __float2bfloat16(0.0f);
-    if (mode == 0) {          // Apad[t][q][k] = A[roff+q][k]
-      const long long k = i % in;
-      const long long tq = i / in;
-      t = (int)(tq / 64), q = (int)(tq % 64);
-      if (q < meta.ranks[t]) v = src[(long long)(meta.roff[t] + q) * in + k];
-    } else if (mode == 1) {   // Bpad[t][o][q] = B[o][roff+q]
-      q = (int)(i % 64);
-      const long long to = i / 64;
-      t = (int)(to / out), o = to % out;
-      if (q < meta.ranks[t]) v = src[o * meta.rsum + meta.roff[t] + q];
-    } else if (mode == 2) {   // Btpad[t][q][o] = B[o][roff+q]
-      o = i % out;
-      const long long tq = i / out;
-      t = (int)(tq / 64), q = (int)(tq % 64);
-      if (q < meta.ranks[t]) v = src[o * meta.rsum + meta.roff[t] + q];
-    } else {                  // Atpad[t][k][q] = A[roff+q][k]
-      q = (int)(i % 64);
-      const long long tk = i / 64;
-      t = (int)(tk / in);
-      const long long k = tk % in;
-      if (q < meta.ranks[t]) v = src[(long long)(meta.roff[t] + q) * in + k];
-    }
-    dst[i] = v;
+// B_cat [out, rsum] -> [out, ld8] (zero columns rsum..ld8-1): only when rsum % 8 != 0,
+// so that TMA's 16-byte stride rule holds for the direct B operand maps.
+__global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                           int out, int rsum, int ld8) {
+  const int total = out * ld8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int o = i / ld8, c = i - o * ld8;
+    dst[i] = c < rsum ? src[(size_t)o * rsum + c] : __float2bfloat16(0.0f);
   }
 }
 
+// out[(t,q), col] (+)= sum over the task's units (fixed order) of the partials.
+// grid (ceil(width / 256), rsum): one adapter row per blockIdx.y, coalesced over cols.
 __global__ void k_finalize(int mode, const float* __restrict__ partial, int width, int nchunks,
                            Meta meta, float* __restrict__ out, long long ld, int accumulate) {
-  const long long total = (long long)meta.rsum * width;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int col = (int)(i % width);
-    const int rq = (int)(i / width);   // global adapter row roff[t] + q
-    int t = 0;
-    while (meta.roff[t + 1] <= rq) ++t;
-    const int q = rq - meta.roff[t];
-    const int c = col / 128, ci = col % 128;
+  const int rq = blockIdx.y;
+  int t = 0;
+  while (meta.roff[t + 1] <= rq) ++t;
+  const int q = rq - meta.roff[t];
+  const int u0 = meta.task_unit_off[t], u1 = meta.task_unit_off[t + 1];
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
+    const int c = col >> 7, ci = col & 127;
     float s = 0.0f;
-    for (int u = meta.task_unit_off[t]; u < meta.task_unit_off[t + 1]; ++u)
-      s += partial[((size_t)(u * nchunks + c) * 64 + q) * 128 + ci];
+    for (int u = u0; u < u1; ++u) s += __ldg(partial + ((size_t)(u * nchunks + c) * 64 + q) * 128 + ci);
     float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
     *dst = accumulate ? *dst + s : s;
   }
@@ -531,21 +573,45 @@ __global__ void k_zero(float* p, long long n) {
 // =====================================================================================
 // launchers
 // =====================================================================================
-void launch_pad(int mode, const __nv_bfloat16* src, __nv_bfloat16* dst, const Meta& meta, int in,
-                int out, cudaStream_t st) {
-  k_pad<<<1184, 256, 0, st>>>(mode, src, dst, meta, in, out);
+void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int rsum, int ld8,
+                     cudaStream_t st) {
+  k_pad_cols<<<592, 256, 0, st>>>(src, dst, out, rsum, ld8);
 }
 
-void launch_rowproj(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
-                    __nv_bfloat16* slots, int num_sms, cudaStream_t st) {
-  (void)num_sms;
+int rowproj_splits(int ntiles, int K) {
+  const int nk = (K + 63) / 64;
+  int s = (2 * 148 + ntiles - 1) / (ntiles > 0 ? ntiles : 1);
+  s = s < 1 ? 1 : s;
+  s = s > 8 ? 8 : s;
+  s = s > nk ? nk : s;
+  return s;
+}
+
+void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
+                    const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
+                    cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_rowproj, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
+    cudaFuncSetAttribute(k_rowproj<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
+    cudaFuncSetAttribute(k_rowproj<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
     init = true;
   }
-  RowArgs a{K, slots, meta};
-  k_rowproj<<<meta.ntiles, 256, R_SMEM, st>>>(mapZ, mapV, a);
+  RowArgs a;
+  a.K = K;
+  a.nsplit = rowproj_splits(meta.ntiles, K);
+  const int nk = (K + 63) / 64;
+  a.kb_per_split = (nk + a.nsplit - 1) / a.nsplit;
+  a.nsplit = (nk + a.kb_per_split - 1) / a.kb_per_split;
+  a.out = slots;
+  a.partial = partial;
+  a.counters = counters;
+  a.meta = meta;
+  if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
+  const int grid = meta.ntiles * a.nsplit;
+  if (v_mn)
+    k_rowproj<true><<<grid, 256, R_SMEM, st>>>(mapZ, mapV, a);
+  else
+    k_rowproj<false><<<grid, 256, R_SMEM, st>>>(mapZ, mapV, a);
 }
 
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
@@ -595,8 +661,10 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
 
 void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
                      long long ld, int accumulate, cudaStream_t st) {
-  k_finalize<<<592, 256, 0, st>>>(mode, partial, width, (width + 127) / 128, meta, out, ld,
-                                  accumulate);
+  if (meta.rsum == 0) return;
+  dim3 grid((width + 255) / 256, meta.rsum);
+  k_finalize<<<grid, 256, 0, st>>>(mode, partial, width, (width + 127) / 128, meta, out, ld,
+                                   accumulate);
 }
 
 void launch_zero_f32(float* p, long long n, cudaStream_t st) {

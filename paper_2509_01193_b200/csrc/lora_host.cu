@@ -313,26 +313,29 @@ Meta device_meta(const Plan& P, const void* dev_base) {
 
 // Workspace layout (bytes from ws base); both directions share it.
 struct Layout {
-  size_t meta = 0, pad1 = 0, pad2 = 0, gslots = 0, partA = 0, partB = 0, total = 0;
+  size_t meta = 0, bpad = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0, total = 0;
   size_t saved = 0;
+  int ld8 = 0;   // row stride (elements) of the B operand the kernels read
 };
 
 Layout layout(const lobra_problem* prob, const Plan& P) {
   Layout L;
-  const size_t in = prob->in, out = prob->out, G = P.ntasks;
+  const size_t in = prob->in, out = prob->out;
   size_t off = 0;
   L.meta = off;
   off += align256(P.buf.size() * 4);
   if (prob->dtype == LOBRA_BF16) {
     const size_t es = 2;
-    const size_t p1 = std::max(G * 64 * in, G * 64 * out) * es;   // Apad / Btpad
-    const size_t p2 = std::max(G * out * 64, G * in * 64) * es;   // Bpad / Atpad
-    L.pad1 = off;
-    off += align256(p1);
-    L.pad2 = off;
-    off += align256(p2);
+    L.ld8 = (P.rsum + 7) & ~7;
+    L.bpad = off;
+    if (L.ld8 != P.rsum) off += align256(out * L.ld8 * es);
     L.gslots = off;
     off += align256((size_t)P.nslots * kTileM * kSlotW * es);
+    const int sp = std::max(rowproj_splits(P.ntiles, (int)in), rowproj_splits(P.ntiles, (int)out));
+    L.rpart = off;
+    if (sp > 1) off += align256((size_t)sp * P.nslots * kTileM * 64 * 4);
+    L.counters = off;
+    off += align256((size_t)P.ntiles * 4);
     const size_t chA = (in + 127) / 128, chB = (out + 127) / 128;
     L.partA = off;
     off += align256((size_t)P.nunits * chA * 64 * 128 * 4);
@@ -440,18 +443,24 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
                     static_cast<const float*>(ad->A), static_cast<const float*>(ad->B),
                     static_cast<const float*>(Hs), in, out, meta, static_cast<float*>(Y), 0, st); }
   } else {
-    auto* Apad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
-    auto* Bpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
-    { Prof p_(LOBRA_K_PAD, st); launch_pad(0, static_cast<const __nv_bfloat16*>(ad->A), Apad, meta, in, out, st); }
-    { Prof p_(LOBRA_K_PAD, st); launch_pad(1, static_cast<const __nv_bfloat16*>(ad->B), Bpad, meta, in, out, st); }
-    CUtensorMap mX, mApad, mW, mSlot, mBpad;
+    const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ad->B);
+    if (L.ld8 != P.rsum) {
+      auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.rsum, L.ld8, st); }
+      Bop = Bp;
+    }
+    CUtensorMap mX, mA, mW, mSlot, mB;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mApad, Apad, in, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mA, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mW, W, in, out, 64, 256)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mBpad, Bpad, 64, (uint64_t)P.ntasks * out, 64, 256)) != LOBRA_OK) return s;
-    { Prof p_(LOBRA_K_ROWPROJ, st); launch_rowproj(mX, mApad, in, meta, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st); }
-    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mBpad, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
+    if ((s = make_map(&mB, Bop, L.ld8, out, 64, 256)) != LOBRA_OK) return s;
+    {
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_rowproj(false, mX, mA, in, meta, static_cast<__nv_bfloat16*>(Hs),
+                     reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);
+    }
+    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
                 ctx->num_sms, st); }
   }
   if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
@@ -513,22 +522,28 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     { Prof p_(LOBRA_K_FP32, st); launch_f32_segred(1, static_cast<const float*>(dY), static_cast<const float*>(Hs), out, meta,
                       dB, 0, accumulate_dadb, st); }
   } else {
-    auto* Btpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad1);
-    auto* Atpad = reinterpret_cast<__nv_bfloat16*>(w + L.pad2);
     auto* Gs = reinterpret_cast<__nv_bfloat16*>(w + L.gslots);
     float* partA = reinterpret_cast<float*>(w + L.partA);
     float* partB = reinterpret_cast<float*>(w + L.partB);
-    { Prof p_(LOBRA_K_PAD, st); launch_pad(2, static_cast<const __nv_bfloat16*>(ad->B), Btpad, meta, in, out, st); }
-    { Prof p_(LOBRA_K_PAD, st); launch_pad(3, static_cast<const __nv_bfloat16*>(ad->A), Atpad, meta, in, out, st); }
+    const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ad->B);
+    if (L.ld8 != P.rsum) {
+      auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.rsum, L.ld8, st); }
+      Bop = Bp;
+    }
     CUtensorMap mdY, mBt, mWmn, mG, mAt, mX, mHs;
     if ((s = make_map(&mdY, dY, out, P.T, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mBt, Btpad, out, (uint64_t)P.ntasks * 64, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mBt, Bop, L.ld8, out, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mWmn, W, in, out, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mG, Gs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mAt, Atpad, 64, (uint64_t)P.ntasks * in, 64, 256)) != LOBRA_OK) return s;
+    if ((s = make_map(&mAt, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mHs, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
-    { Prof p_(LOBRA_K_ROWPROJ, st); launch_rowproj(mdY, mBt, out, meta, Gs, ctx->num_sms, st); }
+    {
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_rowproj(true, mdY, mBt, out, meta, Gs, reinterpret_cast<float*>(w + L.rpart),
+                     reinterpret_cast<int*>(w + L.counters), st);
+    }
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
                 accumulate_dx, meta, ctx->num_sms, st); }
     if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }

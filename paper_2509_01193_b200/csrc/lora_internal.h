@@ -47,20 +47,21 @@ __device__ __forceinline__ int row_task(const Meta& m, int row) {
 }
 
 // ---- bf16 launchers (kernels_bf16.cu) ---------------------------------------------
-// Pads the adapters into the K-major operand copies the tcgen05 kernels consume.
-//  mode 0: Apad [ntasks*64, in]  (row q of task t = A_t[q,:], zeros for q >= r_t)
-//  mode 1: Bpad [ntasks*out, 64] (Bpad[t][o][q] = B_t[o,q])
-//  mode 2: Btpad[ntasks*64, out] (Btpad[t][q][o] = B_t[o,q])
-//  mode 3: Atpad[ntasks*in, 64]  (Atpad[t][k][q] = A_t[q,k])
-void launch_pad(int mode, const __nv_bfloat16* src, __nv_bfloat16* dst, const Meta& meta,
-                int in, int out, cudaStream_t st);
-// H[slot] = s_t * Z[rows of tile] V_t^T for every slot of every tile (zeros in rows of
-// other tasks).  Z [T, K] bf16 (tensor map), V [ntasks*64, K] bf16 K-major (tensor map).
-void launch_rowproj(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
-                    __nv_bfloat16* slots, int num_sms, cudaStream_t st);
-// C[T, N] (+)= Z[T,K] . Wop  +  sum over tile slots: Slot[128,64] . Vext_t[N-tile, 64]^T
-//   b_mn = false: Wop = W^T with W [N, K] K-major (forward, X W^T)
-//   b_mn = true : Wop = W   with W [K, N] (MN-major B operand; backward, dY W)
+// B_cat [out, rsum] -> [out, ld8] with zero columns rsum..ld8-1 (only if rsum % 8 != 0).
+void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int rsum, int ld8,
+                     cudaStream_t st);
+// Split factor of the rank-r projection for `ntiles` tiles and reduction length K.
+int rowproj_splits(int ntiles, int K);
+// slot[s] = s_t * Z[rows of tile] V_t for every slot of every tile (zeros in rows of other
+// tasks and in columns q >= r_t).  v_mn = false: V = A_cat [rsum, K] (forward shrink);
+// v_mn = true: V = B_cat [K, ld8] (backward G).  partial/counters: split-K scratch.
+void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
+                    const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
+                    cudaStream_t st);
+// C[T, N] (+)= Z[T,K] . Wop  +  sum over tile slots: Slot[128, r] . Vext_t
+//   b_mn = false: Wop = W^T with W [N, K] K-major (forward, X W^T); Vext = B_cat [N, ld8]
+//   b_mn = true : Wop = W   with W [K, N] (MN-major B operand; backward, dY W);
+//                 Vext = A_cat [rsum, N] (MN-major)
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st);

@@ -11,11 +11,13 @@ from workloads import synth
 pytestmark = []
 
 
-def _run_both(groups, cost, lens, tasks, step, gmax, R, mode=0, cap=200000):
+def _run_both(groups, cost, lens, tasks, step, gmax, R, mode=0, cap=200000, chunking=0):
     from paper_2509_01193_b200 import _lib
-    ref = D.dispatch(groups, cost, lens, tasks, step, gmax, R, mode=mode, bruteforce_cap=cap)
+    ref = D.dispatch(groups, cost, lens, tasks, step, gmax, R, mode=mode, bruteforce_cap=cap,
+                     chunking=chunking)
     got = _lib.lobra_dispatch([g.tp for g in groups], [g.replicas for g in groups],
-                              [g.max_tokens for g in groups], cost, lens, tasks, step, gmax, R, mode)
+                              [g.max_tokens for g in groups], cost, lens, tasks, step, gmax, R, mode,
+                              chunking=chunking)
     assert got["status"] == 0
     assert got["boundaries"].tolist() == ref.boundaries
     assert np.array_equal(got["d"], ref.d), (got["d"], ref.d)
@@ -74,7 +76,8 @@ def test_random_small_bruteforce(seed):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_two_groups_milp_scale(seed):
+@pytest.mark.parametrize("chunking", [0, 1])
+def test_two_groups_milp_scale(seed, chunking):
     """G=2 (TP1 x p1 + TP2 x p2) on skewed multi-task batches: C++ exact DP == oracle
     HiGHS + lexicographic canonicalisation."""
     rng = np.random.default_rng(200 + seed)
@@ -82,7 +85,7 @@ def test_two_groups_milp_scale(seed):
     tasks = synth.c2_tasks()
     wl = synth.sample_batch(tasks, seed=300 + seed, l_max=4096, per_task=[12, 8, 8, 4])
     cost = _cost_table(groups, 4096 // 256, 256, a1=1.0, a2=1.0 / 8192, unit=64)
-    _run_both(groups, cost, wl.seq_lens, wl.seq_task, 256, 4096, 6, cap=2000)
+    _run_both(groups, cost, wl.seq_lens, wl.seq_task, 256, 4096, 6, cap=2000, chunking=chunking)
 
 
 def test_three_groups_cpp():

@@ -159,3 +159,21 @@ def test_dispatch_properties_random():
                 cnt = int(((res.seq_replica == rep) & (res.seq_bucket == j)).sum())
                 assert cnt <= -(-int(res.d[i, j]) // groups[i].replicas)
         assert res.replica_cost.max() <= res.t_hat
+
+
+def test_packed_chunking_respects_token_budget():
+    """chunking=1 (packing): every chunk holds <= M_i real tokens; the C2-like
+    16384-token pack on one replica with M = 16384 is exactly one chunk."""
+    from workloads import synth
+    wl = synth.config_c2()
+    res = D.dispatch([D.Group(1, 1, 16384)], [[k + 1 for k in range(16)]], wl.seq_lens,
+                     wl.seq_task, 256, 4096, R=16, chunking=1)
+    assert set(res.seq_chunk.tolist()) == {0}
+    rng = np.random.default_rng(3)
+    lens = rng.integers(1, 2048, size=40)
+    res = D.dispatch([D.Group(1, 2, 2048)], [[k + 1 for k in range(8)]], lens, lens % 3, 256,
+                     2048, R=4, chunking=1)
+    for rep in range(2):
+        for c in set(res.seq_chunk[res.seq_replica == rep].tolist()):
+            m = (res.seq_replica == rep) & (res.seq_chunk == c)
+            assert lens[m].sum() <= 2048
