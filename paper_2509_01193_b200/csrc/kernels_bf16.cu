@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int rp = rpad16(meta.ranks[meta.unit_task[u]]);
-      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * 64) * 128 + q * 32 + lane;
+      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * meta.qp) * 128 + q * 32 + lane;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         if (h * 32 >= rp) break;
@@ -556,7 +556,7 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
     const int c = col >> 7, ci = col & 127;
     float s = 0.0f;
-    for (int u = u0; u < u1; ++u) s += __ldg(partial + ((size_t)(u * nchunks + c) * 64 + q) * 128 + ci);
+    for (int u = u0; u < u1; ++u) s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + q) * 128 + ci);
     float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
     *dst = accumulate ? *dst + s : s;
   }
@@ -579,8 +579,10 @@ void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int 
 }
 
 int rowproj_splits(int ntiles, int K) {
+  // one wave of similar-size CTAs (2 resident per SM on 148 SMs): HBM-bound, so what
+  // matters is that every resident CTA streams the same number of bytes
   const int nk = (K + 63) / 64;
-  int s = (2 * 148 + ntiles - 1) / (ntiles > 0 ? ntiles : 1);
+  int s = ntiles > 0 ? (2 * 148) / ntiles : 1;
   s = s < 1 ? 1 : s;
   s = s > 8 ? 8 : s;
   s = s > nk ? nk : s;

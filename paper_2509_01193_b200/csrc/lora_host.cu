@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -162,7 +163,7 @@ struct Plan {
   // offsets (in int32 words) of each array inside buf
   int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
       o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_scales;
-  int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0;
+  int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -240,16 +241,19 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
       if (slot_task[s] == t) task_slots.push_back(s);
     task_slot_off[t + 1] = (int)task_slots.size();
   }
-  // reduction units: split each task's slot list so that units x chunks ~ 2 waves
+  // reduction units: each task's slot list split into near-equal contiguous ranges so
+  // that units x chunks ~ 4 items per SM of equal cost (balanced persistent schedule)
   const int nchunks = std::max(1, (width_hint + 127) / 128);
-  const long long target = 2LL * std::max(num_sms, 1);
-  int per = (int)std::max<long long>(1, ((long long)P.nslots * nchunks + target - 1) / target);
+  const double target = 4.0 * std::max(num_sms, 1);
+  const double per = std::max(1.0, (double)P.nslots * nchunks / target);
   std::vector<int> unit_task, unit_s0, unit_s1, task_unit_off(G + 1, 0);
   for (int t = 0; t < G; ++t) {
-    for (int s = task_slot_off[t]; s < task_slot_off[t + 1]; s += per) {
+    const int n_t = task_slot_off[t + 1] - task_slot_off[t];
+    const int nu = n_t ? std::max(1, (int)std::lround(n_t / per)) : 0;
+    for (int u = 0; u < nu; ++u) {
       unit_task.push_back(t);
-      unit_s0.push_back(s);
-      unit_s1.push_back(std::min(task_slot_off[t + 1], s + per));
+      unit_s0.push_back(task_slot_off[t] + (int)((long long)n_t * u / nu));
+      unit_s1.push_back(task_slot_off[t] + (int)((long long)n_t * (u + 1) / nu));
     }
     task_unit_off[t + 1] = (int)unit_task.size();
   }
@@ -257,6 +261,8 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   std::vector<int> roff(G + 1, 0);
   for (int t = 0; t < G; ++t) roff[t + 1] = roff[t] + ad->ranks[t];
   P.rsum = roff[G];
+  P.qp = 16;
+  for (int t = 0; t < G; ++t) P.qp = std::max(P.qp, (ad->ranks[t] + 15) & ~15);
   // serialize
   P.buf.clear();
   auto put = [&](const std::vector<int>& v) {
@@ -294,6 +300,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.nunits = P.nunits;
   m.rsum = P.rsum;
   m.max_slots_per_tile = P.max_slots;
+  m.qp = P.qp;
   m.seg_off = d + P.o_seg_off;
   m.seg_task = d + P.o_seg_task;
   m.tile_slot_off = d + P.o_tile_slot_off;
@@ -338,9 +345,9 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     off += align256((size_t)P.ntiles * 4);
     const size_t chA = (in + 127) / 128, chB = (out + 127) / 128;
     L.partA = off;
-    off += align256((size_t)P.nunits * chA * 64 * 128 * 4);
+    off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
     L.partB = off;
-    off += align256((size_t)P.nunits * chB * 64 * 128 * 4);
+    off += align256((size_t)P.nunits * chB * P.qp * 128 * 4);
     L.saved = (size_t)P.nslots * kTileM * kSlotW * es;
   } else {
     L.gslots = off;
@@ -375,6 +382,15 @@ lobra_status check_launch(const char* what) {
   return LOBRA_OK;
 }
 
+int sms_hint() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+    return n;
+  cudaGetLastError();
+  return 148;   // B200
+}
+
 lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobra_adapters* ad,
                      int width_hint, int num_sms, Plan& P, Layout& L) {
   lobra_status st = validate(prob, b, ad);
@@ -397,8 +413,10 @@ extern "C" size_t lobra_lora_workspace_bytes(const lobra_problem* prob, const lo
   clear_error();
   Plan P;
   Layout L;
-  // the unit split depends on the SM count; size for the worst case (1 slot per unit)
-  if (prepare(prob, batch, ad, 128, 1 << 20, P, L) != LOBRA_OK) return 0;
+  // the reduction-unit split depends on the SM count of the current device
+  if (prepare(prob, batch, ad, (int)std::min(prob ? prob->in : 1, prob ? prob->out : 1),
+              sms_hint(), P, L) != LOBRA_OK)
+    return 0;
   return L.total;
 }
 
@@ -420,7 +438,9 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
   DevCtx* ctx = nullptr;
   Plan P;
   Layout L;
-  lobra_status s = prepare(prob, batch, ad, (int)prob->in, 1 << 20, P, L);
+  lobra_status s = validate(prob, batch, ad);
+  if (s != LOBRA_OK) return s;
+  s = prepare(prob, batch, ad, (int)std::min(prob->in, prob->out), sms_hint(), P, L);
   if (s != LOBRA_OK) return s;
   if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
   if (!X || !W || !Y || !Hs || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");

@@ -21,6 +21,7 @@ constexpr int kSlotW = 64;      // slot width: ranks padded to 64 columns (r_t <
 //             reductions dA/dB (deterministic two-pass reduction)
 struct Meta {
   int T, nseg, ntiles, nslots, ntasks, nunits, rsum, max_slots_per_tile;
+  int qp;                    // max over tasks of rank padded to 16 (partials' q stride)
   const int* seg_off;        // [nseg+1]
   const int* seg_task;       // [nseg]
   const int* tile_slot_off;  // [ntiles+1]

@@ -45,6 +45,27 @@ def algorithmic_flops(shapes, T: int, ranks, tokens_per_task=None) -> dict:
     return {"base": base, "lora": lora, "total": base + lora}
 
 
+def shard(kind: str, tp_size: int, tp_rank: int, d_in: int, d_out: int):
+    """Megatron TP slices of one projection: column-parallel shards `out`
+    (W rows, B_t rows), row-parallel shards `in` (W columns, A_t columns)."""
+    if kind == "col":
+        o = d_out // tp_size
+        return slice(0, d_in), slice(tp_rank * o, (tp_rank + 1) * o)
+    i = d_in // tp_size
+    return slice(tp_rank * i, (tp_rank + 1) * i), slice(0, d_out)
+
+
+def grad_offsets(kind: str, tp_rank: int, in_l: int, out_l: int, d_in: int, rsum: int):
+    """Where this rank writes its partial adapter gradients inside one projection's
+    full-size [dA_full (rsum x d_in) | dB_full (d_out x rsum)] block of the flat buffer:
+    (dA element offset, dA row stride, dB element offset).  Column rank: partial dA over
+    its out-shard (full rows), its own dB rows.  Row rank: its dA column slice (row stride
+    d_in), partial dB over its in-shard."""
+    if kind == "row":
+        return tp_rank * in_l, d_in, 0
+    return 0, d_in, tp_rank * out_l * rsum
+
+
 @dataclass
 class _Proj:
     name: str
@@ -88,12 +109,10 @@ class LoraLayer:
             A = self._randn((self.rsum, d_in), 1 / math.sqrt(d_in), g)
             Bparts = [self._randn((d_out, int(r)), 1 / math.sqrt(int(r)), g) for r in self.ranks]
             B = torch.cat(Bparts, dim=1)
-            if kind == "col":
-                sl = slice(tp_rank * out_l, (tp_rank + 1) * out_l)
-                W, B = W[sl].contiguous(), B[sl].contiguous()
-            else:
-                sl = slice(tp_rank * in_l, (tp_rank + 1) * in_l)
-                W, A = W[:, sl].contiguous(), A[:, sl].contiguous()
+            si, so = shard(kind, tp_size, tp_rank, d_in, d_out)
+            W = W[so, si].contiguous()
+            A = A[:, si].contiguous()
+            B = B[so].contiguous()
             dA_off = off
             off += self.rsum * d_in
             dB_off = off
@@ -147,16 +166,11 @@ class LoraLayer:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
 
     def _grads(self, p):
+        a_off, a_ld, b_off = grad_offsets(p.kind, self.tp_rank, p.in_l, p.out_l, p.d_in, self.rsum)
         fg = self.flat_grad
-        dA = fg[p.dA_off:p.dA_off + self.rsum * p.d_in]
-        dB = fg[p.dB_off:p.dB_off + p.d_out * self.rsum]
-        dA_ld = 0
-        if p.kind == "row":   # this rank's column slice of dA_full
-            dA = dA[self.tp_rank * p.in_l:]
-            dA_ld = p.d_in
-        else:                 # this rank's rows of dB_full
-            dB = dB[self.tp_rank * p.out_l * self.rsum:]
-        return dA, dB, dA_ld
+        dA = fg[p.dA_off + a_off:p.dA_off + self.rsum * p.d_in]
+        dB = fg[p.dB_off + b_off:p.dB_off + p.d_out * self.rsum]
+        return dA, dB, a_ld
 
     def _tp(self, p):
         if self.tp_size == 1 or self.comm is None:

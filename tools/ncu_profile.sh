@@ -1,0 +1,22 @@
+#!/bin/bash
+# ncu evidence for the bench workload (run under gpurun, 1 GPU; never multi-rank).
+#   tools/ncu_profile.sh <tag>
+# 1) every library launch of one bench step with its device time (cold-cache, serialised)
+# 2) one `--set full` capture each of the fwd/bwd GEMM, the rank-r projection and the
+#    token reduction (q projection, first step).
+set -x
+TAG=${1:-r1}
+OUT=gpurun_out
+K='regex:k_(gemm|rowproj|segred|finalize|pad_cols)'
+B="python bench.py --steps 1 --warmup 1 --profile-only --no-cpu --no-e2e"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
+    --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 0 -c 1 \
+    -o $OUT/prof_gemm_fwd_$TAG $B > $OUT/ncu_gemm_fwd_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 7 -c 1 \
+    -o $OUT/prof_gemm_bwd_$TAG $B > $OUT/ncu_gemm_bwd_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rowproj -s 0 -c 1 \
+    -o $OUT/prof_rowproj_$TAG $B > $OUT/ncu_rowproj_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_segred -s 0 -c 1 \
+    -o $OUT/prof_segred_$TAG $B > $OUT/ncu_segred_$TAG.log 2>&1
+ls -la $OUT
