@@ -215,3 +215,99 @@ def test_bf16_c2_q_projection_full_size():
 
 def _bwd_adapters_only(X, W, A, B, ranks, scales, lens, tasks, dY):
     return O.lora_bwd(X, W, A, B, ranks, scales, lens, tasks, dY, want_dx=False)
+
+
+def _full_size_check(wl, d_in, d_out, seed, row_stride):
+    """Y/dX on sampled rows (every `row_stride`-th row + the first sequence), dA_t/dB_t
+    in full, at the bench launch configuration."""
+    t = synth.layer_tensors(wl, d_in, d_out, seed=seed)
+    Y, dX, dA, dB, _ = run_lib("bf16", wl, t, d_in, d_out)
+    ti = oracle_inputs("bf16", t)
+    rows = np.unique(np.concatenate([np.arange(0, wl.T, row_stride), np.arange(0, wl.seq_lens[0])]))
+    row_task = np.repeat(wl.seq_task, wl.seq_lens)[rows]
+    args = (ti["X"][rows], ti["W"], ti["A"], ti["B"], wl.ranks.tolist(), wl.scales,
+            np.ones(len(rows), np.int32), row_task)
+    errs = {"Y": O.max_rel_err(Y[rows], O.lora_fwd(*args)),
+            "dX": O.max_rel_err(dX[rows], O.lora_bwd(*args, ti["dY"][rows])[0])}
+    fargs = (ti["X"], ti["W"], ti["A"], ti["B"], wl.ranks.tolist(), wl.scales, wl.seq_lens, wl.seq_task)
+    _, dAo, dBo = _bwd_adapters_only(*fargs, ti["dY"])
+    roff = np.concatenate([[0], np.cumsum(wl.ranks)])
+    for k in range(len(wl.ranks)):
+        if (wl.seq_task == k).any():
+            errs[f"dA{k}"] = O.max_rel_err(dA[roff[k]:roff[k + 1]], dAo[roff[k]:roff[k + 1]])
+            errs[f"dB{k}"] = O.max_rel_err(dB[:, roff[k]:roff[k + 1]], dBo[:, roff[k]:roff[k + 1]])
+    bad = {k: v for k, v in errs.items() if not v < BF16_TOL}
+    assert not bad, (bad, errs)
+
+
+def test_bf16_c2_down_projection_full_size():
+    """BASELINE config 2, the down projection 11008 -> 4096 (K = 172 blocks of 64)."""
+    _full_size_check(synth.config_c2(), 11008, 4096, seed=22, row_stride=97)
+
+
+def test_bf16_c3_q_projection_full_size():
+    """BASELINE config 3: 16 tasks, ranks 8/16/32/64, scales 0.5/1/2/4, long-tail lengths
+    up to 16K packed into T = 65536, q projection 4096 -> 4096."""
+    _full_size_check(synth.config_c3(), 4096, 4096, seed=23, row_stride=211)
+
+
+def _wl(lens, tasks, ranks, scales):
+    ts = [synth.TaskSpec(f"t{i}", 0, 0, 1, r, s) for i, (r, s) in enumerate(zip(ranks, scales))]
+    return synth.Workload("edge", ts, np.array(lens, np.int32), np.array(tasks, np.int32), 0)
+
+
+@pytest.mark.parametrize("case", [
+    # (lens, tasks, ranks, scales, in, out)
+    ([1], [0], [16], [2.0], 64, 64),                                   # one token
+    ([0, 5, 0, 3], [1, 0, 1, 0], [8, 4], [1.0, 3.0], 128, 64),         # zero-length seqs, task w/o tokens
+    ([3, 2, 4, 1, 5, 2, 3, 1, 2, 6], list(range(10)), [1, 2, 3, 5, 7, 9, 11, 13, 17, 64],
+     [0.5, 1, 2, 4, 0.5, 1, 2, 4, 0.5, 1], 192, 320),                  # 10 tasks in one tile, odd ranks (B padding path)
+    ([130, 1, 127, 256, 2], [2, 0, 1, 2, 0], [64, 64, 64], [1.0, 1.0, 1.0], 64, 128),  # rank 64, one K block
+    ([300] * 3 + [7] * 20, [0, 1, 2] + [i % 3 for i in range(20)], [16, 32, 48], [2.0, 1.0, 0.5], 256, 256),
+])
+def test_bf16_edge_cases(case):
+    lens, tasks, ranks, scales, d_in, d_out = case
+    wl = _wl(lens, tasks, ranks, scales)
+    t = synth.layer_tensors(wl, d_in, d_out, seed=31)
+    check_all(wl, oracle_inputs("bf16", t), run_lib("bf16", wl, t, d_in, d_out), BF16_TOL, d_in, d_out)
+
+
+@pytest.mark.parametrize("case", [
+    ([1], [0], [16], [2.0], 7, 5),
+    ([0, 5, 0, 3, 40], [1, 0, 1, 0, 2], [8, 4, 1], [1.0, 3.0, -2.0], 33, 70),
+])
+def test_fp32_edge_cases(case):
+    lens, tasks, ranks, scales, d_in, d_out = case
+    wl = _wl(lens, tasks, ranks, scales)
+    t = synth.layer_tensors(wl, d_in, d_out, seed=32)
+    check_all(wl, oracle_inputs("fp32", t), run_lib("fp32", wl, t, d_in, d_out), FP32_TOL, d_in, d_out)
+
+
+def test_bf16_deterministic():
+    """Two identical calls give bit-identical outputs (fixed-order reductions, no atomics
+    in the value path)."""
+    wl = _medium(seed=12)
+    t = synth.layer_tensors(wl, 256, 256, seed=33)
+    a = run_lib("bf16", wl, t, 256, 256)
+    b = run_lib("bf16", wl, t, 256, 256)
+    for x, y in zip(a[:4], b[:4]):
+        assert np.array_equal(x, y)
+
+
+def test_abi_rejects_bad_input_before_launch():
+    torch = _torch()
+    from paper_2509_01193_b200 import _lib
+    dev = torch.device("cuda:0")
+    X = torch.zeros(4, 100, device=dev, dtype=torch.bfloat16)     # in not a multiple of 64
+    W = torch.zeros(64, 100, device=dev, dtype=torch.bfloat16)
+    with pytest.raises(_lib.LobraError) as e:
+        _lib.lobra_lora_fwd(X, W, W, W, [4], [1.0], [4], [0], X, X, X, ws_bytes=1 << 20)
+    assert e.value.status == _lib.LOBRA_ERR_INPUT
+    X = torch.zeros(4, 64, device=dev, dtype=torch.bfloat16)
+    W = torch.zeros(64, 64, device=dev, dtype=torch.bfloat16)
+    with pytest.raises(_lib.LobraError) as e:                        # task id out of range
+        _lib.lobra_lora_fwd(X, W, W, W, [4], [1.0], [4], [3], X, X, X, ws_bytes=1 << 20)
+    assert e.value.status == _lib.LOBRA_ERR_INPUT
+    with pytest.raises(_lib.LobraError) as e:                        # rank 65
+        _lib.lobra_lora_fwd(X, W, W, W, [65], [1.0], [4], [0], X, X, X, ws_bytes=1 << 20)
+    assert e.value.status == _lib.LOBRA_ERR_INPUT
