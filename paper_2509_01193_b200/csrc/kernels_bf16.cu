@@ -105,14 +105,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           mbar_expect_tx(&full[stage], G_STAGE_BYTES);
           tma_load_2d(sA + stage * G_A_BYTES, &mapSlot, &full[stage], 0, s * kTileM);
           // expand operand straight from the caller's adapters, box starting at roff[t]
-          const int roff = meta.roff[t];
-          if (!kBMN) {   // B_cat [out, ld8]: K-major rows o, columns roff..roff+63
-            tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], roff, n * G_BN);
+          if (!kBMN) {   // B operand [out, ld8]: K-major rows o, columns boff..boff+63
+            tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], meta.boff[t], n * G_BN);
           } else {       // A_cat [rsum, in]: MN-major, K rows roff..roff+63
 #pragma unroll
             for (int c = 0; c < 4; ++c)
               tma_load_2d(sB + stage * G_B_BYTES + c * 8192, &mapV, &full[stage],
-                          n * G_BN + c * 64, roff);
+                          n * G_BN + c * 64, meta.roff[t]);
           }
           if (++stage == G_STAGES) stage = 0, phase ^= 1;
         }
@@ -301,11 +300,11 @@ __global__ void __launch_bounds__(256, 2)
           uint8_t* st = smem + stage * R_STAGE_BYTES;
           tma_load_2d(st, &mapZ, &full[stage], kb * 64, m * kTileM);
           for (int i = 0; i < ns; ++i) {
-            const int roff = meta.roff[meta.slot_task[s0 + i]];
-            if (kVmn)
-              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], roff, kb * 64);
-            else
-              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64, roff);
+            const int t = meta.slot_task[s0 + i];
+            if (kVmn)   // B operand [out, ld8], columns boff..boff+63 (MN-major)
+              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], meta.boff[t], kb * 64);
+            else        // A_cat [rsum, in], rows roff..roff+63 (K-major)
+              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64, meta.roff[t]);
           }
           if (++stage == R_STAGES) stage = 0, phase ^= 1;
         }
@@ -533,14 +532,16 @@ __global__ void __launch_bounds__(256, 1)
 // =====================================================================================
 // small helper kernels
 // =====================================================================================
-// B_cat [out, rsum] -> [out, ld8] (zero columns rsum..ld8-1): only when rsum % 8 != 0,
-// so that TMA's 16-byte stride rule holds for the direct B operand maps.
+// B_cat [out, rsum] -> Bp [out, ld8]: task t's r_t columns at boff[t], zero padding.
 __global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                           int out, int rsum, int ld8) {
+                           int out, int ld8, Meta meta) {
   const int total = out * ld8;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int o = i / ld8, c = i - o * ld8;
-    dst[i] = c < rsum ? src[(size_t)o * rsum + c] : __float2bfloat16(0.0f);
+    int t = 0;
+    while (t + 1 < meta.ntasks && meta.boff[t + 1] <= c) ++t;
+    const int q = c - meta.boff[t];
+    dst[i] = q < meta.ranks[t] ? src[(size_t)o * meta.rsum + meta.roff[t] + q] : __float2bfloat16(0.0f);
   }
 }
 
@@ -573,9 +574,9 @@ __global__ void k_zero(float* p, long long n) {
 // =====================================================================================
 // launchers
 // =====================================================================================
-void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int rsum, int ld8,
-                     cudaStream_t st) {
-  k_pad_cols<<<592, 256, 0, st>>>(src, dst, out, rsum, ld8);
+void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int ld8,
+                     const Meta& meta, cudaStream_t st) {
+  k_pad_cols<<<592, 256, 0, st>>>(src, dst, out, ld8, meta);
 }
 
 int rowproj_splits(int ntiles, int K) {

@@ -162,7 +162,10 @@ struct Plan {
   std::vector<int32_t> buf;  // serialized int32 metadata (floats bit-cast)
   // offsets (in int32 words) of each array inside buf
   int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
-      o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_scales;
+      o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_boff,
+      o_scales;
+  int ld8 = 0;      // row stride of the B operand the kernels read (rsum if direct)
+  bool bdirect = true;
   int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16;
 };
 
@@ -284,6 +287,12 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   P.o_task_unit_off = put(task_unit_off);
   P.o_ranks = put(std::vector<int>(ad->ranks, ad->ranks + G));
   P.o_roff = put(roff);
+  std::vector<int> boff(G + 1, 0);
+  P.bdirect = true;
+  for (int t = 0; t < G; ++t) P.bdirect &= (ad->ranks[t] % 8) == 0;
+  for (int t = 0; t < G; ++t) boff[t + 1] = boff[t] + (P.bdirect ? ad->ranks[t] : (ad->ranks[t] + 7) & ~7);
+  P.ld8 = boff[G];
+  P.o_boff = put(boff);
   std::vector<int> sc(G);
   std::memcpy(sc.data(), ad->scales, sizeof(float) * G);
   P.o_scales = put(sc);
@@ -314,6 +323,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.task_unit_off = d + P.o_task_unit_off;
   m.ranks = d + P.o_ranks;
   m.roff = d + P.o_roff;
+  m.boff = d + P.o_boff;
   m.scales = reinterpret_cast<const float*>(d + P.o_scales);
   return m;
 }
@@ -333,9 +343,9 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
   off += align256(P.buf.size() * 4);
   if (prob->dtype == LOBRA_BF16) {
     const size_t es = 2;
-    L.ld8 = (P.rsum + 7) & ~7;
+    L.ld8 = P.ld8;
     L.bpad = off;
-    if (L.ld8 != P.rsum) off += align256(out * L.ld8 * es);
+    if (!P.bdirect) off += align256(out * L.ld8 * es);
     L.gslots = off;
     off += align256((size_t)P.nslots * kTileM * kSlotW * es);
     const int sp = std::max(rowproj_splits(P.ntiles, (int)in), rowproj_splits(P.ntiles, (int)out));
@@ -464,9 +474,9 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
                     static_cast<const float*>(Hs), in, out, meta, static_cast<float*>(Y), 0, st); }
   } else {
     const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ad->B);
-    if (L.ld8 != P.rsum) {
+    if (!P.bdirect) {
       auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
-      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.rsum, L.ld8, st); }
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, L.ld8, meta, st); }
       Bop = Bp;
     }
     CUtensorMap mX, mA, mW, mSlot, mB;
@@ -546,9 +556,9 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     float* partA = reinterpret_cast<float*>(w + L.partA);
     float* partB = reinterpret_cast<float*>(w + L.partB);
     const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ad->B);
-    if (L.ld8 != P.rsum) {
+    if (!P.bdirect) {
       auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
-      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.rsum, L.ld8, st); }
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, L.ld8, meta, st); }
       Bop = Bp;
     }
     CUtensorMap mdY, mBt, mWmn, mG, mAt, mX, mHs;

@@ -35,6 +35,8 @@ struct Meta {
   const int* task_unit_off;  // [ntasks+1]
   const int* ranks;          // [ntasks]
   const int* roff;           // [ntasks+1]
+  const int* boff;           // [ntasks+1] task column offset in the B operand the kernels read
+                             // (== roff when every rank is a multiple of 8, else the padded copy's)
   const float* scales;       // [ntasks]
 };
 
@@ -48,9 +50,11 @@ __device__ __forceinline__ int row_task(const Meta& m, int row) {
 }
 
 // ---- bf16 launchers (kernels_bf16.cu) ---------------------------------------------
-// B_cat [out, rsum] -> [out, ld8] with zero columns rsum..ld8-1 (only if rsum % 8 != 0).
-void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int rsum, int ld8,
-                     cudaStream_t st);
+// B_cat [out, rsum] -> Bp [out, ld8] with task t's columns at boff[t] (8-aligned, zero
+// padded): only when some rank is not a multiple of 8 (TMA needs 16-byte aligned inner
+// coordinates and strides).
+void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int ld8,
+                     const Meta& meta, cudaStream_t st);
 // Split factor of the rank-r projection for `ntiles` tiles and reduction length K.
 int rowproj_splits(int ntiles, int K);
 // slot[s] = s_t * Z[rows of tile] V_t for every slot of every tile (zeros in rows of other
