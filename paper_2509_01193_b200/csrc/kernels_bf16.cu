@@ -13,6 +13,8 @@
 // See DESIGN.md "Kernels" for layouts and the roofline of each.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "lora_internal.h"
 #include "ptx.cuh"
 
@@ -215,6 +217,228 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 // =====================================================================================
+// 2-CTA GEMM with fused K-extension (cta_group::2): a CTA pair computes a 256 x 256 tile,
+// each CTA loads its own 128 rows of A and HALF (128 columns) of B, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) and each CTA drains its 128 accumulator rows.
+// Per CTA and K step: 32 KB of operands for 128 x 256 outputs (vs 48 KB for the 1-CTA
+// kernel) -> two thirds of the L2->SM operand traffic.
+// K-extension across the pair: the union of the two M tiles' tasks; a CTA whose tile lacks
+// a task feeds the all-zero slot (index meta.nslots) for that step.
+// =====================================================================================
+constexpr int P_BK = 64, P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * P_BK * 2;    // 16 KB: this CTA's 128 rows
+constexpr int P_B_BYTES = 128 * P_BK * 2;    // 16 KB: this CTA's half of the 256 B columns
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+struct Gemm2Args {
+  int T, N, K, ntm2, ntn, accumulate;
+  __nv_bfloat16* C;
+  Meta meta;
+};
+
+__device__ __forceinline__ int tile_slot_begin(const Meta& m, int tile) {
+  return tile < m.ntiles ? m.tile_slot_off[tile] : 0;
+}
+__device__ __forceinline__ int tile_slot_end(const Meta& m, int tile) {
+  return tile < m.ntiles ? m.tile_slot_off[tile + 1] : 0;
+}
+// slot of `task` in `tile`, or the zero slot
+__device__ __forceinline__ int find_slot(const Meta& m, int tile, int task) {
+  for (int s = tile_slot_begin(m, tile); s < tile_slot_end(m, tile); ++s)
+    if (m.slot_task[s] == task) return s;
+  return m.nslots;
+}
+
+// Calls f(task, my_slot) for the union of the pair's tasks (tile A's order, then tile B's
+// new tasks); identical sequence in both CTAs.
+template <typename F>
+__device__ __forceinline__ void for_union(const Meta& m, int tA, int tB, uint32_t rank, F&& f) {
+  for (int s = tile_slot_begin(m, tA); s < tile_slot_end(m, tA); ++s) {
+    const int t = m.slot_task[s];
+    f(t, rank == 0 ? s : find_slot(m, tB, t));
+  }
+  for (int s = tile_slot_begin(m, tB); s < tile_slot_end(m, tB); ++s) {
+    const int t = m.slot_task[s];
+    if (find_slot(m, tA, t) != m.nslots) continue;
+    f(t, rank == 1 ? s : m.nslots);
+  }
+}
+
+template <bool kBMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW,
+            const __grid_constant__ CUtensorMap mapSlot, const __grid_constant__ CUtensorMap mapV,
+            const Gemm2Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P_STAGES * P_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_B_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapZ);
+    tma_prefetch(&mapW);
+    tma_prefetch(&mapSlot);
+    tma_prefetch(&mapV);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < P_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 8);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int npt = args.ntm2 * args.ntn;
+  const int nk = (args.K + P_BK - 1) / P_BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const Meta& meta = args.meta;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pt = cid; pt < npt; pt += ncl) {
+        const int mp = pt / args.ntn, n = pt % args.ntn;
+        const int m = 2 * mp + rank;
+        const int ncol = n * 256 + rank * 128;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = mapa(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          tma_load_2d_pair(sA + stage * P_A_BYTES, &mapZ, fb, kb * P_BK, m * 128);
+          if (!kBMN) {
+            tma_load_2d_pair(sB + stage * P_B_BYTES, &mapW, fb, kb * P_BK, ncol);
+          } else {
+            tma_load_2d_pair(sB + stage * P_B_BYTES, &mapW, fb, ncol, kb * P_BK);
+            tma_load_2d_pair(sB + stage * P_B_BYTES + 8192, &mapW, fb, ncol + 64, kb * P_BK);
+          }
+          if (++stage == P_STAGES) stage = 0, phase ^= 1;
+        }
+        for_union(meta, 2 * mp, 2 * mp + 1, rank, [&](int t, int my_slot) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = mapa(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          tma_load_2d_pair(sA + stage * P_A_BYTES, &mapSlot, fb, 0, my_slot * kTileM);
+          if (!kBMN) {
+            tma_load_2d_pair(sB + stage * P_B_BYTES, &mapV, fb, meta.boff[t], ncol);
+          } else {
+            tma_load_2d_pair(sB + stage * P_B_BYTES, &mapV, fb, ncol, meta.roff[t]);
+            tma_load_2d_pair(sB + stage * P_B_BYTES + 8192, &mapV, fb, ncol + 64, meta.roff[t]);
+          }
+          if (++stage == P_STAGES) stage = 0, phase ^= 1;
+        });
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader CTA only)
+      const uint32_t id = idesc_bf16(256, 256, false, kBMN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int pt = cid; pt < npt; pt += ncl, ++it) {
+        const int mp = pt / args.ntn;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 256;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * P_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * P_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < P_BK / 16; ++k) {
+            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
+            mma_bf16_pair(d, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == P_STAGES) stage = 0, phase ^= 1;
+        }
+        for_union(meta, 2 * mp, 2 * mp + 1, 0, [&](int t, int) {
+          const int nk16 = rpad16(meta.ranks[t]) / 16;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * P_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * P_B_BYTES);
+          for (int k = 0; k < nk16; ++k) {
+            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
+            mma_bf16_pair(d, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id, 1u);
+          }
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == P_STAGES) stage = 0, phase ^= 1;
+        });
+        mma_commit_pair(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): own 128 rows
+    const uint32_t q = warp - 4;
+    int it = 0;
+    for (int pt = cid; pt < npt; pt += ncl, ++it) {
+      const int mp = pt / args.ntn, n = pt % args.ntn;
+      const int m = 2 * mp + rank;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = m * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((q * 32u) << 16) + acc * 256 + c * 32, v);
+        const int col0 = n * 256 + c * 32;
+        if (row < args.T && col0 < args.N) {
+          uint4* dst = reinterpret_cast<uint4*>(args.C + (size_t)row * args.N + col0);
+          if (args.accumulate) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 o = dst[j];
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                v[j * 8 + 2 * e] += f.x;
+                v[j * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 o;
+            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+            dst[j] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tempty[acc]), 0));
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
+// =====================================================================================
 // Row projection (shrink): slot[s][row][q] = s_t * sum_k Z[row][k] V_t(q, k)
 //   kVmn = false: V_t rows of A_cat [rsum, K] (K-major; forward H_s = s X A_t^T)
 //   kVmn = true : V_t = columns of B_cat [K, rsum8] (MN-major; backward G_s = s dY B_t)
@@ -345,6 +569,12 @@ __global__ void __launch_bounds__(256, 2)
     const int lrow = q * 32 + lane;
     const int row = m * kTileM + lrow;
     const int my_task = row < meta.T ? row_task(meta, row) : -1;
+    if (blockIdx.x == 0) {   // the all-zero slot (index nslots) used by the 2-CTA GEMM
+      float z[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) z[j] = 0.0f;
+      store_slot_row(args.out, meta.nslots, lrow, z, 0.0f, 0);
+    }
     for (int p = 0; p < npass; ++p) {
       const int s0 = s_begin + p * R_P;
       const int ns = min(R_P, s_end - s0);
@@ -617,15 +847,41 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
     k_rowproj<false><<<grid, 256, R_SMEM, st>>>(mapZ, mapV, a);
 }
 
+bool gemm_uses_pair() {
+  const char* e = getenv("LOBRA_GEMM_1CTA");
+  return !(e && e[0] == '1');
+}
+
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms,
                  cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static int use_pair = -1;
+  if (use_pair < 0) {
+    use_pair = gemm_uses_pair() ? 1 : 0;
     cudaFuncSetAttribute(k_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
     cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
-    init = true;
+    cudaFuncSetAttribute(k_gemm2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    cudaFuncSetAttribute(k_gemm2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+  }
+  if (use_pair) {
+    Gemm2Args a;
+    a.T = T;
+    a.N = N;
+    a.K = K;
+    a.ntm2 = (T + 255) / 256;
+    a.ntn = (N + 255) / 256;
+    a.accumulate = accumulate;
+    a.C = C;
+    a.meta = meta;
+    const int tiles = a.ntm2 * a.ntn;
+    int clusters = num_sms / 2;
+    if (tiles < clusters) clusters = tiles;
+    if (b_mn)
+      k_gemm2<true><<<2 * clusters, G_THREADS, P_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+    else
+      k_gemm2<false><<<2 * clusters, G_THREADS, P_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+    return;
   }
   GemmArgs a;
   a.T = T;

@@ -346,8 +346,8 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     L.ld8 = P.ld8;
     L.bpad = off;
     if (!P.bdirect) off += align256(out * L.ld8 * es);
-    L.gslots = off;
-    off += align256((size_t)P.nslots * kTileM * kSlotW * es);
+    L.gslots = off;   // + one all-zero slot (index nslots)
+    off += align256((size_t)(P.nslots + 1) * kTileM * kSlotW * es);
     const int sp = std::max(rowproj_splits(P.ntiles, (int)in), rowproj_splits(P.ntiles, (int)out));
     L.rpart = off;
     if (sp > 1) off += align256((size_t)sp * P.nslots * kTileM * 64 * 4);
@@ -358,7 +358,7 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
     L.partB = off;
     off += align256((size_t)P.nunits * chB * P.qp * 128 * 4);
-    L.saved = (size_t)P.nslots * kTileM * kSlotW * es;
+    L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * es;
   } else {
     L.gslots = off;
     off += align256((size_t)P.T * kSlotW * 4);
@@ -482,9 +482,10 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
     CUtensorMap mX, mA, mW, mSlot, mB;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mA, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
-    if ((s = make_map(&mW, W, in, out, 64, 256)) != LOBRA_OK) return s;
-    if ((s = make_map(&mSlot, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mB, Bop, L.ld8, out, 64, 256)) != LOBRA_OK) return s;
+    const uint32_t bn = gemm_uses_pair() ? 128 : 256;
+    if ((s = make_map(&mW, W, in, out, 64, bn)) != LOBRA_OK) return s;
+    if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mB, Bop, L.ld8, out, 64, bn)) != LOBRA_OK) return s;
     {
       Prof p_(LOBRA_K_ROWPROJ, st);
       launch_rowproj(false, mX, mA, in, meta, static_cast<__nv_bfloat16*>(Hs),
@@ -565,10 +566,10 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mdY, dY, out, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mBt, Bop, L.ld8, out, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mWmn, W, in, out, 64, 64)) != LOBRA_OK) return s;
-    if ((s = make_map(&mG, Gs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mG, Gs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mAt, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
-    if ((s = make_map(&mHs, Hs, 64, (uint64_t)P.nslots * kTileM, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     {
       Prof p_(LOBRA_K_ROWPROJ, st);
       launch_rowproj(true, mdY, mBt, out, meta, Gs, reinterpret_cast<float*>(w + L.rpart),

@@ -67,6 +67,9 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
 //   b_mn = false: Wop = W^T with W [N, K] K-major (forward, X W^T); Vext = B_cat [N, ld8]
 //   b_mn = true : Wop = W   with W [K, N] (MN-major B operand; backward, dY W);
 //                 Vext = A_cat [rsum, N] (MN-major)
+// true: the 2-CTA (cta_group::2) GEMM is used; its B boxes are 128 rows/columns per CTA
+// (env LOBRA_GEMM_1CTA=1 selects the 1-CTA kernel with 256-wide boxes).
+bool gemm_uses_pair();
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st);
