@@ -7,13 +7,13 @@
 set -x
 TAG=${1:-r1}
 OUT=gpurun_out
-K='regex:k_(gemm|rowproj|segred|finalize|pad_cols)'
+K="regex:k_(gemm|gemm2|rowproj|segred|finalize|pad_cols)"
 B="python bench.py --steps 1 --warmup 1 --profile-only --no-cpu --no-e2e"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
     --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 0 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm2 -s 0 -c 1 \
     -o $OUT/prof_gemm_fwd_$TAG $B > $OUT/ncu_gemm_fwd_$TAG.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 7 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm2 -s 7 -c 1 \
     -o $OUT/prof_gemm_bwd_$TAG $B > $OUT/ncu_gemm_bwd_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rowproj -s 0 -c 1 \
     -o $OUT/prof_rowproj_$TAG $B > $OUT/ncu_rowproj_$TAG.log 2>&1
