@@ -603,12 +603,12 @@ __global__ void __launch_bounds__(256, 2)
     }
     if (args.nsplit > 1) {
       // deterministic split-K reduction by the last CTA of this tile to finish
-      __threadfence();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (lrow == 0) *last_flag = (atomicAdd(&args.counters[m], 1) == args.nsplit - 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int s = s_begin; s < s_end; ++s) {
           const int ts = meta.slot_task[s];
           const int rp = rpad16(meta.ranks[ts]);
@@ -758,23 +758,32 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive(&tempty[acc]);
       // the last unit of (task, chunk) to finish sums all the task's unit partials in
       // unit order (deterministic) and writes dA / dB
-      __threadfence();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (lcol == 0) *last_flag = (atomicAdd(&args.counters[t * args.nchunks + c], 1) ==
                                    meta.task_unit_off[t + 1] - meta.task_unit_off[t] - 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         const int col = c * 128 + lcol;
         const int r = meta.ranks[t], ro = meta.roff[t];
+        // unit-outer, rank-inner: the rank loads of one unit are independent (ILP)
+        float sum[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) sum[j] = 0.0f;
+        for (int uu = meta.task_unit_off[t]; uu < meta.task_unit_off[t + 1]; ++uu) {
+          const float* src = args.partial + ((size_t)(uu * args.nchunks + c) * meta.qp) * 128 + lcol;
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < r) sum[j] += __ldcg(src + (size_t)j * 128);
+        }
         if (col < args.width) {
-          for (int qq = 0; qq < r; ++qq) {
-            float acc_v = 0.0f;
-            for (int uu = meta.task_unit_off[t]; uu < meta.task_unit_off[t + 1]; ++uu)
-              acc_v += __ldcg(args.partial + ((size_t)(uu * args.nchunks + c) * meta.qp + qq) * 128 + lcol);
-            float* o = args.mode == 0 ? args.out + (long long)(ro + qq) * args.ld + col
-                                      : args.out + (long long)col * meta.rsum + ro + qq;
-            *o = args.accumulate ? *o + acc_v : acc_v;
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            if (j >= r) break;
+            float* o = args.mode == 0 ? args.out + (long long)(ro + j) * args.ld + col
+                                      : args.out + (long long)col * meta.rsum + ro + j;
+            *o = args.accumulate ? *o + sum[j] : sum[j];
           }
         }
         if (lcol == 0) args.counters[t * args.nchunks + c] = 0;
