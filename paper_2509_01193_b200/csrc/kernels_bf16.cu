@@ -8,8 +8,8 @@
 // k_rowproj  : the rank-r shrink H_s = s_t X A_t^T (and the backward G_s = s_t dY B_t),
 //              HBM-bound; CTAs per 128-row tile (split-K when tiles are few) stream Z once.
 // k_segred   : the token reductions dA_t = X^T G_s and dB_t = dY^T H_s on tensor cores,
-//              Z tiles used as MN-major A operands (one HBM read of Z); deterministic:
-//              unit partials summed in fixed order by the last unit of each (task, chunk).
+//              Z tiles used as MN-major A operands (one HBM read of Z), deterministic
+//              two-pass (partials + k_finalize in fixed order).
 // See DESIGN.md "Kernels" for layouts and the roofline of each.
 #include <cuda_bf16.h>
 
@@ -650,11 +650,8 @@ constexpr int S_STAGE_BYTES = S_A_BYTES + S_B_BYTES;
 constexpr int S_SMEM = S_STAGES * S_STAGE_BYTES + 1024 + 256;
 
 struct SegArgs {
-  int width, nchunks, nitems, mode, accumulate;
-  long long ld;
+  int width, nchunks, nitems;
   float* partial;
-  float* out;         // mode 0: dA [rsum, ld]; mode 1: dB [width, rsum]
-  int* counters;      // [ntasks * nchunks], zero on entry, reset by the last unit
   Meta meta;
 };
 
@@ -668,7 +665,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + S_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
   const uint32_t warp = warp_id(), lane = lane_id();
   const Meta& meta = args.meta;
 
@@ -741,10 +737,8 @@ __global__ void __launch_bounds__(256, 1)
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int t = meta.unit_task[u];
-      const int rp = rpad16(meta.ranks[t]);
-      const int lcol = q * 32 + lane;
-      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * meta.qp) * 128 + lcol;
+      const int rp = rpad16(meta.ranks[meta.unit_task[u]]);
+      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * meta.qp) * 128 + q * 32 + lane;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         if (h * 32 >= rp) break;
@@ -756,39 +750,6 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // the last unit of (task, chunk) to finish sums all the task's unit partials in
-      // unit order (deterministic) and writes dA / dB
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (lcol == 0) *last_flag = (atomicAdd(&args.counters[t * args.nchunks + c], 1) ==
-                                   meta.task_unit_off[t + 1] - meta.task_unit_off[t] - 1);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*last_flag) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        const int col = c * 128 + lcol;
-        const int r = meta.ranks[t], ro = meta.roff[t];
-        // unit-outer, rank-inner: the rank loads of one unit are independent (ILP)
-        float sum[64];
-#pragma unroll
-        for (int j = 0; j < 64; ++j) sum[j] = 0.0f;
-        for (int uu = meta.task_unit_off[t]; uu < meta.task_unit_off[t + 1]; ++uu) {
-          const float* src = args.partial + ((size_t)(uu * args.nchunks + c) * meta.qp) * 128 + lcol;
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < r) sum[j] += __ldcg(src + (size_t)j * 128);
-        }
-        if (col < args.width) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            if (j >= r) break;
-            float* o = args.mode == 0 ? args.out + (long long)(ro + j) * args.ld + col
-                                      : args.out + (long long)col * meta.rsum + ro + j;
-            *o = args.accumulate ? *o + sum[j] : sum[j];
-          }
-        }
-        if (lcol == 0) args.counters[t * args.nchunks + c] = 0;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
   }
   __syncthreads();
@@ -811,6 +772,24 @@ __global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16*
     while (t + 1 < meta.ntasks && meta.boff[t + 1] <= c) ++t;
     const int q = c - meta.boff[t];
     dst[i] = q < meta.ranks[t] ? src[(size_t)o * meta.rsum + meta.roff[t] + q] : __float2bfloat16(0.0f);
+  }
+}
+
+// out[(t,q), col] (+)= sum over the task's units (fixed order) of the partials.
+// grid (ceil(width / 256), rsum): one adapter row per blockIdx.y, coalesced over cols.
+__global__ void k_finalize(int mode, const float* __restrict__ partial, int width, int nchunks,
+                           Meta meta, float* __restrict__ out, long long ld, int accumulate) {
+  const int rq = blockIdx.y;
+  int t = 0;
+  while (meta.roff[t + 1] <= rq) ++t;
+  const int q = rq - meta.roff[t];
+  const int u0 = meta.task_unit_off[t], u1 = meta.task_unit_off[t + 1];
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
+    const int c = col >> 7, ci = col & 127;
+    float s = 0.0f;
+    for (int u = u0; u < u1; ++u) s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + q) * 128 + ci);
+    float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
+    *dst = accumulate ? *dst + s : s;
   }
 }
 
@@ -922,8 +901,7 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
 }
 
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
-                   const Meta& meta, float* partial, int* counters, int mode, float* out,
-                   long long ld, int accumulate, int num_sms, cudaStream_t st) {
+                   const Meta& meta, float* partial, int num_sms, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_segred, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
@@ -933,17 +911,19 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
   a.width = width;
   a.nchunks = (width + 127) / 128;
   a.nitems = meta.nunits * a.nchunks;
-  a.mode = mode;
-  a.accumulate = accumulate;
-  a.ld = ld;
   a.partial = partial;
-  a.out = out;
-  a.counters = counters;
   a.meta = meta;
   if (a.nitems == 0) return;
-  cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntasks * a.nchunks, st);
   const int grid = a.nitems < num_sms ? a.nitems : num_sms;
   k_segred<<<grid, 256, S_SMEM, st>>>(mapZ, mapSlot, a);
+}
+
+void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
+                     long long ld, int accumulate, cudaStream_t st) {
+  if (meta.rsum == 0) return;
+  dim3 grid((width + 255) / 256, meta.rsum);
+  k_finalize<<<grid, 256, 0, st>>>(mode, partial, width, (width + 127) / 128, meta, out, ld,
+                                   accumulate);
 }
 
 void launch_zero_f32(float* p, long long n, cudaStream_t st) {

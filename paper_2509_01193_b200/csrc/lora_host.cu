@@ -165,7 +165,6 @@ struct Plan {
       o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_boff,
       o_scales;
   int ld8 = 0;      // row stride of the B operand the kernels read (rsum if direct)
-  std::vector<int> task_units, roff_h;   // host copies: units per task, rank offsets
   bool bdirect = true;
   int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16;
 };
@@ -262,12 +261,9 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     task_unit_off[t + 1] = (int)unit_task.size();
   }
   P.nunits = (int)unit_task.size();
-  P.task_units.assign(G, 0);
-  for (int t = 0; t < G; ++t) P.task_units[t] = task_unit_off[t + 1] - task_unit_off[t];
   std::vector<int> roff(G + 1, 0);
   for (int t = 0; t < G; ++t) roff[t + 1] = roff[t] + ad->ranks[t];
   P.rsum = roff[G];
-  P.roff_h = roff;
   P.qp = 16;
   for (int t = 0; t < G; ++t) P.qp = std::max(P.qp, (ad->ranks[t] + 15) & ~15);
   // serialize
@@ -334,8 +330,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
 
 // Workspace layout (bytes from ws base); both directions share it.
 struct Layout {
-  size_t meta = 0, bpad = 0, gslots = 0, rpart = 0, counters = 0, scounters = 0, partA = 0,
-         partB = 0, total = 0;
+  size_t meta = 0, bpad = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0, total = 0;
   size_t saved = 0;
   int ld8 = 0;   // row stride (elements) of the B operand the kernels read
 };
@@ -358,8 +353,6 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     if (sp > 1) off += align256((size_t)sp * P.nslots * kTileM * 64 * 4);
     L.counters = off;
     off += align256((size_t)P.ntiles * 4);
-    L.scounters = off;
-    off += align256((size_t)P.ntasks * std::max((in + 127) / 128, (out + 127) / 128) * 4);
     const size_t chA = (in + 127) / 128, chB = (out + 127) / 128;
     L.partA = off;
     off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
@@ -390,8 +383,6 @@ lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
                 (int)r, (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
   return LOBRA_OK;
 }
-
-int batch_ranks(const lobra_adapters* ad, int t) { return ad->ranks[t]; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -586,23 +577,10 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     }
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
                 accumulate_dx, meta, ctx->num_sms, st); }
-    int* scnt = reinterpret_cast<int*>(w + L.scounters);
-    if (meta.nunits) {
-      Prof p_(LOBRA_K_SEGRED, st);
-      launch_segred(mX, mG, in, meta, partA, scnt, 0, dA, ldA, accumulate_dadb, ctx->num_sms, st);
-    }
-    if (meta.nunits) {
-      Prof p_(LOBRA_K_SEGRED, st);
-      launch_segred(mdY, mHs, out, meta, partB, scnt, 1, dB, 0, accumulate_dadb, ctx->num_sms, st);
-    }
-    if (!accumulate_dadb) {   // tasks without tokens: exact zeros (reading Q10)
-      for (int t = 0; t < P.ntasks; ++t) {
-        if (P.task_units[t]) continue;
-        const int r = batch_ranks(ad, t), ro = P.roff_h[t];
-        cudaMemset2DAsync(dA + (size_t)ro * ldA, ldA * sizeof(float), 0, in * sizeof(float), r, st);
-        cudaMemset2DAsync(dB + ro, P.rsum * sizeof(float), 0, r * sizeof(float), out, st);
-      }
-    }
+    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st); }
+    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta, dB, 0, accumulate_dadb, st); }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
   if (prob->tp_kind == LOBRA_TP_COLUMN) {

@@ -73,13 +73,13 @@ bool gemm_uses_pair();
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st);
-// Token reduction, then fixed-order sum over each task's units by the last unit to finish:
-// mode 0: dA [rsum rows, stride ld] (+)= (Z = X)^T Gslot ; mode 1: dB [width, rsum] (+)=
-// (Z = dY)^T Hslot.  partial/counters: scratch (counters zeroed here).  Tasks without
-// units (no tokens) are not touched.
+// partial[u][chunk][q][128] = sum over the unit's slots: Z[tile rows, chunk cols]^T Slot
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
-                   const Meta& meta, float* partial, int* counters, int mode, float* out,
-                   long long ld, int accumulate, int num_sms, cudaStream_t st);
+                   const Meta& meta, float* partial, int num_sms, cudaStream_t st);
+// out = (accumulate ? out : 0) + sum_u partial   (fixed order). mode 0: dA [r, width] rows
+// with stride ld; mode 1: dB [width, rsum] (PEFT layout, row stride rsum).
+void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
+                     long long ld, int accumulate, cudaStream_t st);
 // Zero (or leave) the dA/dB of every task when the batch has no tokens.
 void launch_zero_f32(float* p, long long n, cudaStream_t st);
 
