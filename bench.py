@@ -216,6 +216,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no e2e/cpu (for ncu)")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="do not record per-kernel CUDA events inside the timed region")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -314,7 +316,7 @@ def main():
     sampler = ClockSampler(local) if rank == 0 or world > 1 else None
     if sampler and rank == 0:
         sampler.start()
-    _lib.lobra_profile_enable(True)
+    _lib.lobra_profile_enable(not args.no_kernel_events)
     _lib.lobra_profile_read(reset=True)
     l0 = _lib.lobra_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <utility>
 
 #include "lora_internal.h"
 #include "ptx.cuh"
@@ -76,6 +77,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   const int ntiles = args.ntm * args.ntn;
   const int nk = (args.K + G_BK - 1) / G_BK;
@@ -299,6 +302,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   const int npt = args.ntm2 * args.ntn;
   const int nk = (args.K + P_BK - 1) / P_BK;
@@ -510,6 +515,8 @@ __global__ void __launch_bounds__(256, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -679,6 +686,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -765,6 +774,8 @@ __global__ void __launch_bounds__(256, 1)
 // B_cat [out, rsum] -> Bp [out, ld8]: task t's r_t columns at boff[t], zero padding.
 __global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                            int out, int ld8, Meta meta) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int total = out * ld8;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int o = i / ld8, c = i - o * ld8;
@@ -779,6 +790,8 @@ __global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16*
 // grid (ceil(width / 256), rsum): one adapter row per blockIdx.y, coalesced over cols.
 __global__ void k_finalize(int mode, const float* __restrict__ partial, int width, int nchunks,
                            Meta meta, float* __restrict__ out, long long ld, int accumulate) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int rq = blockIdx.y;
   int t = 0;
   while (meta.roff[t + 1] <= rq) ++t;
@@ -794,6 +807,8 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
 }
 
 __global__ void k_zero(float* p, long long n) {
+  pdl_wait();
+  pdl_launch_dependents();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     p[i] = 0.0f;
@@ -802,11 +817,37 @@ __global__ void k_zero(float* p, long long n) {
 }  // namespace
 
 // =====================================================================================
-// launchers
+// launchers (programmatic dependent launch unless LOBRA_NO_PDL=1)
 // =====================================================================================
+namespace {
+bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+}  // namespace
 void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int ld8,
                      const Meta& meta, cudaStream_t st) {
-  k_pad_cols<<<592, 256, 0, st>>>(src, dst, out, ld8, meta);
+  launch_k(k_pad_cols, dim3(592), dim3(256), 0, st, src, dst, out, ld8, meta);
 }
 
 int rowproj_splits(int ntiles, int K) {
@@ -842,9 +883,9 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
   const int grid = meta.ntiles * a.nsplit;
   if (v_mn)
-    k_rowproj<true><<<grid, 256, R_SMEM, st>>>(mapZ, mapV, a);
+    launch_k(k_rowproj<true>, dim3(grid), dim3(256), R_SMEM, st, mapZ, mapV, a);
   else
-    k_rowproj<false><<<grid, 256, R_SMEM, st>>>(mapZ, mapV, a);
+    launch_k(k_rowproj<false>, dim3(grid), dim3(256), R_SMEM, st, mapZ, mapV, a);
 }
 
 bool gemm_uses_pair() {
@@ -878,9 +919,9 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
     int clusters = num_sms / 2;
     if (tiles < clusters) clusters = tiles;
     if (b_mn)
-      k_gemm2<true><<<2 * clusters, G_THREADS, P_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+      launch_k(k_gemm2<true>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
     else
-      k_gemm2<false><<<2 * clusters, G_THREADS, P_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+      launch_k(k_gemm2<false>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
     return;
   }
   GemmArgs a;
@@ -895,9 +936,9 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
   const int tiles = a.ntm * a.ntn;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (b_mn)
-    k_gemm<true><<<grid, G_THREADS, G_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+    launch_k(k_gemm<true>, dim3(grid), dim3(G_THREADS), G_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
   else
-    k_gemm<false><<<grid, G_THREADS, G_SMEM, st>>>(mapZ, mapW, mapSlot, mapVext, a);
+    launch_k(k_gemm<false>, dim3(grid), dim3(G_THREADS), G_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
 }
 
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
@@ -915,19 +956,19 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
   a.meta = meta;
   if (a.nitems == 0) return;
   const int grid = a.nitems < num_sms ? a.nitems : num_sms;
-  k_segred<<<grid, 256, S_SMEM, st>>>(mapZ, mapSlot, a);
+  launch_k(k_segred, dim3(grid), dim3(256), S_SMEM, st, mapZ, mapSlot, a);
 }
 
 void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
                      long long ld, int accumulate, cudaStream_t st) {
   if (meta.rsum == 0) return;
   dim3 grid((width + 255) / 256, meta.rsum);
-  k_finalize<<<grid, 256, 0, st>>>(mode, partial, width, (width + 127) / 128, meta, out, ld,
-                                   accumulate);
+  launch_k(k_finalize, grid, dim3(256), 0, st, mode, partial, width, (width + 127) / 128, meta, out,
+           ld, accumulate);
 }
 
 void launch_zero_f32(float* p, long long n, cudaStream_t st) {
-  if (n > 0) k_zero<<<296, 256, 0, st>>>(p, n);
+  if (n > 0) launch_k(k_zero, dim3(296), dim3(256), 0, st, p, n);
 }
 
 }  // namespace lobra
