@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.h"
@@ -49,6 +51,17 @@ void load_nccl() {
   g_nccl.ok = true;
 }
 
+// LOBRA_FORCE_COLLECTIVES=1 issues the NCCL calls even on 1-rank groups (tests exercise
+// the collective path on a single GPU).
+bool force_collectives() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_FORCE_COLLECTIVES");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 lobra_status need_nccl() {
   std::call_once(g_once, load_nccl);
   if (!g_nccl.ok) return fail(LOBRA_ERR_NCCL, "libnccl.so.2 could not be loaded (import torch first)");
@@ -74,7 +87,7 @@ lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaS
   lobra_status s = need_nccl();
   if (s != LOBRA_OK) return s;
   if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
-  if (c->tp_size == 1) return LOBRA_OK;
+  if (c->tp_size == 1 && !force_collectives()) return LOBRA_OK;
   return nccl_check(g_nccl.AllReduce(buf, buf, count, ncclBfloat16, ncclSum, c->tp, st),
                     "TP all-reduce");
 }
@@ -82,7 +95,7 @@ lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaS
   lobra_status s = need_nccl();
   if (s != LOBRA_OK) return s;
   if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
-  if (c->tp_size == 1) return LOBRA_OK;
+  if (c->tp_size == 1 && !force_collectives()) return LOBRA_OK;
   return nccl_check(g_nccl.AllReduce(buf, buf, count, ncclFloat32, ncclSum, c->tp, st),
                     "TP all-reduce");
 }
@@ -156,7 +169,7 @@ extern "C" lobra_status lobra_adapter_allreduce(lobra_comm c, float* flat, size_
   if (!flat && count) return fail(LOBRA_ERR_INPUT, "null buffer");
   lobra_status s = need_nccl();
   if (s != LOBRA_OK) return s;
-  if (c->world_size == 1 || count == 0) return LOBRA_OK;
+  if ((c->world_size == 1 && !force_collectives()) || count == 0) return LOBRA_OK;
   return nccl_check(g_nccl.AllReduce(flat, flat, count, ncclFloat32, ncclSum, c->world,
                                      reinterpret_cast<cudaStream_t>(stream)),
                     "adapter all-reduce");
