@@ -452,11 +452,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
 // over `nsplit` CTAs per tile when the tile count cannot fill the GPU, partials reduced
 // in fixed split order by the last CTA to arrive (deterministic).
 // =====================================================================================
-constexpr int R_STAGES = 3, R_P = 2;             // stages, slots per pass
 constexpr int R_A_BYTES = 128 * 64 * 2;          // 16 KB
 constexpr int R_V_BYTES = 64 * 64 * 2;           // 8 KB per slot
-constexpr int R_STAGE_BYTES = R_A_BYTES + R_P * R_V_BYTES;
-constexpr int R_SMEM = R_STAGES * R_STAGE_BYTES + 1024 + 256;   // ~97 KB: 2 CTAs / SM
+template <int STAGES, int P>
+constexpr int r_smem() { return STAGES * (R_A_BYTES + P * R_V_BYTES) + 1024 + 256; }
 
 struct RowArgs {
   int K, nsplit, kb_per_split;
@@ -483,10 +482,11 @@ __device__ __forceinline__ void store_slot_row(__nv_bfloat16* out, int s, int lr
   }
 }
 
-template <bool kVmn>
-__global__ void __launch_bounds__(256, 2)
+template <bool kVmn, int R_STAGES, int R_P>
+__global__ void __launch_bounds__(256, 1)
     k_rowproj(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
               const RowArgs args) {
+  constexpr int R_STAGE_BYTES = R_A_BYTES + R_P * R_V_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + R_STAGES * R_STAGE_BYTES);
@@ -850,26 +850,52 @@ void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int 
   launch_k(k_pad_cols, dim3(592), dim3(256), 0, st, src, dst, out, ld8, meta);
 }
 
+// rank-r projection configurations: (stages, slots per pass); the resident CTAs per SM
+// follow from the shared memory (2 if <= 113 KB).  LOBRA_RP_CFG selects (tuning).
+struct RpCfg {
+  int stages, p, smem, per_sm;
+};
+static const RpCfg kRpCfg[] = {
+    {3, 2, r_smem<3, 2>(), 2}, {6, 1, r_smem<6, 1>(), 1}, {4, 1, r_smem<4, 1>(), 2},
+    {8, 1, r_smem<8, 1>(), 1}};
+
+int rp_cfg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_RP_CFG");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 3) v = 0;
+  }
+  return v;
+}
+
 int rowproj_splits(int ntiles, int K) {
-  // one wave of similar-size CTAs (2 resident per SM on 148 SMs): HBM-bound, so what
-  // matters is that every resident CTA streams the same number of bytes
+  // one wave of similar-size CTAs: HBM-bound, so what matters is that every resident CTA
+  // streams the same number of bytes
   const int nk = (K + 63) / 64;
-  int s = ntiles > 0 ? (2 * 148) / ntiles : 1;
+  const int slots = kRpCfg[rp_cfg()].per_sm * 148;
+  int s = ntiles > 0 ? slots / ntiles : 1;
   s = s < 1 ? 1 : s;
   s = s > 8 ? 8 : s;
   s = s > nk ? nk : s;
   return s;
 }
 
+template <bool V, int ST, int P>
+void launch_rp(int grid, const CUtensorMap& mapZ, const CUtensorMap& mapV, const RowArgs& a,
+               cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_rowproj<V, ST, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         r_smem<ST, P>());
+    init = true;
+  }
+  launch_k(k_rowproj<V, ST, P>, dim3(grid), dim3(256), r_smem<ST, P>(), st, mapZ, mapV, a);
+}
+
 void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
                     const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
                     cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_rowproj<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
-    cudaFuncSetAttribute(k_rowproj<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, R_SMEM);
-    init = true;
-  }
   RowArgs a;
   a.K = K;
   a.nsplit = rowproj_splits(meta.ntiles, K);
@@ -882,10 +908,16 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   a.meta = meta;
   if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
   const int grid = meta.ntiles * a.nsplit;
-  if (v_mn)
-    launch_k(k_rowproj<true>, dim3(grid), dim3(256), R_SMEM, st, mapZ, mapV, a);
-  else
-    launch_k(k_rowproj<false>, dim3(grid), dim3(256), R_SMEM, st, mapZ, mapV, a);
+  switch (rp_cfg() * 2 + (v_mn ? 1 : 0)) {
+    case 0: launch_rp<false, 3, 2>(grid, mapZ, mapV, a, st); break;
+    case 1: launch_rp<true, 3, 2>(grid, mapZ, mapV, a, st); break;
+    case 2: launch_rp<false, 6, 1>(grid, mapZ, mapV, a, st); break;
+    case 3: launch_rp<true, 6, 1>(grid, mapZ, mapV, a, st); break;
+    case 4: launch_rp<false, 4, 1>(grid, mapZ, mapV, a, st); break;
+    case 5: launch_rp<true, 4, 1>(grid, mapZ, mapV, a, st); break;
+    case 6: launch_rp<false, 8, 1>(grid, mapZ, mapV, a, st); break;
+    default: launch_rp<true, 8, 1>(grid, mapZ, mapV, a, st); break;
+  }
 }
 
 bool gemm_uses_pair() {
