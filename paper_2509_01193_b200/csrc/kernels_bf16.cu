@@ -454,11 +454,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
 // =====================================================================================
 constexpr int R_A_BYTES = 128 * 64 * 2;          // 16 KB
 constexpr int R_V_BYTES = 64 * 64 * 2;           // 8 KB per slot
-template <int STAGES, int P>
-constexpr int r_smem() { return STAGES * (R_A_BYTES + P * R_V_BYTES) + 1024 + 256; }
+template <int STAGES, int P, int KB = 1>
+constexpr int r_smem() { return STAGES * KB * (R_A_BYTES + P * R_V_BYTES) + 1024 + 256; }
 
 struct RowArgs {
-  int K, nsplit, kb_per_split;
+  int K, nsplit, kb_per_split, dbg_no_mma, prefetch;
   __nv_bfloat16* out;
   float* partial;     // [nsplit][nslots][128][64] fp32 (only when nsplit > 1)
   int* counters;      // [ntiles], zero on entry; reset by the last CTA
@@ -482,11 +482,12 @@ __device__ __forceinline__ void store_slot_row(__nv_bfloat16* out, int s, int lr
   }
 }
 
-template <bool kVmn, int R_STAGES, int R_P>
+template <bool kVmn, int R_STAGES, int R_P, int R_KB>
 __global__ void __launch_bounds__(256, 1)
     k_rowproj(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
               const RowArgs args) {
-  constexpr int R_STAGE_BYTES = R_A_BYTES + R_P * R_V_BYTES;
+  // one stage = R_KB consecutive 64-column K blocks: [Z box x R_KB][V slot i box x R_KB]...
+  constexpr int R_STAGE_BYTES = R_KB * (R_A_BYTES + R_P * R_V_BYTES);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + R_STAGES * R_STAGE_BYTES);
@@ -525,17 +526,26 @@ __global__ void __launch_bounds__(256, 1)
       for (int p = 0; p < npass; ++p) {
         const int s0 = s_begin + p * R_P;
         const int ns = min(R_P, s_end - s0);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += R_KB) {
+          const int nkb = min(R_KB, kb1 - kb);
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], R_A_BYTES + ns * R_V_BYTES);
+          mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + ns * R_V_BYTES));
           uint8_t* st = smem + stage * R_STAGE_BYTES;
-          tma_load_2d(st, &mapZ, &full[stage], kb * 64, m * kTileM);
+          if (args.prefetch)   // stream the Z tile into L2 `prefetch` blocks ahead
+            for (int j = 0; j < nkb; ++j)
+              if (kb + j + args.prefetch < kb1)
+                tma_prefetch_2d(&mapZ, (kb + j + args.prefetch) * 64, m * kTileM);
+          for (int j = 0; j < nkb; ++j)
+            tma_load_2d(st + j * R_A_BYTES, &mapZ, &full[stage], (kb + j) * 64, m * kTileM);
           for (int i = 0; i < ns; ++i) {
             const int t = meta.slot_task[s0 + i];
-            if (kVmn)   // B operand [out, ld8], columns boff..boff+63 (MN-major)
-              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], meta.boff[t], kb * 64);
-            else        // A_cat [rsum, in], rows roff..roff+63 (K-major)
-              tma_load_2d(st + R_A_BYTES + i * R_V_BYTES, &mapV, &full[stage], kb * 64, meta.roff[t]);
+            for (int j = 0; j < nkb; ++j) {
+              uint8_t* vd = st + R_KB * R_A_BYTES + (i * R_KB + j) * R_V_BYTES;
+              if (kVmn)   // B operand [out, ld8], columns boff..boff+63 (MN-major)
+                tma_load_2d(vd, &mapV, &full[stage], meta.boff[t], (kb + j) * 64);
+              else        // A_cat [rsum, in], rows roff..roff+63 (K-major)
+                tma_load_2d(vd, &mapV, &full[stage], (kb + j) * 64, meta.roff[t]);
+            }
           }
           if (++stage == R_STAGES) stage = 0, phase ^= 1;
         }
@@ -551,18 +561,27 @@ __global__ void __launch_bounds__(256, 1)
         const int ns = min(R_P, s_end - s0);
         mbar_wait(tempty, (p & 1) ^ 1);
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += R_KB) {
+          const int nkb = min(R_KB, kb1 - kb);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(smem + stage * R_STAGE_BYTES);
+          const uint32_t st0 = smem_u32(smem + stage * R_STAGE_BYTES);
+          if (args.dbg_no_mma) {   // tuning probe: pure TMA streaming, no tensor work
+            mbar_arrive(&empty[stage]);
+            if (++stage == R_STAGES) stage = 0, phase ^= 1;
+            continue;
+          }
           for (int i = 0; i < ns; ++i) {
-            const uint32_t b0 = a0 + R_A_BYTES + i * R_V_BYTES;
+            for (int j = 0; j < nkb; ++j) {
+              const uint32_t a0 = st0 + j * R_A_BYTES;
+              const uint32_t b0 = st0 + R_KB * R_A_BYTES + (i * R_KB + j) * R_V_BYTES;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t bd = kVmn ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
-                                       : sdesc_sw128(b0 + k * 32, 16, 1024);
-              mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id,
-                       (kb != kb0 || k != 0) ? 1u : 0u);
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t bd = kVmn ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                         : sdesc_sw128(b0 + k * 32, 16, 1024);
+                mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id,
+                         (kb != kb0 || j != 0 || k != 0) ? 1u : 0u);
+              }
             }
           }
           mma_commit(&empty[stage]);
@@ -853,18 +872,17 @@ void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int 
 // rank-r projection configurations: (stages, slots per pass); the resident CTAs per SM
 // follow from the shared memory (2 if <= 113 KB).  LOBRA_RP_CFG selects (tuning).
 struct RpCfg {
-  int stages, p, smem, per_sm;
+  int stages, p, kb, per_sm;
 };
-static const RpCfg kRpCfg[] = {
-    {3, 2, r_smem<3, 2>(), 2}, {6, 1, r_smem<6, 1>(), 1}, {4, 1, r_smem<4, 1>(), 2},
-    {8, 1, r_smem<8, 1>(), 1}};
+static const RpCfg kRpCfg[] = {{3, 2, 1, 2}, {6, 1, 1, 1}, {3, 1, 2, 1}, {2, 1, 2, 2},
+                               {4, 1, 2, 1}, {2, 2, 2, 1}};
 
 int rp_cfg() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("LOBRA_RP_CFG");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 3) v = 0;
+    if (v < 0 || v > 5) v = 0;
   }
   return v;
 }
@@ -881,16 +899,16 @@ int rowproj_splits(int ntiles, int K) {
   return s;
 }
 
-template <bool V, int ST, int P>
+template <bool V, int ST, int P, int KB>
 void launch_rp(int grid, const CUtensorMap& mapZ, const CUtensorMap& mapV, const RowArgs& a,
                cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_rowproj<V, ST, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         r_smem<ST, P>());
+    cudaFuncSetAttribute(k_rowproj<V, ST, P, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         r_smem<ST, P, KB>());
     init = true;
   }
-  launch_k(k_rowproj<V, ST, P>, dim3(grid), dim3(256), r_smem<ST, P>(), st, mapZ, mapV, a);
+  launch_k(k_rowproj<V, ST, P, KB>, dim3(grid), dim3(256), r_smem<ST, P, KB>(), st, mapZ, mapV, a);
 }
 
 void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
@@ -898,6 +916,12 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
                     cudaStream_t st) {
   RowArgs a;
   a.K = K;
+  {
+    const char* e = getenv("LOBRA_DBG_RP_NOMMA");
+    a.dbg_no_mma = (e && e[0] == '1') ? 1 : 0;
+    const char* f = getenv("LOBRA_RP_PREFETCH");
+    a.prefetch = f ? atoi(f) : 0;
+  }
   a.nsplit = rowproj_splits(meta.ntiles, K);
   const int nk = (K + 63) / 64;
   a.kb_per_split = (nk + a.nsplit - 1) / a.nsplit;
@@ -909,14 +933,18 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
   const int grid = meta.ntiles * a.nsplit;
   switch (rp_cfg() * 2 + (v_mn ? 1 : 0)) {
-    case 0: launch_rp<false, 3, 2>(grid, mapZ, mapV, a, st); break;
-    case 1: launch_rp<true, 3, 2>(grid, mapZ, mapV, a, st); break;
-    case 2: launch_rp<false, 6, 1>(grid, mapZ, mapV, a, st); break;
-    case 3: launch_rp<true, 6, 1>(grid, mapZ, mapV, a, st); break;
-    case 4: launch_rp<false, 4, 1>(grid, mapZ, mapV, a, st); break;
-    case 5: launch_rp<true, 4, 1>(grid, mapZ, mapV, a, st); break;
-    case 6: launch_rp<false, 8, 1>(grid, mapZ, mapV, a, st); break;
-    default: launch_rp<true, 8, 1>(grid, mapZ, mapV, a, st); break;
+    case 0: launch_rp<false, 3, 2, 1>(grid, mapZ, mapV, a, st); break;
+    case 1: launch_rp<true, 3, 2, 1>(grid, mapZ, mapV, a, st); break;
+    case 2: launch_rp<false, 6, 1, 1>(grid, mapZ, mapV, a, st); break;
+    case 3: launch_rp<true, 6, 1, 1>(grid, mapZ, mapV, a, st); break;
+    case 4: launch_rp<false, 3, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 5: launch_rp<true, 3, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 6: launch_rp<false, 2, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 7: launch_rp<true, 2, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 8: launch_rp<false, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 9: launch_rp<true, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
+    case 10: launch_rp<false, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
+    default: launch_rp<true, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
   }
 }
 

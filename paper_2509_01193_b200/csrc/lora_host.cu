@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -374,10 +375,17 @@ lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
+  static int promo = -1;   // LOBRA_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B (default)
+  if (promo < 0) {
+    const char* e = getenv("LOBRA_L2PROMO");
+    promo = e ? atoi(e) : 3;
+    if (promo < 0 || promo > 3) promo = 3;
+  }
+  const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_SWIZZLE_128B, pr[promo], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(LOBRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=%llu x %llu box=%u x %u",
                 (int)r, (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
