@@ -233,13 +233,21 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n_gpus = max(world, 1)
+    # LOBRA_BENCH_GLOO=1: test mode for the N > 1 control flow on ONE GPU (all ranks share
+    # cuda:0, gloo process group, TP1 replicas only, adapter sync through torch.distributed)
+    gloo_test = os.environ.get("LOBRA_BENCH_GLOO") == "1"
+    if gloo_test:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     _lib.load()
 
-    groups = deployment_for(n_gpus)
+    groups = deployment_for(n_gpus) if not gloo_test else [(1, n_gpus, 16384)]
     reps = replica_ranks(groups)
     my_rep = next(i for i, rr in enumerate(reps) if rank in rr)
     my_group = 0
@@ -252,7 +260,7 @@ def main():
     tp_size = groups[my_group][0]
     tp_rank = reps[my_rep].index(rank)
     comm = None
-    if world > 1:
+    if world > 1 and not gloo_test:
         uid = [_lib.lobra_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = _lib.lobra_comm_init(uid[0], world, rank, my_rep)
@@ -297,7 +305,12 @@ def main():
             T = int(lens.sum())
             layer.forward(lens, tsk, io, T, stream=stream)
             layer.backward(lens, tsk, io, T, accumulate_dadb=(ci > 0 or tp_size > 1), stream=stream)
-        layer.sync_adapter_grads(stream=stream)
+        if not chunks:   # a replica without work this step contributes zeros (P:170 sync)
+            layer.flat_grad.zero_()
+        if gloo_test and world > 1:
+            dist.all_reduce(layer.flat_grad)
+        else:
+            layer.sync_adapter_grads(stream=stream)
 
     plans = [plan(b) for b in batches]
     stream = torch.cuda.current_stream()
@@ -342,7 +355,7 @@ def main():
     _lib.lobra_profile_enable(False)
     clocks = sampler.stop() if (sampler and rank == 0) else None
     if world > 1:
-        t = torch.tensor([ms_local], device=dev)
+        t = torch.tensor([ms_local], device="cpu" if gloo_test else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     else:
@@ -373,7 +386,7 @@ def main():
     capped = bool(clocks and "sw_power_cap" in clocks.get("reasons", []))
     peak_kind = "bf16_tflops_sustained" if capped and "bf16_tflops_sustained" in peaks else "bf16_tflops"
     peak_t = float(peaks[peak_kind])
-    achieved = dom_fl / (dom_ms / 1000.0) / 1e12
+    achieved = dom_fl / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -381,7 +394,7 @@ def main():
     roofline = {"bound": "tensor", "kernel": f"k_gemm ({dom})", "achieved": achieved, "peak": peak_t,
                 "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": traffic,
                 "peak_source": f"{peak_src} {peak_kind}" + (" (sw_power_cap active in the timed region)" if capped else " (short timed region at full clocks)"),
-                "share_of_step": dom_ms / ms_local,
+                "share_of_step": dom_ms / ms_local if ms_local > 0 else 0.0,
                 "flops_per_launch": dom_fl / max(prof[dom][0], 1),
                 "ms_per_launch": dom_ms / max(prof[dom][0], 1)}
     flops_step = algorithmic_flops(LLAMA2_7B, int(tokens / args.steps), ranks)["total"]
@@ -415,7 +428,10 @@ def main():
                     h2d += host_dy[k][:T].numel() * 2
                 layer.forward(lens, tsk, io, T)
                 layer.backward(lens, tsk, io, T, accumulate_dadb=True)
-            layer.sync_adapter_grads()
+            if gloo_test and world > 1:
+                dist.all_reduce(layer.flat_grad)
+            else:
+                layer.sync_adapter_grads()
             host_grad.copy_(layer.flat_grad, non_blocking=True)
             d2h += layer.flat_grad.numel() * 4
             e2e_tokens += tok
@@ -423,7 +439,7 @@ def main():
         torch.cuda.synchronize()
         e_ms = f0.elapsed_time(f1)
         if world > 1:
-            t = torch.tensor([e_ms], device=dev)
+            t = torch.tensor([e_ms], device="cpu" if gloo_test else dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": e2e_tokens / (e_ms / 1000.0), "unit": "tokens/s",
