@@ -666,6 +666,232 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // =====================================================================================
+// Row projection with an LDGSTS producer: 4 producer warps stream Z with 16-byte cp.async,
+// each warp reading KB x 128 contiguous bytes of a row per instruction and writing the
+// 128-byte-swizzled K-major UMMA layout directly; the adapter operand (K-major, qp rows:
+// A_cat for the forward, B^T for the backward) comes by TMA.  Same math, epilogue and
+// split-K reduction as k_rowproj.  Warps: 0-3 producers, 4-7 epilogue, 8 MMA + TMEM.
+// =====================================================================================
+struct RowLdArgs {
+  const __nv_bfloat16* Z;
+  int K, nsplit, kb_per_split, qp;
+  __nv_bfloat16* out;
+  float* partial;
+  int* counters;
+  Meta meta;
+};
+
+template <int STAGES, int KB>
+__global__ void __launch_bounds__(288, 1)
+    k_rowproj_ld(const __grid_constant__ CUtensorMap mapV, const RowLdArgs args) {
+  constexpr int P = 2;                           // slots per pass
+  constexpr int ZB = KB * R_A_BYTES;             // Z bytes per stage
+  const int vbox = args.qp * 128;                // one K block of one slot's operand
+  const int stage_bytes = ZB + P * KB * vbox;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+  const int m = blockIdx.x / args.nsplit, split = blockIdx.x % args.nsplit;
+  const int s_begin = meta.tile_slot_off[m], s_end = meta.tile_slot_off[m + 1];
+  const int npass = (s_end - s_begin + P - 1) / P;
+  const int nk = (args.K + 63) / 64;
+  const int kb0 = split * args.kb_per_split, kb1 = min(nk, kb0 + args.kb_per_split);
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mapV);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 128 + 1), mbar_init(&empty[s], 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp < 4) {  // ---------------- LDGSTS producers (128 threads)
+    constexpr int LPR = KB * 8 < 32 ? KB * 8 : 32;   // lanes per row
+    constexpr int RPI = 32 / LPR;                    // rows per instruction
+    const int pt = threadIdx.x;
+    const int c = lane % LPR;                        // 16-byte chunk within the row segment
+    const int b = c >> 3, j = c & 7;                 // K block, chunk in 128 B
+    int stage = 0;
+    uint32_t phase = 0;
+    int g = 0;                                       // stages issued
+    for (int p = 0; p < npass; ++p) {
+      const int s0 = s_begin + p * P;
+      const int ns = min(P, s_end - s0);
+      for (int kb = kb0; kb < kb1; kb += KB, ++g) {
+        const int nkb = min(KB, kb1 - kb);
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * stage_bytes;
+        const uint32_t zb = smem_u32(st);
+        for (int it = 0; it < 32 / RPI; ++it) {
+          const int r = warp * 32 + it * RPI + lane / LPR;
+          const int row = m * kTileM + r;
+          const int col = (kb + b) * 64 + j * 8;
+          const bool ok = row < meta.T && b < nkb && col < args.K;
+          const __nv_bfloat16* src = args.Z + (ok ? (size_t)row * args.K + col : 0);
+          cp_async16(zb + b * R_A_BYTES + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+        if (pt == 0) {   // adapter operand by TMA, counted on the same barrier
+          mbar_expect_tx(&full[stage], ns * nkb * vbox);
+          for (int i = 0; i < ns; ++i) {
+            const int t = meta.slot_task[s0 + i];
+            for (int q = 0; q < nkb; ++q)
+              tma_load_2d(st + ZB + (i * KB + q) * vbox, &mapV, &full[stage], (kb + q) * 64,
+                          meta.roff[t]);
+          }
+        }
+        if (g >= STAGES - 1) {   // the stage issued STAGES-1 steps ago has landed
+          cp_async_wait<STAGES - 1>();
+          fence_proxy_async_smem();
+          const int sd = (stage + 1) % STAGES;   // == (g - (STAGES - 1)) % STAGES
+          mbar_arrive(&full[sd]);
+        }
+        if (++stage == STAGES) stage = 0, phase ^= 1;
+      }
+    }
+    // drain: signal the last min(g, STAGES-1) stages
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    const int pending = g < STAGES - 1 ? g : STAGES - 1;
+    for (int k = pending; k >= 1; --k) mbar_arrive(&full[(stage - k + STAGES) % STAGES]);
+  } else if (warp == 8) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t id = idesc_bf16(128, args.qp, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int p = 0; p < npass; ++p) {
+        const int s0 = s_begin + p * P;
+        const int ns = min(P, s_end - s0);
+        mbar_wait(tempty, (p & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = kb0; kb < kb1; kb += KB) {
+          const int nkb = min(KB, kb1 - kb);
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t st0 = smem_u32(smem + stage * stage_bytes);
+          for (int i = 0; i < ns; ++i)
+            for (int q = 0; q < nkb; ++q) {
+              const uint32_t a0 = st0 + q * R_A_BYTES;
+              const uint32_t b0 = st0 + ZB + (i * KB + q) * vbox;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024),
+                         sdesc_sw128(b0 + k * 32, 16, 1024), id,
+                         (kb != kb0 || q != 0 || k != 0) ? 1u : 0u);
+            }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) stage = 0, phase ^= 1;
+        }
+        mma_commit(tfull);
+      }
+    }
+  } else {  // ---------------- epilogue (warps 4-7)
+    const uint32_t q = warp - 4;
+    const int lrow = q * 32 + lane;
+    const int row = m * kTileM + lrow;
+    const int my_task = row < meta.T ? row_task(meta, row) : -1;
+    if (blockIdx.x == 0) {
+      float z[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) z[i] = 0.0f;
+      store_slot_row(args.out, meta.nslots, lrow, z, 0.0f, 0);
+    }
+    for (int p = 0; p < npass; ++p) {
+      const int s0 = s_begin + p * P;
+      const int ns = min(P, s_end - s0);
+      mbar_wait(tfull, p & 1);
+      tc_fence_after();
+      for (int i = 0; i < ns; ++i) {
+        const int s = s0 + i;
+        const int ts = meta.slot_task[s];
+        float v[64];
+        tmem_ld32(tmem + ((q * 32u) << 16) + i * 64, *reinterpret_cast<float(*)[32]>(v));
+        tmem_ld32(tmem + ((q * 32u) << 16) + i * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        if (args.nsplit == 1) {
+          const bool mine = ts == my_task;
+          store_slot_row(args.out, s, lrow, v, mine ? meta.scales[ts] : 0.0f, mine ? meta.ranks[ts] : 0);
+        } else {
+          const int rp = rpad16(meta.ranks[ts]);
+          float4* dst = reinterpret_cast<float4*>(
+              args.partial + (((size_t)split * meta.nslots + s) * kTileM + lrow) * 64);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (4 * jj < rp) dst[jj] = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+    if (args.nsplit > 1) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (lrow == 0) *last_flag = (atomicAdd(&args.counters[m], 1) == args.nsplit - 1);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*last_flag) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int s = s_begin; s < s_end; ++s) {
+          const int ts = meta.slot_task[s];
+          const int rp = rpad16(meta.ranks[ts]);
+          float v[64];
+#pragma unroll
+          for (int jj = 0; jj < 64; ++jj) v[jj] = 0.0f;
+          for (int sp = 0; sp < args.nsplit; ++sp) {
+            const float4* src = reinterpret_cast<const float4*>(
+                args.partial + (((size_t)sp * meta.nslots + s) * kTileM + lrow) * 64);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              if (4 * jj >= rp) break;
+              const float4 f = __ldcg(src + jj);
+              v[4 * jj] += f.x, v[4 * jj + 1] += f.y, v[4 * jj + 2] += f.z, v[4 * jj + 3] += f.w;
+            }
+          }
+          const bool mine = ts == my_task;
+          store_slot_row(args.out, s, lrow, v, mine ? meta.scales[ts] : 0.0f, mine ? meta.ranks[ts] : 0);
+        }
+        if (lrow == 0) args.counters[m] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+}
+
+// B [out, rsum] -> Bt [rsum, out] (the backward projection's K-major operand)
+__global__ void k_transpose_b(const __nv_bfloat16* __restrict__ B, __nv_bfloat16* __restrict__ Bt,
+                              int out, int rsum) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int o0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int o = o0 + i, r = r0 + threadIdx.x;
+    tile[i][threadIdx.x] = (o < out && r < rsum) ? B[(size_t)o * rsum + r] : __float2bfloat16(0.0f);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = r0 + i, o = o0 + threadIdx.x;
+    if (r < rsum && o < out) Bt[(size_t)r * out + o] = tile[threadIdx.x][i];
+  }
+}
+
+// =====================================================================================
 // Segmented token reduction: partial[u][c][q][i] = sum_{slots of unit u} sum_rows
 //      Z[row][c*128 + i] * Slot[row][q]          (Z^T as an MN-major A operand)
 // =====================================================================================
@@ -887,11 +1113,17 @@ int rp_cfg() {
   return v;
 }
 
+bool rowproj_uses_ld() {
+  const char* e = getenv("LOBRA_RP_TMA");
+  return !(e && e[0] == '1');
+}
+
 int rowproj_splits(int ntiles, int K) {
   // one wave of similar-size CTAs: HBM-bound, so what matters is that every resident CTA
   // streams the same number of bytes
   const int nk = (K + 63) / 64;
-  const int slots = kRpCfg[rp_cfg()].per_sm * 148;
+  const int per_sm = rowproj_uses_ld() ? (rp_cfg() == 3 ? 2 : 1) : kRpCfg[rp_cfg()].per_sm;
+  const int slots = per_sm * 148;
   int s = ntiles > 0 ? slots / ntiles : 1;
   s = s < 1 ? 1 : s;
   s = s > 8 ? 8 : s;
@@ -945,6 +1177,46 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
     case 9: launch_rp<true, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
     case 10: launch_rp<false, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
     default: launch_rp<true, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
+  }
+}
+
+void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int rsum, cudaStream_t st) {
+  launch_k(k_transpose_b, dim3((out + 31) / 32, (rsum + 31) / 32), dim3(32, 8), 0, st, B, Bt, out, rsum);
+}
+
+template <int ST, int KB>
+void launch_rpld(int grid, const CUtensorMap& mapV, const RowLdArgs& a, cudaStream_t st) {
+  const int smem = ST * (KB * R_A_BYTES + 2 * KB * a.qp * 128) + 1024 + 256;
+  static int init = 0;
+  if (init < smem) {
+    cudaFuncSetAttribute(k_rowproj_ld<ST, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = smem;
+  }
+  launch_k(k_rowproj_ld<ST, KB>, dim3(grid), dim3(288), smem, st, mapV, a);
+}
+
+void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, int qp,
+                       const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
+                       cudaStream_t st) {
+  RowLdArgs a;
+  a.Z = Z;
+  a.K = K;
+  a.qp = qp;
+  a.nsplit = rowproj_splits(meta.ntiles, K);
+  const int nk = (K + 63) / 64;
+  a.kb_per_split = (nk + a.nsplit - 1) / a.nsplit;
+  a.nsplit = (nk + a.kb_per_split - 1) / a.kb_per_split;
+  a.out = slots;
+  a.partial = partial;
+  a.counters = counters;
+  a.meta = meta;
+  if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
+  const int grid = meta.ntiles * a.nsplit;
+  switch (rp_cfg()) {
+    case 1: launch_rpld<2, 4>(grid, mapVk, a, st); break;
+    case 2: launch_rpld<4, 2>(grid, mapVk, a, st); break;
+    case 3: launch_rpld<2, 2>(grid, mapVk, a, st); break;
+    default: launch_rpld<3, 2>(grid, mapVk, a, st); break;
   }
 }
 

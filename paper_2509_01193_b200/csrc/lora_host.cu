@@ -331,7 +331,8 @@ Meta device_meta(const Plan& P, const void* dev_base) {
 
 // Workspace layout (bytes from ws base); both directions share it.
 struct Layout {
-  size_t meta = 0, bpad = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0, total = 0;
+  size_t meta = 0, bpad = 0, bt = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0,
+         total = 0;
   size_t saved = 0;
   int ld8 = 0;   // row stride (elements) of the B operand the kernels read
 };
@@ -347,6 +348,8 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     L.ld8 = P.ld8;
     L.bpad = off;
     if (!P.bdirect) off += align256(out * L.ld8 * es);
+    L.bt = off;       // B^T [rsum, out] (K-major operand of the backward projection)
+    off += align256((size_t)P.rsum * out * es);
     L.gslots = off;   // + one all-zero slot (index nslots)
     off += align256((size_t)(P.nslots + 1) * kTileM * kSlotW * es);
     const int sp = std::max(rowproj_splits(P.ntiles, (int)in), rowproj_splits(P.ntiles, (int)out));
@@ -494,7 +497,14 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mW, W, in, out, 64, bn)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mB, Bop, L.ld8, out, 64, bn)) != LOBRA_OK) return s;
-    {
+    if (rowproj_uses_ld()) {
+      CUtensorMap mAk;
+      if ((s = make_map(&mAk, ad->A, in, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_rowproj_ld(static_cast<const __nv_bfloat16*>(X), in, mAk, P.qp, meta,
+                        static_cast<__nv_bfloat16*>(Hs), reinterpret_cast<float*>(w + L.rpart),
+                        reinterpret_cast<int*>(w + L.counters), st);
+    } else {
       Prof p_(LOBRA_K_ROWPROJ, st);
       launch_rowproj(false, mX, mA, in, meta, static_cast<__nv_bfloat16*>(Hs),
                      reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);
@@ -578,7 +588,19 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mAt, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
-    {
+    if (rowproj_uses_ld()) {
+      auto* Bt = reinterpret_cast<__nv_bfloat16*>(w + L.bt);
+      {
+        Prof p_(LOBRA_K_PAD, st);
+        launch_transpose_b(static_cast<const __nv_bfloat16*>(ad->B), Bt, out, P.rsum, st);
+      }
+      CUtensorMap mBk;
+      if ((s = make_map(&mBk, Bt, out, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_rowproj_ld(static_cast<const __nv_bfloat16*>(dY), out, mBk, P.qp, meta, Gs,
+                        reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters),
+                        st);
+    } else {
       Prof p_(LOBRA_K_ROWPROJ, st);
       launch_rowproj(true, mdY, mBt, out, meta, Gs, reinterpret_cast<float*>(w + L.rpart),
                      reinterpret_cast<int*>(w + L.counters), st);

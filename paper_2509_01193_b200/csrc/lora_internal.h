@@ -63,6 +63,14 @@ int rowproj_splits(int ntiles, int K);
 void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
                     const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
                     cudaStream_t st);
+// LDGSTS-producer variant (default; LOBRA_RP_TMA=1 selects the TMA-producer kernel):
+// Z raw [T, K]; mapVk K-major adapter operand, box {64, qp} (A_cat forward, B^T backward).
+bool rowproj_uses_ld();
+void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, int qp,
+                       const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
+                       cudaStream_t st);
+// B [out, rsum] -> Bt [rsum, out]
+void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int rsum, cudaStream_t st);
 // C[T, N] (+)= Z[T,K] . Wop  +  sum over tile slots: Slot[128, r] . Vext_t
 //   b_mn = false: Wop = W^T with W [N, K] K-major (forward, X W^T); Vext = B_cat [N, ld8]
 //   b_mn = true : Wop = W   with W [K, N] (MN-major B operand; backward, dY W);
