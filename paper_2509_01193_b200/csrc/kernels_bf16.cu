@@ -235,7 +235,7 @@ constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
 
 struct Gemm2Args {
-  int T, N, K, ntm2, ntn, accumulate;
+  int T, N, K, ntm2, ntn, accumulate, group_m;
   __nv_bfloat16* C;
   Meta meta;
 };
@@ -266,6 +266,20 @@ __device__ __forceinline__ void for_union(const Meta& m, int tA, int tB, uint32_
     if (find_slot(m, tA, t) != m.nslots) continue;
     f(t, rank == 1 ? s : m.nslots);
   }
+}
+
+// Pair-tile order: groups of `group_m` pair-M blocks, N-major inside a group, so that the
+// concurrently running clusters share a few X panels AND a few W panels (both stay in L2).
+__device__ __forceinline__ void pair_tile(int pt, int ntm2, int ntn, int group_m, int& mp, int& n) {
+  if (group_m <= 1) {
+    mp = pt / ntn, n = pt % ntn;
+    return;
+  }
+  const int per_group = group_m * ntn;
+  const int g = pt / per_group, r = pt % per_group;
+  const int gm = min(group_m, ntm2 - g * group_m);   // the last group may be short
+  mp = g * group_m + r % gm;
+  n = r / gm;
 }
 
 template <bool kBMN>
@@ -315,7 +329,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int pt = cid; pt < npt; pt += ncl) {
-        const int mp = pt / args.ntn, n = pt % args.ntn;
+        int mp, n;
+        pair_tile(pt, args.ntm2, args.ntn, args.group_m, mp, n);
         const int m = 2 * mp + rank;
         const int ncol = n * 256 + rank * 128;
         for (int kb = 0; kb < nk; ++kb) {
@@ -353,7 +368,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int pt = cid; pt < npt; pt += ncl, ++it) {
-        const int mp = pt / args.ntn;
+        int mp, n_unused;
+        pair_tile(pt, args.ntm2, args.ntn, args.group_m, mp, n_unused);
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -393,7 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     const uint32_t q = warp - 4;
     int it = 0;
     for (int pt = cid; pt < npt; pt += ncl, ++it) {
-      const int mp = pt / args.ntn, n = pt % args.ntn;
+      int mp, n;
+      pair_tile(pt, args.ntm2, args.ntn, args.group_m, mp, n);
       const int m = 2 * mp + rank;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -458,7 +475,7 @@ template <int STAGES, int P, int KB = 1>
 constexpr int r_smem() { return STAGES * KB * (R_A_BYTES + P * R_V_BYTES) + 1024 + 256; }
 
 struct RowArgs {
-  int K, nsplit, kb_per_split, dbg_no_mma, prefetch;
+  int K, nsplit, kb_per_split, dbg_no_mma, prefetch, interleave;
   __nv_bfloat16* out;
   float* partial;     // [nsplit][nslots][128][64] fp32 (only when nsplit > 1)
   int* counters;      // [ntiles], zero on entry; reset by the last CTA
@@ -526,12 +543,16 @@ __global__ void __launch_bounds__(256, 1)
       for (int p = 0; p < npass; ++p) {
         const int s0 = s_begin + p * R_P;
         const int ns = min(R_P, s_end - s0);
-        for (int kb = kb0; kb < kb1; kb += R_KB) {
-          const int nkb = min(R_KB, kb1 - kb);
+        for (int kk = kb0; kk < kb1; kk += R_KB) {
+          // interleaved: this split takes K blocks split, split + nsplit, ... so that the
+          // CTAs of one tile read adjacent column blocks of the same rows concurrently
+          const int kb = args.interleave ? split + (kk - kb0) * args.nsplit : kk;
+          if (kb >= nk) break;
+          const int nkb = args.interleave ? 1 : min(R_KB, kb1 - kk);
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + ns * R_V_BYTES));
           uint8_t* st = smem + stage * R_STAGE_BYTES;
-          if (args.prefetch)   // stream the Z tile into L2 `prefetch` blocks ahead
+          if (args.prefetch && !args.interleave)   // stream the Z tile into L2 ahead
             for (int j = 0; j < nkb; ++j)
               if (kb + j + args.prefetch < kb1)
                 tma_prefetch_2d(&mapZ, (kb + j + args.prefetch) * 64, m * kTileM);
@@ -561,8 +582,10 @@ __global__ void __launch_bounds__(256, 1)
         const int ns = min(R_P, s_end - s0);
         mbar_wait(tempty, (p & 1) ^ 1);
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; kb += R_KB) {
-          const int nkb = min(R_KB, kb1 - kb);
+        for (int kk = kb0; kk < kb1; kk += R_KB) {
+          const int kb = args.interleave ? split + (kk - kb0) * args.nsplit : kk;
+          if (kb >= nk) break;
+          const int nkb = args.interleave ? 1 : min(R_KB, kb1 - kk);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t st0 = smem_u32(smem + stage * R_STAGE_BYTES);
@@ -580,7 +603,7 @@ __global__ void __launch_bounds__(256, 1)
                 const uint64_t bd = kVmn ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
                                          : sdesc_sw128(b0 + k * 32, 16, 1024);
                 mma_bf16(tmem + i * 64, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id,
-                         (kb != kb0 || j != 0 || k != 0) ? 1u : 0u);
+                         (kk != kb0 || j != 0 || k != 0) ? 1u : 0u);
               }
             }
           }
@@ -1113,9 +1136,9 @@ int rp_cfg() {
   return v;
 }
 
-bool rowproj_uses_ld() {
-  const char* e = getenv("LOBRA_RP_TMA");
-  return !(e && e[0] == '1');
+bool rowproj_uses_ld() {   // opt-in (LOBRA_RP_LD=1): measured slower than TMA on B200
+  const char* e = getenv("LOBRA_RP_LD");
+  return e && e[0] == '1';
 }
 
 int rowproj_splits(int ntiles, int K) {
@@ -1125,6 +1148,10 @@ int rowproj_splits(int ntiles, int K) {
   const int per_sm = rowproj_uses_ld() ? (rp_cfg() == 3 ? 2 : 1) : kRpCfg[rp_cfg()].per_sm;
   const int slots = per_sm * 148;
   int s = ntiles > 0 ? slots / ntiles : 1;
+  if (const char* fs = getenv("LOBRA_RP_SPLITS")) {   // tuning override
+    const int v = atoi(fs);
+    if (v >= 1 && v <= 8) s = v;
+  }
   s = s < 1 ? 1 : s;
   s = s > 8 ? 8 : s;
   s = s > nk ? nk : s;
@@ -1153,6 +1180,8 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
     a.dbg_no_mma = (e && e[0] == '1') ? 1 : 0;
     const char* f = getenv("LOBRA_RP_PREFETCH");
     a.prefetch = f ? atoi(f) : 0;
+    const char* g = getenv("LOBRA_RP_INTERLEAVE");
+    a.interleave = (g && g[0] == '1') ? 1 : 0;
   }
   a.nsplit = rowproj_splits(meta.ntiles, K);
   const int nk = (K + 63) / 64;
@@ -1247,6 +1276,16 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
     a.accumulate = accumulate;
     a.C = C;
     a.meta = meta;
+    {
+      // measured (profiles/r1_gemm_raster.md): N-fastest is best while W fits in L2 next to
+      // the X panels; 16-block groups once W is large (gate/up/down: 90 MB)
+      static int gm = -2;
+      if (gm == -2) {
+        const char* e = getenv("LOBRA_GEMM_GROUP_M");
+        gm = e ? atoi(e) : -1;
+      }
+      a.group_m = gm >= 0 ? gm : ((double)N * K * 2 > 48e6 ? 16 : 1);
+    }
     const int tiles = a.ntm2 * a.ntn;
     int clusters = num_sms / 2;
     if (tiles < clusters) clusters = tiles;
