@@ -202,7 +202,9 @@ typedef struct {
 } lobra_dispatch_out;
 
 /* mode: 0 = balanced (Eq. 3), 1 = length-based (Fig. 4(c): every bucket to the
- * supporting group with the smallest c_ij * n_i, ties to the earlier group).
+ * supporting group with the smallest c_ij * n_i, ties to the earlier group), 2 = uniform
+ * (Task-Fused baseline: exactly one deployed homogeneous group, the k-th
+ * sequence goes to replica k mod p).
  * chunking: 0 = padded micro-batches of App. D (per bucket, b_j = floor(M_i / s_j)
  * sequences); 1 = packed micro-batches ("can also be applied when
  * packing is employed"; reading Q6b): the replica's sequences in (bucket desc, index)
@@ -238,6 +240,26 @@ LOBRA_API lobra_status lobra_adapter_allreduce(lobra_comm comm, float* flat_grad
                                      lobra_stream_t stream);
 
 /* ------------------------------------------------------------------------------
+ * Adapter optimizer: one AdamW step ("We use the Adam optimizer
+ * [adam, adamw]"; decoupled weight decay):
+ *     g = grad_scale * grad;  m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
+ *     p = p - lr * ( (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps) + wd * p )
+ * over a flat fp32 master-parameter buffer with per-group hyper-parameters (multi-tenant:
+ * one group per task).  params/m/v are updated in place; grads are read.  group: device
+ * uint8 [count] group id per element, or NULL (every element in group 0).  hp: host
+ * array [num_groups], 1 <= num_groups <= 64.  params_bf16: optional device bf16 [count]
+ * copy of the updated parameters (what the LoRA kernels read), or NULL.  All device
+ * pointers 16-byte aligned.  Errors: LOBRA_ERR_INPUT, LOBRA_ERR_CUDA.
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+} lobra_adamw_hparams;
+LOBRA_API lobra_status lobra_adamw_step(float* params, void* params_bf16, const float* grads,
+                                        float* m, float* v, const uint8_t* group, size_t count,
+                                        const lobra_adamw_hparams* hp, int32_t num_groups,
+                                        int64_t step, float grad_scale, lobra_stream_t stream);
+
+/* ------------------------------------------------------------------------------
  * Tracing: per-kernel-class device times (CUDA events recorded on the launching
  * stream around every kernel the library enqueues, only while enabled) and a launch
  * counter (always on).  The paper's cost model is fitted from such single-layer
@@ -251,6 +273,7 @@ enum {
   LOBRA_K_FINALIZE = 4,   /* fixed-order partial sums                           */
   LOBRA_K_PAD = 5,        /* adapter operand packing                            */
   LOBRA_K_FP32 = 6,       /* fp32 SIMT path kernels                             */
+  LOBRA_K_OPT = 7,        /* adapter optimizer (AdamW)                          */
   LOBRA_K_NUM = 8
 };
 typedef struct {

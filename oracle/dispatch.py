@@ -338,6 +338,10 @@ def dispatch(groups, cost, seq_lens, seq_task, grid_step, grid_max, R, mode=0,
         for j in range(Rb):
             best = min((c[i][j] * groups[i].tp, i) for i in live if j < r[i])
             d[best[1], j] = Bj[j]
+    elif mode == 2:   # uniform (Task-Fused): one homogeneous group, even by count
+        if len(live) != 1:
+            raise DispatchError(1, "uniform dispatch needs exactly one deployed group")
+        d[live[0]] = Bj
     else:
         raise DispatchError(1, f"unknown mode {mode}")
     check_eq3(d, Bj, p, r)
@@ -356,7 +360,13 @@ def dispatch(groups, cost, seq_lens, seq_task, grid_step, grid_max, R, mode=0,
     rbase = np.concatenate([[0], np.cumsum(p)]).astype(np.int64)
     seq_replica = np.full(n, -1, dtype=np.int64)
     running = [0] * int(rbase[-1])
-    for i in range(G):
+    if mode == 2:     # the k-th sequence (ascending index) -> replica k mod p
+        i = live[0]
+        for k in range(n):
+            rep = int(rbase[i] + k % p[i])
+            seq_replica[k] = rep
+            running[rep] += c[i][seq_bucket[k]]
+    for i in range(G if mode != 2 else 0):
         for j in range(Rb):
             idx = [k for k in range(n) if seq_bucket[k] == j and seq_group[k] == i]
             if not idx:

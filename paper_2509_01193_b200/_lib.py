@@ -25,8 +25,9 @@ EXPORTED = [
     "lobra_lora_fwd", "lobra_lora_bwd", "lobra_dispatch", "lobra_nccl_unique_id",
     "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
     "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
+    "lobra_adamw_step",
 ]
-K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "other"]
+K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -57,6 +58,11 @@ class DispatchOut(C.Structure):
                 ("seq_bucket", _i32p), ("seq_replica", _i32p), ("seq_chunk", _i32p),
                 ("pack_order", _i32p), ("replica_cost", _i64p), ("t_hat", C.c_int64),
                 ("nodes", C.c_int64)]
+
+
+class AdamHP(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float)]
 
 
 class Profile(C.Structure):
@@ -115,6 +121,10 @@ def load() -> C.CDLL:
     lib.lobra_profile_read.restype = C.c_int
     lib.lobra_profile_read.argtypes = [C.POINTER(Profile), C.c_int]
     lib.lobra_launch_count.restype = C.c_int64
+    lib.lobra_adamw_step.restype = C.c_int
+    lib.lobra_adamw_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_size_t, C.POINTER(AdamHP), C.c_int32,
+                                     C.c_int64, C.c_float, C.c_void_p]
     _LIB = lib
     return lib
 
@@ -305,3 +315,15 @@ def lobra_profile_read(reset: bool = True) -> dict:
 
 def lobra_launch_count() -> int:
     return int(load().lobra_launch_count())
+
+
+# ---------------------------------------------------------------------------- optimizer
+def lobra_adamw_step(params, grads, m, v, hparams, step, group=None, params_bf16=None,
+                     grad_scale=1.0, stream=None):
+    """One multi-tenant AdamW step (include/lobra.h).  hparams: list of dicts with keys
+    lr, beta1, beta2, eps, weight_decay (one per group); group: uint8 tensor or None."""
+    hp = (AdamHP * len(hparams))(*[AdamHP(h["lr"], h["beta1"], h["beta2"], h["eps"],
+                                          h["weight_decay"]) for h in hparams])
+    _check(load().lobra_adamw_step(_ptr(params), _ptr(params_bf16), _ptr(grads), _ptr(m), _ptr(v),
+                                   _ptr(group), int(params.numel()), hp, len(hparams), int(step),
+                                   float(grad_scale), _stream(stream)))

@@ -286,7 +286,7 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   if (grid_step < 1 || grid_max < grid_step || grid_max % grid_step)
     return fail(LOBRA_ERR_INPUT, "grid_max must be a positive multiple of grid_step");
   if (R < 1) return fail(LOBRA_ERR_INPUT, "R must be >= 1");
-  if (mode != 0 && mode != 1) return fail(LOBRA_ERR_INPUT, "unknown mode %d", mode);
+  if (mode < 0 || mode > 2) return fail(LOBRA_ERR_INPUT, "unknown mode %d", mode);
   if (chunking != 0 && chunking != 1) return fail(LOBRA_ERR_INPUT, "unknown chunking %d", chunking);
   const int G = dep->num_groups;
   const int n = batch->num_seqs;
@@ -371,6 +371,11 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   Budget bud{node_cap > 0 ? node_cap : (i64)400000000};
   std::vector<std::vector<i64>> dl = by_length(L, ltp);
   lobra_status st = LOBRA_OK;
+  if (mode == 2 && L.G != 1)
+    return fail(LOBRA_ERR_INPUT, "uniform dispatch (mode 2) needs exactly one deployed group");
+  if (mode == 2) {
+    for (int j = 0; j < Rb; ++j) dl[0][j] = Bj[j];
+  }
   if (mode == 0 && L.G >= 2) {
     const i64 UB = objective(L, dl);
     if (L.G == 2) {
@@ -424,7 +429,16 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   for (int i = 0; i < G; ++i) rbase[i + 1] = rbase[i] + p[i];
   std::vector<i64> running(total_rep, 0);
   std::vector<int> seq_rep(n, -1);
-  for (int i = 0; i < G; ++i) {
+  for (int i = 0; i < G && mode == 2; ++i) {   // uniform: k-th sequence -> replica k mod p
+    if (!p[i]) continue;
+    int k = 0;
+    for (int s = 0; s < n; ++s) {
+      const int rep = (int)(rbase[i] + (k++) % p[i]);
+      seq_rep[s] = rep;
+      running[rep] += I.c[i][seq_b[s]];
+    }
+  }
+  for (int i = 0; i < G && mode != 2; ++i) {
     if (!p[i]) continue;
     for (int j = 0; j < Rb; ++j) {
       int start = 0;

@@ -127,3 +127,17 @@ def test_c5_scale_runs_fast():
     # sequences longer than 8192 never reach a TP1 replica
     long = wl.seq_lens > 8192
     assert (got["seq_replica"][long] >= 4).all()
+
+
+def test_uniform_mode_cpp():
+    rng = np.random.default_rng(9)
+    lens = rng.integers(1, 4096, size=37)
+    tasks = rng.integers(0, 4, size=37)
+    groups = [D.Group(2, 4, 4096)]
+    cost = _cost_table(groups, 16, 256, a1=1.0, unit=64)
+    got, ref = _run_both(groups, cost, lens, tasks, 256, 4096, 8, mode=2, chunking=1)
+    assert np.bincount(got["seq_replica"]).tolist() == [10, 9, 9, 9]
+    from paper_2509_01193_b200 import _lib
+    with pytest.raises(_lib.LobraError):
+        _lib.lobra_dispatch([1, 2], [2, 1], [2048, 4096], _cost_table([D.Group(1, 2, 2048), D.Group(2, 1, 4096)], 16, 256),
+                            lens, tasks, 256, 4096, 8, 2)

@@ -1,0 +1,164 @@
+"""GPU-seconds ablation of the paper's dispatch designs on B200 layer costs.
+
+    python tools/ablation.py [--steps 20] [--out profiles/r1_ablation.json]     (under gpurun)
+
+1. MEASURES the time of one Llama-2-7B layer's seven LoRA projections (fwd + bwd, C2 task
+   mix, this library's kernels) on one B200 for packed chunks of T tokens, and fits
+   t_1(T) = a0 + a1 * T (projection-only layers are linear in tokens: App. D's t(b, s) with
+   no s^2 term).
+2. MODELS a TP-k replica as t_k(T) = a0 + a1 * T / k + 4 all-reduces of T x 4096 bf16 at the
+   measured 8-rank NCCL bus bandwidth (B200_PROFILING.md: 725 GB/s); Megatron TP.
+3. For C5-like steps (the 12 dataset-table tasks + 4 clones, batch sizes of Table
+   tb:dataset_summary, lengths <= 16K) on N = 8 GPUs with the per-replica token limits of
+   DESIGN.md Q25 (TP1 8K, TP2 16K, TP4 32K), evaluates:
+     A  Task-Fused: homogeneous replicas able to hold the longest sequence, uniform dispatch
+     B  heterogeneous replicas + length-based dispatch (fixed 1K buckets)
+     C  + workload-balanced dispatch (Eq. 3, fixed 1K buckets)
+     D  + dynamic bucketing (256 grid, R = 16)  -- LobRA
+   with every dispatch computed by lobra_dispatch (the exact C++ solver), the deployment
+   for B-D chosen by enumerating all TP{1,2,4} mixes of 8 GPUs (a small stage-1 search).
+GPU-seconds per step = N x max over replicas of the sum of its chunk times.
+"""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2509_01193_b200 import _lib  # noqa: E402
+from workloads import synth  # noqa: E402
+
+M_LIMIT = {1: 8192, 2: 16384, 4: 32768}
+BUS_BW = 725e9
+
+
+def measure_layer(Ts=(1024, 2048, 4096, 8192, 16384), reps=5):
+    import torch
+    from paper_2509_01193_b200.layer import LLAMA2_7B, LoraLayer
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    tasks = synth.c2_tasks()
+    layer = LoraLayer(LLAMA2_7B, [t.rank for t in tasks], [t.scale for t in tasks], dev, seed=1)
+    io = layer.alloc_io(max(Ts), seed=2)
+    out = {}
+    for T in Ts:
+        wl = synth.pack_tokens(tasks, T, 4096, seed=10 + T, name="cal")
+        for _ in range(2):
+            layer.forward(wl.seq_lens, wl.seq_task, io, T)
+            layer.backward(wl.seq_lens, wl.seq_task, io, T, accumulate_dadb=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            layer.forward(wl.seq_lens, wl.seq_task, io, T)
+            layer.backward(wl.seq_lens, wl.seq_task, io, T, accumulate_dadb=False)
+        e1.record()
+        torch.cuda.synchronize()
+        out[T] = e0.elapsed_time(e1) / reps / 1000.0
+    Tv = np.array(sorted(out), float)
+    tv = np.array([out[int(T)] for T in Tv])
+    a1, a0 = np.polyfit(Tv, tv, 1)
+    return {"points_s": {int(k): v for k, v in out.items()}, "a0_s": float(a0), "a1_s_per_token": float(a1)}
+
+
+def t_rep(k, T, a0, a1):
+    comm = 0.0 if k == 1 else 4 * 2 * (k - 1) / k * T * 4096 * 2 / BUS_BW
+    return a0 + a1 * T / k + comm
+
+
+def cost_table(groups, a0, a1, grid_step, grid_max, unit=1e-5):
+    U = grid_max // grid_step
+    return [[max(1, int(round(t_rep(tp, (u + 1) * grid_step, 0.0, a1) / unit))) for u in range(U)]
+            for tp, _, _ in groups]
+
+
+def step_time(groups, wl, mode, grid_step, R, a0, a1):
+    tp = [g[0] for g in groups]
+    reps = [g[1] for g in groups]
+    M = [g[2] for g in groups]
+    gmax = 16384
+    d = _lib.lobra_dispatch(tp, reps, M, cost_table(groups, a0, a1, grid_step, gmax), wl.seq_lens,
+                            wl.seq_task, grid_step, gmax, R, mode, chunking=1)
+    rbase = np.concatenate([[0], np.cumsum(reps)])
+    times = []
+    for rep in range(int(rbase[-1])):
+        gi = int(np.searchsorted(rbase, rep, side="right") - 1)
+        mine = d["seq_replica"] == rep
+        t = 0.0
+        for c in set(d["seq_chunk"][mine].tolist()):
+            T = int(wl.seq_lens[mine & (d["seq_chunk"] == c)].sum())
+            t += t_rep(tp[gi], T, a0, a1)
+        times.append(t)
+    return max(times), float(np.mean(times))
+
+
+def deployments(n=8, tps=(1, 2, 4)):
+    """All (tp, replicas, M) mixes using exactly n GPUs, ordered by (tp, M)."""
+    out = []
+    for counts in itertools.product(*[range(n // t + 1) for t in tps]):
+        if sum(c * t for c, t in zip(counts, tps)) == n:
+            out.append([(t, c, M_LIMIT[t]) for c, t in zip(counts, tps) if c > 0])
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_ablation.json"))
+    ap.add_argument("--a0", type=float, default=None, help="skip the GPU measurement (seconds)")
+    ap.add_argument("--a1", type=float, default=None)
+    args = ap.parse_args()
+    if args.a0 is None:
+        cal = measure_layer()
+    else:
+        cal = {"points_s": {}, "a0_s": args.a0, "a1_s_per_token": args.a1}
+    a0, a1 = cal["a0_s"], cal["a1_s_per_token"]
+    tasks = synth.c3_tasks()
+    per_task = [t.batch_size for t in tasks[:12]] + [64] * 4
+    batches = [synth.sample_batch(tasks, seed=100 + i, l_max=16384, per_task=per_task)
+               for i in range(args.steps)]
+    n = 8
+    res = {"calibration": cal, "n_gpus": n, "steps": args.steps, "strategies": {}}
+    # A: Task-Fused, homogeneous TP able to hold the longest sequence of every batch
+    longest = max(int(b.seq_lens.max()) for b in batches)
+    tpA = min(t for t in (1, 2, 4) if M_LIMIT[t] >= longest)
+    depA = [(tpA, n // tpA, M_LIMIT[tpA])]
+    t0 = time.time()
+    sA = [step_time(depA, b, 2, 256, 16, a0, a1) for b in batches]
+    res["strategies"]["A_task_fused"] = {"deployment": depA, "step_s": float(np.mean([x[0] for x in sA]))}
+    # B-D on the best heterogeneous deployment for D (covering the longest sequence)
+    best = None
+    for dep in deployments(n):
+        if max(g[2] for g in dep) < longest:
+            continue
+        sD = [step_time(dep, b, 0, 256, 16, a0, a1)[0] for b in batches[:5]]
+        key = float(np.mean(sD))
+        if best is None or key < best[0]:
+            best = (key, dep)
+    dep = best[1]
+    for name, mode, grid in (("B_hetero_length_fixed", 1, 1024), ("C_hetero_balanced_fixed", 0, 1024),
+                             ("D_lobra_balanced_dynamic", 0, 256)):
+        st = [step_time(dep, b, mode, grid, 16, a0, a1) for b in batches]
+        res["strategies"][name] = {"deployment": dep, "step_s": float(np.mean([x[0] for x in st])),
+                                   "mean_replica_s": float(np.mean([x[1] for x in st]))}
+    base = res["strategies"]["A_task_fused"]["step_s"]
+    for k, v in res["strategies"].items():
+        v["gpu_seconds"] = n * v["step_s"]
+        v["reduction_vs_task_fused"] = 1.0 - v["step_s"] / base
+    res["planning_wall_s"] = time.time() - t0
+    res["tokens_per_step"] = float(np.mean([b.T for b in batches]))
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump(res, open(args.out, "w"), indent=1)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
