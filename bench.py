@@ -103,18 +103,34 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ plans
-def deployment_for(n_gpus: int):
-    """(tp, replicas, max_tokens) per group, ordered by (tp, M) -- SURVEY.md §8(d)."""
+CANDIDATES = [(1, 16384), (2, 32768)]   # (TP degree, max tokens per chunk), Q25
+
+
+def deployment_for(n_gpus: int, tasks=None):
+    """(tp, replicas, max_tokens) per deployed group, ordered by (tp, M), chosen by the
+    paper's stage-1 planner (lobra_plan_deployment: §4.2 Eq. 2 + App. A) on a sample of
+    100 x B lengths of the step's task mix with the bench cost model."""
     if n_gpus == 1:
         return [(1, 1, 16384)]
-    if n_gpus == 2:
-        return [(1, 2, 16384)]
-    if n_gpus == 4:
-        return [(1, 2, 16384), (2, 1, 32768)]
-    if n_gpus == 8:
-        return [(1, 4, 16384), (2, 2, 32768)]
-    if n_gpus % 2 == 0:
-        return [(1, n_gpus - 2, 16384), (2, 1, 32768)]
+    from paper_2509_01193_b200 import _lib
+    from workloads import synth
+    tasks = tasks or synth.c2_tasks()
+    per_step = synth.pack_tokens(tasks, T_PER_GPU * n_gpus, 4096, seed=7).seq_lens
+    sample = synth.sample_batch(tasks, seed=8, l_max=4096,
+                                per_task=[max(1, 100 * len(per_step) * t.batch_size //
+                                              sum(x.batch_size for x in tasks)) for t in tasks])
+    grid_max = max(m for _, m in CANDIDATES)
+    cands = [(tp, 0, m) for tp, m in CANDIDATES]
+    try:
+        res = _lib.lobra_plan_deployment([c[0] for c in cands], [c[2] for c in cands],
+                                         cost_table(cands, 256, grid_max), n_gpus, sample.seq_lens,
+                                         len(per_step), 256, grid_max, 16)
+        groups = [(tp, int(p), m) for (tp, m), p in zip(CANDIDATES, res["replicas"]) if p > 0]
+        used = sum(tp * p for tp, p, _ in groups)
+        if used == n_gpus:
+            return groups
+    except Exception:
+        pass
     return [(1, n_gpus, 16384)]
 
 

@@ -217,6 +217,49 @@ LOBRA_API lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_b
                             int32_t chunking, int64_t node_cap, lobra_dispatch_out* out);
 
 /* ------------------------------------------------------------------------------
+ * Stage-1 deployment planning (§4.2 Eq. 2, App. A, PP = 1).
+ *  1. bucket a length sample with the dynamic-bucketing DP ("randomly sample a
+ *     large number (100 x B by default) of training data and perform the bucketing");
+ *  2. demands B_j = ceil(batch_size * f_j), f_j = sample fraction of bucket j (reading
+ *     Q22); batch_size = 0 uses the sample's bucket counts as the demands (Eq. 1 with a
+ *     concrete batch);
+ *  3. configuration proposal (App. A Observation 1): a candidate is dropped when another
+ *     with the same GPU count supports at least as long sequences at no higher cost;
+ *  4. enumerate the maximal plans sum_i p_i n_i <= N covering every demanded bucket
+ *     (App. A "integer partition problem");
+ *  5. Theorem-1 lower bound (App. A): length-based dispatch times t_i, bound
+ *     sum_i N_i t_i / sum_i N_i; keep plans within (1 + threshold) of the minimum bound
+ *     (threshold < 0: keep all; 0.15 in the paper);
+ *  6. solve Eq. 3 exactly for every kept plan; return the best (ties: fewer GPUs, fewer
+ *     replicas, lexicographically smaller p).
+ * Host only, deterministic.  Errors: LOBRA_ERR_INPUT, LOBRA_ERR_INFEASIBLE (no plan covers
+ * the longest bucket), LOBRA_ERR_BUDGET (a per-plan solve hit node_cap; best incumbent).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_configs;         /* S candidate configurations                             */
+  const int32_t* tp;           /* [S] n_i GPUs per replica                                */
+  const int32_t* max_tokens;   /* [S] M_i, multiple of grid_step                         */
+  const int64_t* cost;         /* [S * U] integer cost of one sequence at grid value u_k */
+} lobra_candidates;
+
+typedef struct {
+  int32_t* replicas;           /* [S] out: p_i (0 = not deployed)                         */
+  int32_t* boundaries;         /* [R] out: bucket boundaries                              */
+  int64_t* demands;            /* [R] out: B_j                                            */
+  int32_t num_buckets;         /* out                                                     */
+  int32_t plans_total;         /* out: maximal covering plans                             */
+  int32_t plans_solved;        /* out: plans kept by the lower-bound filter               */
+  int32_t gpus_used;           /* out                                                     */
+  int64_t t_hat;               /* out: Eq. 3 objective of the chosen plan                 */
+} lobra_plan_out;
+
+LOBRA_API lobra_status lobra_plan_deployment(const lobra_candidates* cand, int32_t n_gpus,
+                                             const int32_t* lens, int32_t n_lens,
+                                             int32_t batch_size, int32_t grid_step,
+                                             int32_t grid_max, int32_t R, double threshold,
+                                             int64_t node_cap, lobra_plan_out* out);
+
+/* ------------------------------------------------------------------------------
  * Communication (NCCL over NVLink/NVSwitch).  One process per GPU.
  * ------------------------------------------------------------------------------ */
 /* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (e.g. with

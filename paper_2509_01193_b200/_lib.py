@@ -25,7 +25,7 @@ EXPORTED = [
     "lobra_lora_fwd", "lobra_lora_bwd", "lobra_dispatch", "lobra_nccl_unique_id",
     "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
     "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
-    "lobra_adamw_step",
+    "lobra_adamw_step", "lobra_plan_deployment",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim"]
 
@@ -58,6 +58,16 @@ class DispatchOut(C.Structure):
                 ("seq_bucket", _i32p), ("seq_replica", _i32p), ("seq_chunk", _i32p),
                 ("pack_order", _i32p), ("replica_cost", _i64p), ("t_hat", C.c_int64),
                 ("nodes", C.c_int64)]
+
+
+class Candidates(C.Structure):
+    _fields_ = [("num_configs", C.c_int32), ("tp", _i32p), ("max_tokens", _i32p), ("cost", _i64p)]
+
+
+class PlanOut(C.Structure):
+    _fields_ = [("replicas", _i32p), ("boundaries", _i32p), ("demands", _i64p),
+                ("num_buckets", C.c_int32), ("plans_total", C.c_int32), ("plans_solved", C.c_int32),
+                ("gpus_used", C.c_int32), ("t_hat", C.c_int64)]
 
 
 class AdamHP(C.Structure):
@@ -121,6 +131,10 @@ def load() -> C.CDLL:
     lib.lobra_profile_read.restype = C.c_int
     lib.lobra_profile_read.argtypes = [C.POINTER(Profile), C.c_int]
     lib.lobra_launch_count.restype = C.c_int64
+    lib.lobra_plan_deployment.restype = C.c_int
+    lib.lobra_plan_deployment.argtypes = [C.POINTER(Candidates), C.c_int32, _i32p, C.c_int32,
+                                          C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                          C.c_int64, C.POINTER(PlanOut)]
     lib.lobra_adamw_step.restype = C.c_int
     lib.lobra_adamw_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_size_t, C.POINTER(AdamHP), C.c_int32,
@@ -327,3 +341,29 @@ def lobra_adamw_step(params, grads, m, v, hparams, step, group=None, params_bf16
     _check(load().lobra_adamw_step(_ptr(params), _ptr(params_bf16), _ptr(grads), _ptr(m), _ptr(v),
                                    _ptr(group), int(params.numel()), hp, len(hparams), int(step),
                                    float(grad_scale), _stream(stream)))
+
+
+# ---------------------------------------------------------------------------- planner
+def lobra_plan_deployment(tp, max_tokens, cost, n_gpus, lens, batch_size=0, grid_step=256,
+                          grid_max=16384, R=16, threshold=0.15, node_cap=0):
+    """Stage-1 deployment planning (include/lobra.h).  Returns a dict; raises LobraError
+    on input/infeasible errors (status LOBRA_ERR_BUDGET is reported in the dict)."""
+    tp, max_tokens, lens = _i32(tp), _i32(max_tokens), _i32(lens)
+    cost = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
+    S = len(tp)
+    reps = np.zeros(S, np.int32)
+    bnd = np.zeros(R, np.int32)
+    dem = np.zeros(R, np.int64)
+    cand = Candidates(S, tp.ctypes.data_as(_i32p), max_tokens.ctypes.data_as(_i32p),
+                      cost.ctypes.data_as(_i64p))
+    o = PlanOut(reps.ctypes.data_as(_i32p), bnd.ctypes.data_as(_i32p), dem.ctypes.data_as(_i64p),
+                0, 0, 0, 0, 0)
+    st = load().lobra_plan_deployment(C.byref(cand), n_gpus, lens.ctypes.data_as(_i32p), len(lens),
+                                      batch_size, grid_step, grid_max, R, threshold, node_cap,
+                                      C.byref(o))
+    if st not in (LOBRA_OK, LOBRA_ERR_BUDGET):
+        raise LobraError(st, load().lobra_last_error().decode())
+    nb = o.num_buckets
+    return {"status": st, "replicas": reps, "boundaries": bnd[:nb], "demands": dem[:nb],
+            "plans_total": o.plans_total, "plans_solved": o.plans_solved, "gpus_used": o.gpus_used,
+            "t_hat": int(o.t_hat)}

@@ -24,6 +24,8 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -112,12 +114,15 @@ struct Two {
   Two(const Inst& in, int ga, int gb, std::vector<i64> dem, i64 la, i64 lb, i64 ub, Budget& bud)
       : I(in), a(ga), b(gb), D(std::move(dem)), La(la), Lb(lb), UB(ub) {
     if (UB < 0) return;
-    const int R = I.R;
+    Suf.assign(I.R + 1, std::vector<i64>(UB + 1, 0));
+    ok = layers(I.R, bud);
+  }
+  // (Re)compute Suf[j] for j = top-1 .. 0 (Suf[top..R] unchanged).
+  bool layers(int top, Budget& bud) {
     i64 cells = 0;
-    for (int j = 0; j < R; ++j) cells += (UB + 1) * (cdiv(D[j], I.p[a]) + 2);
-    if (!bud.take(cells)) return;
-    Suf.assign(R + 1, std::vector<i64>(UB + 1, 0));
-    for (int j = R - 1; j >= 0; --j) {
+    for (int j = 0; j < top; ++j) cells += (UB + 1) * (cdiv(D[j], I.p[a]) + 2);
+    if (!bud.take(cells)) return false;
+    for (int j = top - 1; j >= 0; --j) {
       std::vector<i64>& cur = Suf[j];
       const std::vector<i64>& nxt = Suf[j + 1];
       std::fill(cur.begin(), cur.end(), BIG);
@@ -142,7 +147,17 @@ struct Two {
         }
       }
     }
-    ok = true;
+    return true;
+  }
+  // New residual demands (same groups, UB, loads): recompute only the layers at and below
+  // the last bucket whose demand changed.
+  bool update(const std::vector<i64>& dem, Budget& bud) {
+    int top = 0;
+    for (int j = 0; j < I.R; ++j)
+      if (dem[j] != D[j]) top = j + 1;
+    D = dem;
+    ok = layers(top, bud);
+    return ok;
   }
   // min over budgets of max(La + b, Lb + Suf_0(b))
   i64 best() const {
@@ -217,6 +232,7 @@ struct Multi {
   bool want_lex = false;
   i64 target = BIG;
   bool done = false;
+  std::unique_ptr<Two> leaf;
   Multi(const Inst& in, Budget& b, i64 ub) : I(in), bud(b), UB(ub) {
     cur.assign(I.G, std::vector<i64>(I.R, 0));
   }
@@ -225,9 +241,15 @@ struct Multi {
     if (done || bud.hit) return;
     const int G = I.G;
     if (i == G - 2) {
-      Two two(I, G - 2, G - 1, rem, load[G - 2], load[G - 1],
-              (want_lex ? target : std::min(best, UB)) - load[G - 2], bud);
-      if (!two.ok) return;
+      // the leading groups never load groups G-2, G-1: La = Lb = 0; one cached 2-group DP
+      // over budgets 0..UB, updated incrementally from leaf to leaf
+      if (!leaf) {
+        leaf.reset(new Two(I, G - 2, G - 1, rem, 0, 0, UB, bud));
+      } else if (!leaf->update(rem, bud)) {
+        return;
+      }
+      if (!leaf->ok) return;
+      Two& two = *leaf;
       if (!want_lex) {
         const i64 t = std::max(two.best(), *std::max_element(load.begin(), load.end() - 2));
         if (t < best) {
@@ -235,7 +257,8 @@ struct Multi {
         }
       } else {
         std::vector<i64> da;
-        if (two.lexmin(target, da)) {
+        const i64 lead = *std::max_element(load.begin(), load.end() - 2);
+        if (lead <= target && two.lexmin(target, da)) {
           sol = cur;
           for (int jj = 0; jj < I.R; ++jj) {
             sol[G - 2][jj] = da[jj];
@@ -273,6 +296,40 @@ struct Multi {
     }
   }
 };
+
+// Exact Eq. 3 over the deployed groups of L: the lexicographically smallest optimal d
+// (reading Q12).  false = node budget hit (dl then holds the best incumbent found, or
+// the length-based solution).
+bool eq3_exact(const Inst& L, const std::vector<i64>& tp, Budget& bud,
+               std::vector<std::vector<i64>>& dl) {
+  dl = by_length(L, tp);
+  if (L.G == 1) {
+    dl[0] = L.Bj;
+    return true;
+  }
+  const i64 UB = objective(L, dl);
+  if (L.G == 2) {
+    Two two(L, 0, 1, L.Bj, 0, 0, UB, bud);
+    std::vector<i64> da;
+    if (two.ok) {
+      const i64 t = two.best();
+      if (two.lexmin(t, da))
+        for (int j = 0; j < L.R; ++j) dl[0][j] = da[j], dl[1][j] = L.Bj[j] - da[j];
+    }
+  } else {
+    Multi m(L, bud, UB);
+    std::vector<i64> rem = L.Bj, load(L.G, 0);
+    m.best = UB + 1;
+    m.rec(0, 0, rem, load);
+    if (!bud.hit && m.best <= UB) {
+      m.want_lex = true;
+      m.target = m.best;
+      m.rec(0, 0, rem, load);
+      if (m.done) dl = m.sol;
+    }
+  }
+  return !bud.hit;
+}
 
 }  // namespace
 
@@ -376,33 +433,7 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   if (mode == 2) {
     for (int j = 0; j < Rb; ++j) dl[0][j] = Bj[j];
   }
-  if (mode == 0 && L.G >= 2) {
-    const i64 UB = objective(L, dl);
-    if (L.G == 2) {
-      Two two(L, 0, 1, Bj, 0, 0, UB, bud);
-      std::vector<i64> da;
-      if (two.ok) {
-        const i64 t = two.best();
-        if (two.lexmin(t, da)) {
-          for (int j = 0; j < Rb; ++j) dl[0][j] = da[j], dl[1][j] = Bj[j] - da[j];
-        }
-      }
-    } else {
-      Multi m(L, bud, UB);
-      std::vector<i64> rem = Bj, load(L.G, 0);
-      m.best = UB + 1;
-      m.rec(0, 0, rem, load);
-      if (!bud.hit && m.best <= UB) {
-        m.want_lex = true;
-        m.target = m.best;
-        m.rec(0, 0, rem, load);
-        if (m.done) dl = m.sol;
-      }
-    }
-    if (bud.hit) st = LOBRA_ERR_BUDGET;
-  } else if (mode == 0 && L.G == 1) {
-    for (int j = 0; j < Rb; ++j) dl[0][j] = Bj[j];
-  }
+  if (mode == 0 && !eq3_exact(L, ltp, bud, dl)) st = LOBRA_ERR_BUDGET;
   // write d (all groups; undeployed rows are 0)
   std::vector<std::vector<i64>> d(G, std::vector<i64>(Rb, 0));
   for (size_t k = 0; k < live.size(); ++k) d[live[k]] = dl[k];
@@ -534,4 +565,179 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   out->nodes = bud.used;
   if (st == LOBRA_ERR_BUDGET) lobra::set_error("Eq. 3 solver node cap hit; incumbent returned");
   return st;
+}
+
+// ------------------------------------------------------------------ stage-1 planner
+extern "C" lobra_status lobra_plan_deployment(const lobra_candidates* cand, int32_t n_gpus,
+                                              const int32_t* lens, int32_t n_lens,
+                                              int32_t batch_size, int32_t grid_step,
+                                              int32_t grid_max, int32_t R, double threshold,
+                                              int64_t node_cap, lobra_plan_out* out) {
+  using lobra::fail;
+  lobra::clear_error();
+  if (!cand || !lens || !out || !out->replicas || !out->boundaries || !out->demands)
+    return fail(LOBRA_ERR_INPUT, "null argument");
+  const int S = cand->num_configs;
+  if (S < 1 || !cand->tp || !cand->max_tokens || !cand->cost)
+    return fail(LOBRA_ERR_INPUT, "candidate arrays missing");
+  if (n_gpus < 1 || n_lens < 1 || batch_size < 0 || R < 1)
+    return fail(LOBRA_ERR_INPUT, "need n_gpus >= 1, n_lens >= 1, batch_size >= 0, R >= 1");
+  if (grid_step < 1 || grid_max < grid_step || grid_max % grid_step)
+    return fail(LOBRA_ERR_INPUT, "grid_max must be a positive multiple of grid_step");
+  const int U = grid_max / grid_step;
+  for (int i = 0; i < S; ++i)
+    if (cand->tp[i] < 1 || cand->max_tokens[i] < grid_step || cand->max_tokens[i] % grid_step)
+      return fail(LOBRA_ERR_INPUT, "candidate %d: tp >= 1, max_tokens multiple of grid_step", i);
+  // 1. histogram + dynamic bucketing of the sample
+  std::vector<i64> hist(U, 0);
+  for (int k = 0; k < n_lens; ++k) {
+    const i64 l = lens[k];
+    if (l < 1) return fail(LOBRA_ERR_INPUT, "sample length %lld < 1", (long long)l);
+    if (l > grid_max) return fail(LOBRA_ERR_INFEASIBLE, "sample length %lld exceeds the grid", (long long)l);
+    hist[cdiv(l, grid_step) - 1]++;
+  }
+  std::vector<i64> ou, oc;
+  for (int k = 0; k < U; ++k)
+    if (hist[k]) ou.push_back((i64)(k + 1) * grid_step), oc.push_back(hist[k]);
+  const std::vector<i64> bnd = bucketize(ou, oc, R);
+  const int Rb = (int)bnd.size();
+  std::vector<i64> cnt(Rb, 0);
+  {
+    size_t v = 0;
+    for (int j = 0; j < Rb; ++j)
+      while (v < ou.size() && ou[v] <= bnd[j]) cnt[j] += oc[v++];
+  }
+  // 2. demands
+  std::vector<i64> Bj(Rb);
+  for (int j = 0; j < Rb; ++j)
+    Bj[j] = batch_size > 0 ? ((i64)batch_size * cnt[j] + n_lens - 1) / n_lens : cnt[j];
+  // per-config support and costs
+  std::vector<int> r(S, 0);
+  std::vector<std::vector<i64>> c(S, std::vector<i64>(Rb));
+  for (int i = 0; i < S; ++i)
+    for (int j = 0; j < Rb; ++j) {
+      r[i] += bnd[j] <= cand->max_tokens[i];
+      c[i][j] = cand->cost[(size_t)i * U + (bnd[j] / grid_step - 1)];
+    }
+  // 3. configuration proposal: drop dominated candidates with the same GPU count
+  std::vector<char> keep(S, 1);
+  for (int a = 0; a < S; ++a)
+    for (int b = 0; b < S && keep[a]; ++b) {
+      if (a == b || !keep[b] || cand->tp[a] != cand->tp[b] || r[b] < r[a]) continue;
+      bool dom = true;
+      for (int j = 0; j < r[a]; ++j) dom &= c[b][j] <= c[a][j];
+      if (!dom) continue;
+      bool strict = r[b] > r[a];
+      for (int j = 0; j < r[a]; ++j) strict |= c[b][j] < c[a][j];
+      if (strict || b < a) keep[a] = 0;
+    }
+  int last = -1;
+  for (int j = 0; j < Rb; ++j)
+    if (Bj[j] > 0) last = j;
+  int min_n = INT32_MAX;
+  for (int i = 0; i < S; ++i)
+    if (keep[i]) min_n = std::min(min_n, (int)cand->tp[i]);
+  // 4. maximal covering plans
+  std::vector<std::vector<int>> plans;
+  std::vector<int> p(S, 0);
+  std::function<void(int, int)> rec = [&](int i, int left) {
+    if (i == S) {
+      if (left >= min_n) return;                       // not maximal
+      int cover = 0;
+      for (int k = 0; k < S; ++k)
+        if (p[k]) cover = std::max(cover, r[k]);
+      if (cover - 1 < last) return;                    // longest demanded bucket uncovered
+      plans.push_back(p);
+      return;
+    }
+    if (!keep[i]) {
+      p[i] = 0;
+      rec(i + 1, left);
+      return;
+    }
+    for (int q = left / cand->tp[i]; q >= 0; --q) {
+      p[i] = q;
+      rec(i + 1, left - q * cand->tp[i]);
+    }
+    p[i] = 0;
+  };
+  rec(0, n_gpus);
+  if (plans.empty()) return fail(LOBRA_ERR_INFEASIBLE, "no deployment plan covers the longest bucket");
+  // 5. Theorem-1 lower bounds via length-based dispatch
+  struct Cand {
+    double lb;
+    int idx;
+  };
+  std::vector<Cand> lbs;
+  auto make_inst = [&](const std::vector<int>& pl, std::vector<i64>& tp_l) {
+    Inst L;
+    L.R = Rb;
+    L.Bj = Bj;
+    for (int i = 0; i < S; ++i)
+      if (pl[i] > 0) {
+        L.p.push_back(pl[i]);
+        L.r.push_back(r[i]);
+        L.c.push_back(c[i]);
+        tp_l.push_back(cand->tp[i]);
+      }
+    L.G = (int)L.p.size();
+    return L;
+  };
+  for (size_t k = 0; k < plans.size(); ++k) {
+    std::vector<i64> tpl;
+    Inst L = make_inst(plans[k], tpl);
+    const auto d = by_length(L, tpl);
+    double num = 0, den = 0;
+    for (int g = 0; g < L.G; ++g) {
+      i64 t = 0;
+      for (int j = 0; j < Rb; ++j) t += L.cost(g, j, d[g][j]);
+      num += (double)(L.p[g] * tpl[g]) * (double)t;
+      den += (double)(L.p[g] * tpl[g]);
+    }
+    lbs.push_back({num / den, (int)k});
+  }
+  double min_lb = lbs[0].lb;
+  for (auto& e : lbs) min_lb = std::min(min_lb, e.lb);
+  // 6. exact Eq. 3 per kept plan
+  Budget bud{node_cap > 0 ? node_cap : (i64)400000000};
+  bool hit = false;
+  int solved = 0;
+  i64 best_t = BIG;
+  int best = -1;
+  auto better = [&](i64 t, int k) {
+    if (best < 0 || t != best_t) return best < 0 || t < best_t;
+    auto key = [&](const std::vector<int>& pl) {
+      i64 g = 0, rp = 0;
+      for (int i = 0; i < S; ++i) g += (i64)pl[i] * cand->tp[i], rp += pl[i];
+      return std::make_pair(g, rp);
+    };
+    const auto a = key(plans[k]), b = key(plans[best]);
+    if (a != b) return a < b;
+    return plans[k] < plans[best];
+  };
+  for (auto& e : lbs) {
+    if (threshold >= 0 && e.lb > (1.0 + threshold) * min_lb + 1e-9) continue;
+    std::vector<i64> tpl;
+    Inst L = make_inst(plans[e.idx], tpl);
+    std::vector<std::vector<i64>> d;
+    Budget b1{bud.cap};
+    if (!eq3_exact(L, tpl, b1, d)) hit = true;
+    ++solved;
+    const i64 t = objective(L, d);
+    if (better(t, e.idx)) best_t = t, best = e.idx;
+  }
+  for (int i = 0; i < S; ++i) out->replicas[i] = plans[best][i];
+  out->num_buckets = Rb;
+  for (int j = 0; j < Rb; ++j) out->boundaries[j] = (int32_t)bnd[j], out->demands[j] = Bj[j];
+  out->plans_total = (int)plans.size();
+  out->plans_solved = solved;
+  int g = 0;
+  for (int i = 0; i < S; ++i) g += plans[best][i] * cand->tp[i];
+  out->gpus_used = g;
+  out->t_hat = best_t;
+  if (hit) {
+    lobra::set_error("a per-plan Eq. 3 solve hit the node cap; incumbents used");
+    return LOBRA_ERR_BUDGET;
+  }
+  return LOBRA_OK;
 }
