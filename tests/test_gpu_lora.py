@@ -311,3 +311,45 @@ def test_abi_rejects_bad_input_before_launch():
     with pytest.raises(_lib.LobraError) as e:                        # rank 65
         _lib.lobra_lora_fwd(X, W, W, W, [65], [1.0], [4], [0], X, X, X, ws_bytes=1 << 20)
     assert e.value.status == _lib.LOBRA_ERR_INPUT
+
+
+def test_empty_batch():
+    """T = 0 (every sequence empty): forward is a no-op, backward writes zero adapter
+    gradients (reading Q10) and leaves dX alone."""
+    torch = _torch()
+    from paper_2509_01193_b200 import _lib
+    dev = torch.device("cuda:0")
+    for code, td in ((_lib.LOBRA_BF16, torch.bfloat16), (_lib.LOBRA_FP32, torch.float32)):
+        X = torch.zeros(1, 64, device=dev, dtype=td)
+        W = torch.zeros(64, 64, device=dev, dtype=td)
+        A = torch.zeros(8, 64, device=dev, dtype=td)
+        B = torch.zeros(64, 8, device=dev, dtype=td)
+        ws = torch.empty(_lib.lobra_lora_workspace_bytes(code, 64, 64, [0, 0], [0, 1], [4, 4], [1, 1]),
+                         dtype=torch.uint8, device=dev)
+        Hs = torch.empty(_lib.lobra_lora_saved_bytes(code, 64, 64, [0, 0], [0, 1], [4, 4], [1, 1]),
+                         dtype=torch.uint8, device=dev)
+        _lib.lobra_lora_fwd(X, W, A, B, [4, 4], [1, 1], [0, 0], [0, 1], X, Hs, ws)
+        dA = torch.full((8, 64), 7.0, device=dev)
+        dB = torch.full((64, 8), 7.0, device=dev)
+        _lib.lobra_lora_bwd(X, W, A, B, [4, 4], [1, 1], [0, 0], [0, 1], Hs, X, X, dA, dB, ws)
+        torch.cuda.synchronize()
+        assert not dA.any() and not dB.any()
+        dA.fill_(7.0)
+        _lib.lobra_lora_bwd(X, W, A, B, [4, 4], [1, 1], [0, 0], [0, 1], Hs, X, X, dA, dB, ws,
+                            accumulate_dadb=True)
+        torch.cuda.synchronize()
+        assert (dA == 7.0).all()
+
+
+def test_workspace_too_small_is_rejected():
+    torch = _torch()
+    from paper_2509_01193_b200 import _lib
+    dev = torch.device("cuda:0")
+    X = torch.zeros(300, 128, device=dev, dtype=torch.bfloat16)
+    W = torch.zeros(128, 128, device=dev, dtype=torch.bfloat16)
+    A = torch.zeros(16, 128, device=dev, dtype=torch.bfloat16)
+    B = torch.zeros(128, 16, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(1024, dtype=torch.uint8, device=dev)
+    with pytest.raises(_lib.LobraError) as e:
+        _lib.lobra_lora_fwd(X, W, A, B, [16], [1.0], [300], [0], X, X, ws)
+    assert e.value.status == _lib.LOBRA_ERR_INPUT and "workspace" in str(e.value)
