@@ -1037,6 +1037,221 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // =====================================================================================
+// Fused backward dY pass: ONE HBM read of dY computes both
+//   G_s  = s_t dY B_t        (per row: reduction over `out`)   -> fp32 partials per
+//                                                                (slot, 512-col chunk)
+//   dB_t = H_s^T dY          (per column: reduction over tokens) -> fp32 partials per
+//                                                                (unit, 128-col block)
+// Work item = (dy unit u: consecutive slots of one task, 512-column chunk c).  Per slot and
+// 128-column sub-block b the stage holds the dY tile (2 boxes, K-major for G / MN-major for
+// dB), the H slot (MN-major B for dB) and B^T[qp x 128] (K-major B for G).  TMEM: four dB
+// accumulators (4 x 64 cols) kept across the unit's slots + two G accumulators (2 x 64).
+// k_gfin then sums the G chunk partials in fixed order, scales by s_t, masks and writes
+// the bf16 G slots; the dB partials go through k_finalize (fixed order) as before.
+// =====================================================================================
+constexpr int Y_STAGES = 3;
+constexpr int Y_Z_BYTES = 2 * 128 * 64 * 2;   // dY tile: 2 boxes of 64 cols x 128 rows
+constexpr int Y_H_BYTES = 128 * 64 * 2;       // H slot
+constexpr int Y_BT_MAX = 2 * 64 * 128;        // B^T: 2 boxes of 64 cols x qp(<=64) rows
+constexpr int Y_STAGE_BYTES = Y_Z_BYTES + Y_H_BYTES + Y_BT_MAX;
+constexpr int Y_SMEM = Y_STAGES * Y_STAGE_BYTES + 1024 + 256;
+
+struct DyArgs {
+  int width, nchunks, nitems, n128, qp;
+  float* gpart;    // [nslots][nchunks][128][qp]
+  float* bpart;    // [ndyunits][n128][qp][128]   (k_finalize layout)
+  Meta meta;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    k_dypass(const __grid_constant__ CUtensorMap mapDY, const __grid_constant__ CUtensorMap mapH,
+             const __grid_constant__ CUtensorMap mapBt, const DyArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Y_STAGES * Y_STAGE_BYTES);
+  uint64_t* empty = full + Y_STAGES;
+  uint64_t* gfull = empty + Y_STAGES;    // [2]
+  uint64_t* gempty = gfull + 2;          // [2]
+  uint64_t* bfull = gempty + 2;          // [1]
+  uint64_t* bempty = bfull + 1;          // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+  const int bt_box = args.qp * 128;      // one 64-col box of B^T rows
+
+  if (warp == 0 && lane == 0) tma_prefetch(&mapDY), tma_prefetch(&mapH), tma_prefetch(&mapBt);
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < Y_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&gfull[a], 1), mbar_init(&gempty[a], 128);
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
+        const int u = item / args.nchunks, c = item % args.nchunks;
+        const int t = meta.dy_unit_task[u];
+        const int nb = min(4, args.n128 - c * 4);
+        for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k) {
+          const int sl = meta.task_slots[k];
+          const int tile = meta.slot_tile[sl];
+          for (int b = 0; b < nb; ++b) {
+            const int col = c * 512 + b * 128;
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
+            uint8_t* st = smem + stage * Y_STAGE_BYTES;
+            tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
+            tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
+            tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], 0, sl * kTileM);
+            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES, &mapBt, &full[stage], col, meta.roff[t]);
+            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES + bt_box, &mapBt, &full[stage], col + 64, meta.roff[t]);
+            if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t id_b = idesc_bf16(128, 64, true, true);          // dB: both MN-major
+      const uint32_t id_g = idesc_bf16(128, args.qp, false, false);   // G: both K-major
+      int stage = 0;
+      uint32_t phase = 0;
+      int gcount = 0, it = 0;
+      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
+        const int u = item / args.nchunks, c = item % args.nchunks;
+        const int nb = min(4, args.n128 - c * 4);
+        mbar_wait(bempty, (it & 1) ^ 1);
+        tc_fence_after();
+        bool first_slot = true;
+        for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k, ++gcount) {
+          const int gb = gcount & 1;
+          mbar_wait(&gempty[gb], ((gcount >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dg = tmem + 256 + gb * 64;
+          for (int b = 0; b < nb; ++b) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t z0 = smem_u32(smem + stage * Y_STAGE_BYTES);
+            const uint32_t h0 = z0 + Y_Z_BYTES;
+            const uint32_t t0 = h0 + Y_H_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)   // dB[b] += dY^T H   (K = 128 tokens)
+              mma_bf16(tmem + b * 64, sdesc_sw128(z0 + kk * 2048, 16384, 1024),
+                       sdesc_sw128(h0 + kk * 2048, 8192, 1024), id_b,
+                       (first_slot && kk == 0) ? 0u : 1u);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)      // G += dY[:, 64 cols] B^T[qp, 64 cols]^T
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16(dg, sdesc_sw128(z0 + j * 16384 + kk * 32, 16, 1024),
+                         sdesc_sw128(t0 + j * bt_box + kk * 32, 16, 1024), id_g,
+                         (b == 0 && j == 0 && kk == 0) ? 0u : 1u);
+            mma_commit(&empty[stage]);
+            if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+          }
+          mma_commit(&gfull[gb]);
+          first_slot = false;
+        }
+        mma_commit(bfull);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue
+    const uint32_t q = warp - 4;
+    const int lr = q * 32 + lane;    // row of the tile (G) / column of the sub-block (dB)
+    int gcount = 0, it = 0;
+    for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
+      const int u = item / args.nchunks, c = item % args.nchunks;
+      const int nb = min(4, args.n128 - c * 4);
+      const int t = meta.dy_unit_task[u];
+      const int rp = rpad16(meta.ranks[t]);
+      for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k, ++gcount) {
+        const int gb = gcount & 1;
+        const int sl = meta.task_slots[k];
+        mbar_wait(&gfull[gb], (gcount >> 1) & 1);
+        tc_fence_after();
+        float* dst = args.gpart + (((size_t)sl * args.nchunks + c) * kTileM + lr) * args.qp;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (h * 32 >= rp) break;
+          float v[32];
+          tmem_ld32(tmem + ((q * 32u) << 16) + 256 + gb * 64 + h * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (h * 32 + j < rp)
+              *reinterpret_cast<float4*>(dst + h * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(&gempty[gb]);
+      }
+      mbar_wait(bfull, it & 1);
+      tc_fence_after();
+      for (int b = 0; b < nb; ++b) {
+        float* dst = args.bpart + ((size_t)(u * args.n128 + c * 4 + b) * meta.qp) * 128 + lr;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (h * 32 >= rp) break;
+          float v[32];
+          tmem_ld32(tmem + ((q * 32u) << 16) + b * 64 + h * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (h * 32 + j < rp) dst[(size_t)(h * 32 + j) * 128] = v[j];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// G slots from the chunk partials: slot[s][row][q] = s_t * sum_c gpart[s][c][row][q] for
+// rows of the slot's task and q < r_t, zero otherwise; also the all-zero slot nslots.
+__global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Meta meta,
+                       __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int total = (meta.nslots + 1) * kTileM;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int s = i / kTileM, lrow = i % kTileM;
+    float v[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = 0.0f;
+    int rp = 0;
+    float sc = 0.0f;
+    if (s < meta.nslots) {
+      const int t = meta.slot_task[s];
+      const int row = meta.slot_tile[s] * kTileM + lrow;
+      if (row < meta.T && row_task(meta, row) == t) {
+        rp = meta.ranks[t];
+        sc = meta.scales[t];
+        for (int c = 0; c < nchunks; ++c) {
+          const float* src = gpart + (((size_t)s * nchunks + c) * kTileM + lrow) * qp;
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < rp) v[j] += src[j];
+        }
+      }
+    }
+    store_slot_row(out, s, lrow, v, sc, rp);
+  }
+}
+
+// =====================================================================================
 // small helper kernels
 // =====================================================================================
 // B_cat [out, rsum] -> Bp [out, ld8]: task t's r_t columns at boff[t], zero padding.
@@ -1064,7 +1279,8 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
   int t = 0;
   while (meta.roff[t + 1] <= rq) ++t;
   const int q = rq - meta.roff[t];
-  const int u0 = meta.task_unit_off[t], u1 = meta.task_unit_off[t + 1];
+  const int* tuo = (mode == 1 && meta.use_dy_units) ? meta.dy_task_unit_off : meta.task_unit_off;
+  const int u0 = tuo[t], u1 = tuo[t + 1];
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
     const int c = col >> 7, ci = col & 127;
     float s = 0.0f;
@@ -1247,6 +1463,30 @@ void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, 
     case 3: launch_rpld<2, 2>(grid, mapVk, a, st); break;
     default: launch_rpld<3, 2>(grid, mapVk, a, st); break;
   }
+}
+
+void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
+                   int width, int qp, const Meta& meta, float* gpart, float* bpart,
+                   __nv_bfloat16* gslots, int num_sms, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_dypass, cudaFuncAttributeMaxDynamicSharedMemorySize, Y_SMEM);
+    init = true;
+  }
+  DyArgs a;
+  a.width = width;
+  a.n128 = (width + 127) / 128;
+  a.nchunks = (width + 511) / 512;
+  a.nitems = meta.ndyunits * a.nchunks;
+  a.qp = qp;
+  a.gpart = gpart;
+  a.bpart = bpart;
+  a.meta = meta;
+  if (a.nitems > 0) {
+    const int grid = a.nitems < num_sms ? a.nitems : num_sms;
+    launch_k(k_dypass, dim3(grid), dim3(256), Y_SMEM, st, mapDY, mapH, mapBt, a);
+  }
+  launch_k(k_gfin, dim3(num_sms * 2), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
 }
 
 bool gemm_uses_pair() {

@@ -215,10 +215,11 @@ struct Plan {
   // offsets (in int32 words) of each array inside buf
   int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
       o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_boff,
+      o_dy_unit_task, o_dy_unit_s0, o_dy_unit_s1, o_dy_task_unit_off,
       o_scales;
   int ld8 = 0;      // row stride of the B operand the kernels read (rsum if direct)
   bool bdirect = true;
-  int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16;
+  int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16, ndyunits = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -256,8 +257,8 @@ lobra_status validate(const lobra_problem* prob, const lobra_batch* b, const lob
   return LOBRA_OK;
 }
 
-void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int num_sms,
-                Plan& P) {
+void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int dy_width,
+                int num_sms, Plan& P) {
   const int n = b->num_seqs, G = ad->num_tasks;
   P.ntasks = G;
   std::vector<int> seg_off{0}, seg_task;
@@ -313,6 +314,23 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     task_unit_off[t + 1] = (int)unit_task.size();
   }
   P.nunits = (int)unit_task.size();
+  // units of the fused dY pass: 512-column items, ~4 equal items per SM
+  std::vector<int> dy_task, dy_s0, dy_s1, dy_off(G + 1, 0);
+  {
+    const int nch = std::max(1, (dy_width + 511) / 512);
+    const double per_dy = std::max(1.0, (double)P.nslots * nch / (4.0 * std::max(num_sms, 1)));
+    for (int t = 0; t < G; ++t) {
+      const int n_t = task_slot_off[t + 1] - task_slot_off[t];
+      const int nu = n_t ? std::max(1, (int)std::lround(n_t / per_dy)) : 0;
+      for (int u = 0; u < nu; ++u) {
+        dy_task.push_back(t);
+        dy_s0.push_back(task_slot_off[t] + (int)((long long)n_t * u / nu));
+        dy_s1.push_back(task_slot_off[t] + (int)((long long)n_t * (u + 1) / nu));
+      }
+      dy_off[t + 1] = (int)dy_task.size();
+    }
+  }
+  P.ndyunits = (int)dy_task.size();
   std::vector<int> roff(G + 1, 0);
   for (int t = 0; t < G; ++t) roff[t + 1] = roff[t] + ad->ranks[t];
   P.rsum = roff[G];
@@ -337,6 +355,10 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   P.o_unit_s0 = put(unit_s0);
   P.o_unit_s1 = put(unit_s1);
   P.o_task_unit_off = put(task_unit_off);
+  P.o_dy_unit_task = put(dy_task);
+  P.o_dy_unit_s0 = put(dy_s0);
+  P.o_dy_unit_s1 = put(dy_s1);
+  P.o_dy_task_unit_off = put(dy_off);
   P.o_ranks = put(std::vector<int>(ad->ranks, ad->ranks + G));
   P.o_roff = put(roff);
   std::vector<int> boff(G + 1, 0);
@@ -373,6 +395,12 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.unit_s0 = d + P.o_unit_s0;
   m.unit_s1 = d + P.o_unit_s1;
   m.task_unit_off = d + P.o_task_unit_off;
+  m.ndyunits = P.ndyunits;
+  m.use_dy_units = 0;
+  m.dy_unit_task = d + P.o_dy_unit_task;
+  m.dy_unit_s0 = d + P.o_dy_unit_s0;
+  m.dy_unit_s1 = d + P.o_dy_unit_s1;
+  m.dy_task_unit_off = d + P.o_dy_task_unit_off;
   m.ranks = d + P.o_ranks;
   m.roff = d + P.o_roff;
   m.boff = d + P.o_boff;
@@ -383,7 +411,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
 // Workspace layout (bytes from ws base); both directions share it.
 struct Layout {
   size_t meta = 0, bpad = 0, bt = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0,
-         total = 0;
+         gpart = 0, total = 0;
   size_t saved = 0;
   int ld8 = 0;   // row stride (elements) of the B operand the kernels read
 };
@@ -412,7 +440,9 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     L.partA = off;
     off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
     L.partB = off;
-    off += align256((size_t)P.nunits * chB * P.qp * 128 * 4);
+    off += align256((size_t)std::max(P.nunits, P.ndyunits) * chB * P.qp * 128 * 4);
+    L.gpart = off;    // fused dY pass: G partials [nslots][ceil(out/512)][128][qp]
+    off += align256((size_t)P.nslots * ((out + 511) / 512) * kTileM * P.qp * 4);
     L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * es;
   } else {
     L.gslots = off;
@@ -454,6 +484,11 @@ lobra_status check_launch(const char* what) {
   return LOBRA_OK;
 }
 
+bool dy_fused() {   // LOBRA_DY_UNFUSED=1: separate G projection + dB reduction (two dY reads)
+  const char* e = getenv("LOBRA_DY_UNFUSED");
+  return !(e && e[0] == '1');
+}
+
 int sms_hint() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -467,7 +502,7 @@ lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobr
                      int width_hint, int num_sms, Plan& P, Layout& L) {
   lobra_status st = validate(prob, b, ad);
   if (st != LOBRA_OK) return st;
-  build_plan(b, ad, width_hint, num_sms, P);
+  build_plan(b, ad, width_hint, (int)prob->out, num_sms, P);
   L = layout(prob, P);
   return LOBRA_OK;
 }
@@ -639,7 +674,22 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mAt, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
-    if (rowproj_uses_ld()) {
+    const bool fused_dy = dy_fused();
+    Meta meta_b = meta;
+    if (fused_dy) {
+      // G_s and the dB partials in ONE read of dY
+      auto* Bt = reinterpret_cast<__nv_bfloat16*>(w + L.bt);
+      {
+        Prof p_(LOBRA_K_PAD, st);
+        launch_transpose_b(static_cast<const __nv_bfloat16*>(ad->B), Bt, out, P.rsum, st);
+      }
+      CUtensorMap mBk;
+      if ((s = make_map(&mBk, Bt, out, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_dypass(mdY, mHs, mBk, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
+                    ctx->num_sms, st);
+      meta_b.use_dy_units = 1;
+    } else if (rowproj_uses_ld()) {
       auto* Bt = reinterpret_cast<__nv_bfloat16*>(w + L.bt);
       {
         Prof p_(LOBRA_K_PAD, st);
@@ -660,8 +710,8 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
                 accumulate_dx, meta, ctx->num_sms, st); }
     if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
     { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st); }
-    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
-    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta, dB, 0, accumulate_dadb, st); }
+    if (!fused_dy && meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta_b, dB, 0, accumulate_dadb, st); }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
   if (prob->tp_kind == LOBRA_TP_COLUMN) {

@@ -33,6 +33,13 @@ struct Meta {
   const int* unit_s0;        // [nunits] range into task_slots
   const int* unit_s1;        // [nunits]
   const int* task_unit_off;  // [ntasks+1]
+  // units of the fused dY pass (512-column items); k_finalize mode 1 uses them when
+  // use_dy_units != 0
+  int ndyunits, use_dy_units;
+  const int* dy_unit_task;
+  const int* dy_unit_s0;
+  const int* dy_unit_s1;
+  const int* dy_task_unit_off;
   const int* ranks;          // [ntasks]
   const int* roff;           // [ntasks+1]
   const int* boff;           // [ntasks+1] task column offset in the B operand the kernels read
@@ -88,6 +95,10 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
 // with stride ld; mode 1: dB [width, rsum] (PEFT layout, row stride rsum).
 void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
                      long long ld, int accumulate, cudaStream_t st);
+// Fused dY pass (G slots + dB partials in one dY read) followed by the G finalize.
+void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
+                   int width, int qp, const Meta& meta, float* gpart, float* bpart,
+                   __nv_bfloat16* gslots, int num_sms, cudaStream_t st);
 // Zero (or leave) the dA/dB of every task when the batch has no tokens.
 void launch_zero_f32(float* p, long long n, cudaStream_t st);
 
