@@ -1044,7 +1044,8 @@ __global__ void __launch_bounds__(256, 1)
 //                                                                (unit, 128-col block)
 // Work item = (dy unit u: consecutive slots of one task, 512-column chunk c).  Per slot and
 // 128-column sub-block b the stage holds the dY tile (2 boxes, K-major for G / MN-major for
-// dB), the H slot (MN-major B for dB) and B^T[qp x 128] (K-major B for G).  TMEM: four dB
+// dB), the H slot (MN-major B for dB) and 2 boxes of the caller's B (64 q x 64 o rows,
+// MN-major B for G: no transpose copy).  TMEM: four dB
 // accumulators (4 x 64 cols) kept across the unit's slots + two G accumulators (2 x 64).
 // k_gfin then sums the G chunk partials in fixed order, scales by s_t, masks and writes
 // the bf16 G slots; the dB partials go through k_finalize (fixed order) as before.
@@ -1052,7 +1053,7 @@ __global__ void __launch_bounds__(256, 1)
 constexpr int Y_STAGES = 3;
 constexpr int Y_Z_BYTES = 2 * 128 * 64 * 2;   // dY tile: 2 boxes of 64 cols x 128 rows
 constexpr int Y_H_BYTES = 128 * 64 * 2;       // H slot
-constexpr int Y_BT_MAX = 2 * 64 * 128;        // B^T: 2 boxes of 64 cols x qp(<=64) rows
+constexpr int Y_BT_MAX = 2 * 64 * 128;        // B: 2 MN-major boxes of 64 q x 64 o rows
 constexpr int Y_STAGE_BYTES = Y_Z_BYTES + Y_H_BYTES + Y_BT_MAX;
 constexpr int Y_SMEM = Y_STAGES * Y_STAGE_BYTES + 1024 + 256;
 
@@ -1077,7 +1078,7 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
   const uint32_t warp = warp_id(), lane = lane_id();
   const Meta& meta = args.meta;
-  const int bt_box = args.qp * 128;      // one 64-col box of B^T rows
+  constexpr int bt_box = 64 * 128;       // one MN-major box of B_cat: 64 q x 64 o rows
 
   if (warp == 0 && lane == 0) tma_prefetch(&mapDY), tma_prefetch(&mapH), tma_prefetch(&mapBt);
   if (warp == 1 && lane == 0) {
@@ -1114,8 +1115,9 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
             tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
             tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], 0, sl * kTileM);
-            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES, &mapBt, &full[stage], col, meta.roff[t]);
-            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES + bt_box, &mapBt, &full[stage], col + 64, meta.roff[t]);
+            // B_t straight from the caller's B (MN-major: q contiguous, rows = o = K)
+            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES, &mapBt, &full[stage], meta.boff[t], col);
+            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES + bt_box, &mapBt, &full[stage], meta.boff[t], col + 64);
             if (++stage == Y_STAGES) stage = 0, phase ^= 1;
           }
         }
@@ -1124,7 +1126,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t id_b = idesc_bf16(128, 64, true, true);          // dB: both MN-major
-      const uint32_t id_g = idesc_bf16(128, args.qp, false, false);   // G: both K-major
+      const uint32_t id_g = idesc_bf16(128, 64, false, true);   // G: A K-major, B MN-major
       int stage = 0;
       uint32_t phase = 0;
       int gcount = 0, it = 0;
@@ -1155,7 +1157,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
                 mma_bf16(dg, sdesc_sw128(z0 + j * 16384 + kk * 32, 16, 1024),
-                         sdesc_sw128(t0 + j * bt_box + kk * 32, 16, 1024), id_g,
+                         sdesc_sw128(t0 + j * bt_box + kk * 2048, 8192, 1024), id_g,
                          (b == 0 && j == 0 && kk == 0) ? 0u : 1u);
             mma_commit(&empty[stage]);
             if (++stage == Y_STAGES) stage = 0, phase ^= 1;

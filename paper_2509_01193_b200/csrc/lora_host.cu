@@ -677,16 +677,10 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     const bool fused_dy = dy_fused();
     Meta meta_b = meta;
     if (fused_dy) {
-      // G_s and the dB partials in ONE read of dY
-      auto* Bt = reinterpret_cast<__nv_bfloat16*>(w + L.bt);
-      {
-        Prof p_(LOBRA_K_PAD, st);
-        launch_transpose_b(static_cast<const __nv_bfloat16*>(ad->B), Bt, out, P.rsum, st);
-      }
-      CUtensorMap mBk;
-      if ((s = make_map(&mBk, Bt, out, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
+      // G_s and the dB partials in ONE read of dY; B read in place
+      // (MN-major operand, box 64 q x 64 o rows: the same map as the two-pass projection)
       Prof p_(LOBRA_K_ROWPROJ, st);
-      launch_dypass(mdY, mHs, mBk, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
+      launch_dypass(mdY, mHs, mBt, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
                     ctx->num_sms, st);
       meta_b.use_dy_units = 1;
     } else if (rowproj_uses_ld()) {
