@@ -49,18 +49,59 @@ def load_peaks():
 
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled every 10 ms
+    from a thread (the GPU found by its PCI bus id, so CUDA_VISIBLE_DEVICES remapping does
+    not matter); `nvidia-smi -lms 100` when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.nvml = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            try:
+                pr = torch.cuda.get_device_properties(gpu_index)
+                bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                h = nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.bits = [(n, getattr(nv, b)) for n, b in zip(self.NAMES, (
+                "nvmlClocksEventReasonHwSlowdown", "nvmlClocksEventReasonHwThermalSlowdown",
+                "nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksEventReasonSwPowerCap"))]
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.nvml, self.h = nv, h
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv, h = self.nvml, self.h
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.mx.append(float(self.max_mhz))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for n, bit in self.bits:
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self.stop_ev.wait(0.01)
 
     def start(self):
+        if self.nvml is not None:
+            self.stop_ev = threading.Event()
+            self.th = threading.Thread(target=self._poll, daemon=True)
+            self.th.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
@@ -76,30 +117,34 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
-        if self.proc is None:
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.th.join(timeout=5)
+            src = "nvml 10 ms"
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
+        else:
+            self.proc.terminate()
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            src = "nvidia-smi 100 ms"
+            for ln in self.lines:
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(self.NAMES, parts[4:8]):
+                    if v.lower() == "active":
+                        self.reasons.add(nm)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": src}
 
 
 # ------------------------------------------------------------------------------ plans
@@ -226,7 +271,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lobra", choices=["lobra", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -342,40 +387,63 @@ def main():
     barrier()
 
     peaks, peak_src = load_peaks()
-    sampler = ClockSampler(local) if rank == 0 or world > 1 else None
-    if sampler and rank == 0:
-        sampler.start()
-    _lib.lobra_profile_enable(not args.no_kernel_events)
-    _lib.lobra_profile_read(reset=True)
-    l0 = _lib.lobra_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tokens = 0
-    tokens_local = 0
-    disp_ms = []
-    barrier()
-    e0.record(stream)
-    for i in range(args.steps):
-        # a7: the dispatch of this step runs on the host while the GPU works on the
-        # previously enqueued step ("fully overlapped")
-        t0 = time.perf_counter()
-        chunks, tok, _ = plan(batches[(args.warmup + i) % n_batches])
-        disp_ms.append(1000 * (time.perf_counter() - t0))
-        run_step(chunks)
-        tokens += tok
-        tokens_local += sum(int(c[0].sum()) for c in chunks)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms_local = e0.elapsed_time(e1)
-    launches = _lib.lobra_launch_count() - l0
-    prof = _lib.lobra_profile_read(reset=True)
-    _lib.lobra_profile_enable(False)
-    clocks = sampler.stop() if (sampler and rank == 0) else None
+
+    def timed():
+        sampler = ClockSampler(local) if rank == 0 else None
+        if sampler:
+            sampler.start()
+        _lib.lobra_profile_enable(not args.no_kernel_events)
+        _lib.lobra_profile_read(reset=True)
+        l0 = _lib.lobra_launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tokens = 0
+        tokens_local = 0
+        disp_ms = []
+        barrier()
+        e0.record(stream)
+        for i in range(args.steps):
+            # a7: the dispatch of this step runs on the host while the GPU works on the
+            # previously enqueued step ("fully overlapped")
+            t0 = time.perf_counter()
+            chunks, tok, _ = plan(batches[(args.warmup + i) % n_batches])
+            disp_ms.append(1000 * (time.perf_counter() - t0))
+            run_step(chunks)
+            tokens += tok
+            tokens_local += sum(int(c[0].sum()) for c in chunks)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_local = e0.elapsed_time(e1)
+        launches = _lib.lobra_launch_count() - l0
+        prof = _lib.lobra_profile_read(reset=True)
+        _lib.lobra_profile_enable(False)
+        clocks = sampler.stop() if sampler else None
+        if world > 1:
+            t = torch.tensor([ms_local], device="cpu" if gloo_test else dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_total = float(t.item())
+        else:
+            ms_total = ms_local
+        return ms_total, ms_local, tokens, tokens_local, disp_ms, launches, prof, clocks
+
+    def rejected(c):
+        """hw/thermal slowdown, or SM clocks well below max with no reason (a clock lock)."""
+        if not c or not c.get("sm_mhz") or not c.get("sm_max_mhz"):
+            return False
+        bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        if bad & set(c["reasons"]):
+            return True
+        return c["sm_mhz"] < 0.85 * c["sm_max_mhz"] and not c["reasons"]
+
+    ms_total, ms_local, tokens, tokens_local, disp_ms, launches, prof, clocks = timed()
+    redo = [1 if (rank == 0 and rejected(clocks)) else 0]
     if world > 1:
-        t = torch.tensor([ms_local], device="cpu" if gloo_test else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    else:
-        ms_total = ms_local
+        t = torch.tensor(redo, device="cpu" if gloo_test else dev)
+        dist.broadcast(t, 0)
+        redo = [int(t.item())]
+    remeasured = None
+    if redo[0]:
+        remeasured = clocks
+        ms_total, ms_local, tokens, tokens_local, disp_ms, launches, prof, clocks = timed()
     ms_step = ms_total / args.steps
     value = tokens / (ms_total / 1000.0)
 
@@ -397,11 +465,13 @@ def main():
     clocks = clocks if clocks is not None else {}
     dom_fl = fl_fwd if dom == "gemm_fwd" else fl_bwd
     dom_ms = prof[dom][1]
-    # the burst figure for a kernel timed in a short region at full clocks; the sustained
-    # (power-capped) figure when the clock record shows the power cap active
+    # Peak: the measured BURST cuBLAS figure, always.  The sustained figure (cuBLAS back to
+    # back for 4 s under the 1000 W cap) is lower than what this GEMM reaches under the same
+    # cap, so it would give frac > 1; it is reported beside as `frac_vs_sustained`.
     capped = bool(clocks and "sw_power_cap" in clocks.get("reasons", []))
-    peak_kind = "bf16_tflops_sustained" if capped and "bf16_tflops_sustained" in peaks else "bf16_tflops"
+    peak_kind = "bf16_tflops"
     peak_t = float(peaks[peak_kind])
+    peak_sus = float(peaks.get("bf16_tflops_sustained", peak_t))
     achieved = dom_fl / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -409,7 +479,8 @@ def main():
         traffic = json.load(open(tf)).get("k_gemm_" + dom.split("_")[1])
     roofline = {"bound": "tensor", "kernel": f"k_gemm ({dom})", "achieved": achieved, "peak": peak_t,
                 "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": traffic,
-                "peak_source": f"{peak_src} {peak_kind}" + (" (sw_power_cap active in the timed region)" if capped else " (short timed region at full clocks)"),
+                "peak_source": f"{peak_src} {peak_kind} (burst)" + ("; sw_power_cap was active in the timed region" if capped else ""),
+                "frac_vs_sustained": achieved / peak_sus,
                 "share_of_step": dom_ms / ms_local if ms_local > 0 else 0.0,
                 "flops_per_launch": dom_fl / max(prof[dom][0], 1),
                 "ms_per_launch": dom_ms / max(prof[dom][0], 1)}
@@ -520,7 +591,7 @@ def main():
                 "frac_of_bf16_peak": {"burst": step_tflops / float(peaks["bf16_tflops"]),
                                       "sustained": step_tflops / float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])),
                 "nominal_2250": step_tflops / 2250.0},
-                "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+                "clocks": clocks, **({"remeasured_after": remeasured} if remeasured else {}), "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
                 "kernels": kern, "dispatch_ms_median": statistics.median(disp_ms) if disp_ms else None,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

@@ -1223,33 +1223,46 @@ __global__ void __launch_bounds__(256, 1)
 
 // G slots from the chunk partials: slot[s][row][q] = s_t * sum_c gpart[s][c][row][q] for
 // rows of the slot's task and q < r_t, zero otherwise; also the all-zero slot nslots.
+// One thread per (slot row, 8 output columns): float4 loads of the chunk partials, summed in
+// chunk order (the order the single-thread form used), scaled, masked, one 16-byte store.
 __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Meta meta,
                        __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_launch_dependents();
-  const int total = (meta.nslots + 1) * kTileM;
+  const int total = (meta.nslots + 1) * kTileM * (kSlotW / 8);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int s = i / kTileM, lrow = i % kTileM;
-    float v[64];
+    const int g = i & 7, r = i >> 3;
+    const int s = r / kTileM, lrow = r % kTileM;
+    float v[8];
 #pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = 0.0f;
+    for (int e = 0; e < 8; ++e) v[e] = 0.0f;
     int rp = 0;
     float sc = 0.0f;
-    if (s < meta.nslots) {
+    if (s < meta.nslots && g * 8 < qp) {
       const int t = meta.slot_task[s];
       const int row = meta.slot_tile[s] * kTileM + lrow;
-      if (row < meta.T && row_task(meta, row) == t) {
-        rp = meta.ranks[t];
+      if (row < meta.T && row_task(meta, row) == t && g * 8 < meta.ranks[t]) {
+        rp = meta.ranks[t] - g * 8;
         sc = meta.scales[t];
+        const float* src = gpart + ((size_t)s * nchunks * kTileM + lrow) * qp + g * 8;
+        const size_t cstride = (size_t)kTileM * qp;
         for (int c = 0; c < nchunks; ++c) {
-          const float* src = gpart + (((size_t)s * nchunks + c) * kTileM + lrow) * qp;
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < rp) v[j] += src[j];
+          const float4 a = __ldg(reinterpret_cast<const float4*>(src + c * cstride));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(src + c * cstride) + 1);
+          v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+          v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
         }
       }
     }
-    store_slot_row(out, s, lrow, v, sc, rp);
+    float w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e] = e < rp ? v[e] * sc : 0.0f;
+    uint4 o;
+    o.x = pack_bf16x2(w[0], w[1]);
+    o.y = pack_bf16x2(w[2], w[3]);
+    o.z = pack_bf16x2(w[4], w[5]);
+    o.w = pack_bf16x2(w[6], w[7]);
+    reinterpret_cast<uint4*>(out + ((size_t)s * kTileM + lrow) * kSlotW)[g] = o;
   }
 }
 

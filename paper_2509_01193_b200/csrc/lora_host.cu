@@ -427,8 +427,8 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     L.ld8 = P.ld8;
     L.bpad = off;
     if (!P.bdirect) off += align256(out * L.ld8 * es);
-    L.bt = off;       // B^T [rsum, out] (K-major operand of the backward projection)
-    off += align256((size_t)P.rsum * out * es);
+    L.bt = off;       // B^T [rsum, out]: only the opt-in LDGSTS projection (LOBRA_RP_LD=1) reads it
+    if (rowproj_uses_ld()) off += align256((size_t)P.rsum * out * es);
     L.gslots = off;   // + one all-zero slot (index nslots)
     off += align256((size_t)(P.nslots + 1) * kTileM * kSlotW * es);
     const int sp = std::max(rowproj_splits(P.ntiles, (int)in), rowproj_splits(P.ntiles, (int)out));
@@ -683,7 +683,7 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
       launch_dypass(mdY, mHs, mBt, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
                     ctx->num_sms, st);
       meta_b.use_dy_units = 1;
-    } else if (rowproj_uses_ld()) {
+    } else if (rowproj_uses_ld()) {   // workspace has L.bt only in this mode
       auto* Bt = reinterpret_cast<__nv_bfloat16*>(w + L.bt);
       {
         Prof p_(LOBRA_K_PAD, st);

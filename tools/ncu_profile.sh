@@ -4,11 +4,11 @@
 # 1) every library launch of one bench step with its device time (cold-cache, serialised)
 # 2) DRAM bytes of all 14 GEMM launches of one step (-> profiles/traffic.json)
 # 3) one `--set full` capture each of the q-projection fwd/bwd GEMM, the rank-r
-#    projection and the token reduction.
+#    projection, the token reduction and the fused backward dY pass.
 set -x
 TAG=${1:-r1}
 OUT=gpurun_out
-K="regex:k_(gemm|gemm2|rowproj|segred|finalize|pad_cols|transpose_b)"
+K="regex:k_(gemm|gemm2|rowproj|segred|finalize|pad_cols|transpose_b|dypass|gfin)"
 B="python bench.py --steps 1 --warmup 1 --profile-only --no-cpu --no-e2e"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
     --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
@@ -23,4 +23,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ro
     -o $OUT/prof_rowproj_$TAG $B > $OUT/ncu_rowproj_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_segred -s 0 -c 1 \
     -o $OUT/prof_segred_$TAG $B > $OUT/ncu_segred_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dypass -s 0 -c 1 \
+    -o $OUT/prof_dypass_$TAG $B > $OUT/ncu_dypass_$TAG.log 2>&1
 ls -la $OUT
