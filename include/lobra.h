@@ -260,6 +260,36 @@ LOBRA_API lobra_status lobra_plan_deployment(const lobra_candidates* cand, int32
                                              int64_t node_cap, lobra_plan_out* out);
 
 /* ------------------------------------------------------------------------------
+ * Configuration proposal from a profiled throughput table (App. A "Configuration
+ * Proposal": "SELECT config, MAX(thruput) FROM thruput_table GROUP BY
+ * num_gpus, seq_len"; Table tb:parallel_config_thruputs).
+ * Reading Q26: a configuration with n_c = tp * pp GPUs per replica competes in
+ * every group (g = gpu_counts[k], seq_len[l]) with n_c <= g and g % n_c == 0, as g / n_c
+ * replicas at its own per-GPU throughput (the table's "-": "the throughput remains the same
+ * after model replication").  The group winner has the maximum throughput; ties go to fewer
+ * GPUs per replica, then smaller TP, then smaller PP, then lower index.  Exact double
+ * comparisons (no tolerance).
+ *   thruput : [C * L] row-major, tokens per GPU per second of one replica of config c at
+ *             seq_len[l]; <= 0 (or NaN) = cannot run that length (out of memory)
+ *   winner  : [K * L] out, config index of each group, -1 when no configuration runs it
+ *   keep    : [C] out, 1 for the proposed configurations (winners of at least one group)
+ * Host only.  Errors: LOBRA_ERR_INPUT (null/empty arrays, tp or pp < 1, gpu_counts < 1).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_configs;         /* C                                                       */
+  const int32_t* tp;           /* [C] TP degree                                           */
+  const int32_t* pp;           /* [C] PP degree (GPUs per replica = tp * pp)              */
+  int32_t num_lens;            /* L                                                       */
+  const int32_t* seq_len;      /* [L] profiled sequence lengths                           */
+  const double* thruput;       /* [C * L]                                                 */
+  int32_t num_gpu_counts;      /* K                                                       */
+  const int32_t* gpu_counts;   /* [K] the table's num_gpus columns                        */
+} lobra_thruput_table;
+
+LOBRA_API lobra_status lobra_propose_configs(const lobra_thruput_table* table, int32_t* winner,
+                                             int32_t* keep);
+
+/* ------------------------------------------------------------------------------
  * Communication (NCCL over NVLink/NVSwitch).  One process per GPU.
  * ------------------------------------------------------------------------------ */
 /* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (e.g. with

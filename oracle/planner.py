@@ -133,3 +133,66 @@ def solve_joint(tp, max_tokens, cost, N, Bj_bounds, grid_step):
         if best is None or k < best:
             best = k
     return best
+
+
+# ------------------------------------------------------------------------------------------
+# Configuration proposal from a profiled throughput table (App. A; Table
+# tb:parallel_config_thruputs).  Reading Q26: a configuration with
+# n_c = tp * pp GPUs per replica competes in every (num_gpus = g, seq_len) group with
+# n_c <= g and n_c | g, as g / n_c replicas at its own per-GPU throughput (the table's "-":
+# "the throughput remains the same after model replication"); the winner of a group is the
+# maximum throughput ("SELECT config, MAX(thruput) ... GROUP BY num_gpus, seq_len"), ties to
+# fewer GPUs per replica, then smaller TP, then smaller PP, then table order.
+# ------------------------------------------------------------------------------------------
+def propose_from_table(tp, pp, seq_lens, thruput, gpu_counts):
+    """Returns (winner[g][l] config index or -1, keep[c] 0/1).  thruput[c][l] <= 0 means the
+    configuration cannot run that length (the table's out-of-memory mark)."""
+    C = len(tp)
+    winner = []
+    for g in gpu_counts:
+        row = []
+        for li in range(len(seq_lens)):
+            best = -1
+            for c in range(C):
+                n = tp[c] * pp[c]
+                if n > g or g % n != 0 or not thruput[c][li] > 0:
+                    continue
+                if best < 0:
+                    best = c
+                    continue
+                kc = (-thruput[c][li], n, tp[c], pp[c], c)
+                kb = (-thruput[best][li], tp[best] * pp[best], tp[best], pp[best], best)
+                if kc < kb:
+                    best = c
+            row.append(best)
+        winner.append(row)
+    keep = [0] * C
+    for row in winner:
+        for c in row:
+            if c >= 0:
+                keep[c] = 1
+    return winner, keep
+
+
+def check_partial_order(tp, pp, seq_lens, thruput, gpu_counts):
+    """Observation 1 on the replication-inclusive table: for every GPU count g,
+    configurations alpha, beta runnable on g GPUs and lengths s < s0 where both run at both:
+    alpha faster at s0 must be faster at s.  Returns the violations (g, alpha, beta, s0, s)."""
+    out = []
+    C = len(tp)
+    L = len(seq_lens)
+    for g in gpu_counts:
+        cfg = [c for c in range(C) if tp[c] * pp[c] <= g and g % (tp[c] * pp[c]) == 0]
+        for a in cfg:
+            for b in cfg:
+                if a == b:
+                    continue
+                for l0 in range(L):
+                    if not (thruput[a][l0] > 0 and thruput[b][l0] > 0):
+                        continue
+                    if not thruput[a][l0] > thruput[b][l0]:
+                        continue
+                    for l in range(l0):
+                        if thruput[a][l] > 0 and thruput[b][l] > 0 and not thruput[a][l] > thruput[b][l]:
+                            out.append((g, a, b, seq_lens[l0], seq_lens[l]))
+    return out

@@ -25,7 +25,7 @@ EXPORTED = [
     "lobra_lora_fwd", "lobra_lora_bwd", "lobra_dispatch", "lobra_nccl_unique_id",
     "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
     "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
-    "lobra_adamw_step", "lobra_plan_deployment",
+    "lobra_adamw_step", "lobra_plan_deployment", "lobra_propose_configs",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim"]
 
@@ -62,6 +62,12 @@ class DispatchOut(C.Structure):
 
 class Candidates(C.Structure):
     _fields_ = [("num_configs", C.c_int32), ("tp", _i32p), ("max_tokens", _i32p), ("cost", _i64p)]
+
+
+class ThruputTable(C.Structure):
+    _fields_ = [("num_configs", C.c_int32), ("tp", _i32p), ("pp", _i32p), ("num_lens", C.c_int32),
+                ("seq_len", _i32p), ("thruput", C.POINTER(C.c_double)), ("num_gpu_counts", C.c_int32),
+                ("gpu_counts", _i32p)]
 
 
 class PlanOut(C.Structure):
@@ -131,6 +137,8 @@ def load() -> C.CDLL:
     lib.lobra_profile_read.restype = C.c_int
     lib.lobra_profile_read.argtypes = [C.POINTER(Profile), C.c_int]
     lib.lobra_launch_count.restype = C.c_int64
+    lib.lobra_propose_configs.restype = C.c_int
+    lib.lobra_propose_configs.argtypes = [C.POINTER(ThruputTable), _i32p, _i32p]
     lib.lobra_plan_deployment.restype = C.c_int
     lib.lobra_plan_deployment.argtypes = [C.POINTER(Candidates), C.c_int32, _i32p, C.c_int32,
                                           C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
@@ -367,3 +375,19 @@ def lobra_plan_deployment(tp, max_tokens, cost, n_gpus, lens, batch_size=0, grid
     return {"status": st, "replicas": reps, "boundaries": bnd[:nb], "demands": dem[:nb],
             "plans_total": o.plans_total, "plans_solved": o.plans_solved, "gpus_used": o.gpus_used,
             "t_hat": int(o.t_hat)}
+
+
+def lobra_propose_configs(tp, pp, seq_lens, thruput, gpu_counts):
+    """Configuration proposal from a throughput table (include/lobra.h).  Returns
+    (winner [K, L] int32 with -1 for empty groups, keep [C] int32)."""
+    tp, pp, sl, gc = _i32(tp), _i32(pp), _i32(seq_lens), _i32(gpu_counts)
+    th = np.ascontiguousarray(np.asarray(thruput, dtype=np.float64).reshape(len(tp), len(sl)))
+    win = np.zeros((len(gc), len(sl)), np.int32)
+    keep = np.zeros(len(tp), np.int32)
+    t = ThruputTable(len(tp), tp.ctypes.data_as(_i32p), pp.ctypes.data_as(_i32p), len(sl),
+                     sl.ctypes.data_as(_i32p), th.ctypes.data_as(C.POINTER(C.c_double)), len(gc),
+                     gc.ctypes.data_as(_i32p))
+    st = load().lobra_propose_configs(C.byref(t), win.ctypes.data_as(_i32p), keep.ctypes.data_as(_i32p))
+    if st != LOBRA_OK:
+        raise LobraError(st, load().lobra_last_error().decode())
+    return win, keep

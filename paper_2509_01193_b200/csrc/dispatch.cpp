@@ -741,3 +741,42 @@ extern "C" lobra_status lobra_plan_deployment(const lobra_candidates* cand, int3
   }
   return LOBRA_OK;
 }
+
+// Configuration proposal (App. A) -- see include/lobra.h and reading Q26.
+extern "C" lobra_status lobra_propose_configs(const lobra_thruput_table* tb, int32_t* winner,
+                                              int32_t* keep) {
+  using lobra::fail;
+  lobra::clear_error();
+  if (!tb || !winner || !keep) return fail(LOBRA_ERR_INPUT, "null argument");
+  const int C = tb->num_configs, L = tb->num_lens, K = tb->num_gpu_counts;
+  if (C < 1 || L < 1 || K < 1 || !tb->tp || !tb->pp || !tb->seq_len || !tb->thruput || !tb->gpu_counts)
+    return fail(LOBRA_ERR_INPUT, "empty throughput table");
+  for (int c = 0; c < C; ++c)
+    if (tb->tp[c] < 1 || tb->pp[c] < 1) return fail(LOBRA_ERR_INPUT, "config %d: tp, pp >= 1", c);
+  for (int k = 0; k < K; ++k)
+    if (tb->gpu_counts[k] < 1) return fail(LOBRA_ERR_INPUT, "gpu_counts[%d] < 1", k);
+  for (int c = 0; c < C; ++c) keep[c] = 0;
+  for (int k = 0; k < K; ++k) {
+    const int g = tb->gpu_counts[k];
+    for (int l = 0; l < L; ++l) {
+      int best = -1;
+      for (int c = 0; c < C; ++c) {
+        const int n = tb->tp[c] * tb->pp[c];
+        const double v = tb->thruput[(size_t)c * L + l];
+        if (n > g || g % n != 0 || !(v > 0.0)) continue;
+        if (best < 0) { best = c; continue; }
+        const double vb = tb->thruput[(size_t)best * L + l];
+        const int nb = tb->tp[best] * tb->pp[best];
+        bool better;
+        if (v != vb) better = v > vb;
+        else if (n != nb) better = n < nb;
+        else if (tb->tp[c] != tb->tp[best]) better = tb->tp[c] < tb->tp[best];
+        else better = tb->pp[c] < tb->pp[best];   // equal keys: the lower index stays
+        if (better) best = c;
+      }
+      winner[(size_t)k * L + l] = best;
+      if (best >= 0) keep[best] = 1;
+    }
+  }
+  return LOBRA_OK;
+}

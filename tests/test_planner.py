@@ -100,3 +100,80 @@ def test_single_candidate():
     got = _lib.lobra_plan_deployment([2], [4096], [[k + 1 for k in range(16)]], 7, [100, 900, 3000],
                                      0, 256, 4096, 4)
     assert got["replicas"].tolist() == [3] and got["gpus_used"] == 6
+
+
+# ---------------------------------------------------------------- configuration proposal
+T3 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_thruputs.json")))
+
+
+def _t3():
+    tp = [c[0] for c in T3["configs"]]
+    pp = [c[1] for c in T3["configs"]]
+    return tp, pp, T3["seq_lens"], T3["thruput"], T3["gpu_counts"]
+
+
+def test_oracle_proposal_selects_the_bold_configs_of_table3():
+    """App. A: the proposal on Table tb:parallel_config_thruputs keeps exactly the bolded
+    configurations, each winning the cell the paper bolds (P:918 5.11, P:960 2.33,
+    P:971 3.79, ...)."""
+    tp, pp, sl, th, gc = _t3()
+    win, keep = PL.propose_from_table(tp, pp, sl, th, gc)
+    kept = sorted(T3["configs"][c] for c in range(len(tp)) if keep[c])
+    assert kept == sorted(T3["expected_bold"])
+    for cell in T3["expected_cells"]:
+        c = win[gc.index(cell["num_gpus"])][sl.index(cell["seq_len"])]
+        assert T3["configs"][c] == cell["config"]
+        assert th[c][sl.index(cell["seq_len"])] == cell["thruput"]
+    # without replication the (2 GPUs, 2K) group would pick <TP=1,PP=2> (4.88, not bold)
+    assert T3["configs"][win[gc.index(2)][sl.index(2048)]] == [1, 1]
+    # no configuration runs 4K on one GPU
+    assert win[gc.index(1)][sl.index(4096)] == -1
+
+
+def test_observation1_holds_on_table3():
+    """the paper's table is consistent with the partial order (Observation 1)."""
+    assert PL.check_partial_order(*_t3()) == []
+    # a planted inversion is reported
+    tp, pp, sl, th, gc = _t3()
+    th = [list(r) for r in th]
+    th[8][0] = 3.0      # <TP=2,PP=4> now slower than <TP=4,PP=1> at 2K but faster at 8K
+    v = PL.check_partial_order(tp, pp, sl, th, gc)
+    assert (8, 8, 3, 8192, 2048) in v
+
+
+def test_proposal_single_config_and_ties():
+    win, keep = PL.propose_from_table([2], [1], [1024], [[1.0]], [2, 4])
+    assert keep == [1] and win == [[0], [0]]
+    # equal throughput: fewer GPUs per replica, then smaller TP, then smaller PP
+    win, keep = PL.propose_from_table([2, 1, 1], [1, 2, 1], [512], [[3.0], [3.0], [3.0]], [2])
+    assert win == [[2]]
+    win, keep = PL.propose_from_table([2, 1], [1, 2], [512], [[3.0], [3.0]], [2])
+    assert win == [[1]]
+
+
+def test_cpp_proposal_equals_oracle():
+    from paper_2509_01193_b200 import _lib
+    tp, pp, sl, th, gc = _t3()
+    win, keep = _lib.lobra_propose_configs(tp, pp, sl, th, gc)
+    ow, ok = PL.propose_from_table(tp, pp, sl, th, gc)
+    assert win.tolist() == ow and keep.tolist() == ok
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        C = int(rng.integers(1, 9))
+        L = int(rng.integers(1, 5))
+        tp = rng.choice([1, 2, 4, 8], C).tolist()
+        pp = rng.choice([1, 2, 4], C).tolist()
+        th = np.round(rng.uniform(-1, 5, (C, L)), 1)     # coarse values force ties; <= 0 = OOM
+        gc = sorted(set(rng.choice([1, 2, 4, 8, 16, 32], int(rng.integers(1, 4))).tolist()))
+        sl = [256 * (i + 1) for i in range(L)]
+        win, keep = _lib.lobra_propose_configs(tp, pp, sl, th, gc)
+        ow, ok = PL.propose_from_table(tp, pp, sl, th.tolist(), gc)
+        assert win.tolist() == ow and keep.tolist() == ok
+
+
+def test_cpp_proposal_errors():
+    from paper_2509_01193_b200 import _lib
+    with pytest.raises(_lib.LobraError):
+        _lib.lobra_propose_configs([0], [1], [512], [[1.0]], [1])
+    with pytest.raises(_lib.LobraError):
+        _lib.lobra_propose_configs([1], [1], [512], [[1.0]], [0])
