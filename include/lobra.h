@@ -168,6 +168,62 @@ LOBRA_API lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_bat
                             size_t ws_bytes, lobra_stream_t stream);
 
 /* ------------------------------------------------------------------------------
+ * Projection groups ("inputs sharing X are done in one pass: {q,k,v}
+ * uses A_cat = [A_q; A_k; A_v] of width 3r; {gate,up} uses width 2r").
+ * num_proj (1..4) projections that read the same X [T, in] and share the task set, the
+ * ranks and the scales (one LoRA configuration per task).  Projection p has
+ * W_p [out_p, in], A_p [sum r, in], B_p [out_p, sum r] in the single-projection layouts
+ * above.  Results equal num_proj lobra_lora_fwd / lobra_lora_bwd calls (backward:
+ * dX (+)= sum_p dX_p, i.e. the single calls with accumulate_dx = 1 after the first), but
+ * X is read ONCE for all the shrinks H_s,p and ONCE for all the dA_p reductions: the
+ * H_s / G_s slots hold one qp-column band per projection (qp = max rank padded to 16;
+ * bands used when num_proj * qp <= 64 and dtype is bf16).  Otherwise the call runs the
+ * num_proj single-projection sequences internally (same results, no X sharing).
+ * TP: all projections of a group have tp_kind; a COLUMN group all-reduces dX once at the
+ * end of the backward; a ROW group all-reduces every Y_p in the forward.
+ * Hs: one buffer of lobra_lora_group_saved_bytes bytes, written by the forward, read by
+ * the backward.  Host arrays (out, A, B, W, Y, dY, dA, dB pointer arrays) are read during
+ * the call only.  Errors as for the single-projection calls (checked for every p).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  lobra_dtype dtype;
+  int64_t in;                  /* shared input width                                      */
+  int32_t num_proj;            /* 1..4                                                    */
+  const int64_t* out;          /* [num_proj] host: out_p (this rank's shard)              */
+  lobra_tp_kind tp_kind;       /* same for every projection of the group                  */
+  lobra_comm tp;
+  int64_t dA_ld;               /* row stride of every dA_p (0 = in)                       */
+} lobra_group_problem;
+
+typedef struct {
+  int32_t num_tasks;
+  const int32_t* ranks;        /* [num_tasks] host, shared by the group                   */
+  const float* scales;         /* [num_tasks] host, shared by the group                   */
+  const void* const* A;        /* [num_proj] host array of device pointers: A_p            */
+  const void* const* B;        /* [num_proj] host array of device pointers: B_p            */
+} lobra_group_adapters;
+
+LOBRA_API size_t lobra_lora_group_workspace_bytes(const lobra_group_problem* prob,
+                                                  const lobra_batch* batch,
+                                                  const lobra_group_adapters* ad);
+LOBRA_API size_t lobra_lora_group_saved_bytes(const lobra_group_problem* prob,
+                                              const lobra_batch* batch,
+                                              const lobra_group_adapters* ad);
+LOBRA_API lobra_status lobra_lora_group_fwd(const lobra_group_problem* prob,
+                                            const lobra_batch* batch,
+                                            const lobra_group_adapters* ad, const void* X,
+                                            const void* const* W, void* const* Y, void* Hs,
+                                            void* ws, size_t ws_bytes, lobra_stream_t stream);
+LOBRA_API lobra_status lobra_lora_group_bwd(const lobra_group_problem* prob,
+                                            const lobra_batch* batch,
+                                            const lobra_group_adapters* ad, const void* X,
+                                            const void* const* W, const void* Hs,
+                                            const void* const* dY, void* dX, int accumulate_dx,
+                                            float* const* dA, float* const* dB,
+                                            int accumulate_dadb, void* ws, size_t ws_bytes,
+                                            lobra_stream_t stream);
+
+/* ------------------------------------------------------------------------------
  * Per-step dispatch (host only, deterministic; every rank may compute it locally).
  * Implements P:591-619 (dynamic bucketing DP over the grid u_k = k*grid_step,
  * k = 1..grid_max/grid_step, empty intervals ignored, lexicographically smallest optimal

@@ -26,6 +26,8 @@ EXPORTED = [
     "lobra_comm_init", "lobra_comm_destroy", "lobra_comm_tp_info", "lobra_adapter_allreduce",
     "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
     "lobra_adamw_step", "lobra_plan_deployment", "lobra_propose_configs",
+    "lobra_lora_group_workspace_bytes", "lobra_lora_group_saved_bytes", "lobra_lora_group_fwd",
+    "lobra_lora_group_bwd",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim"]
 
@@ -46,6 +48,16 @@ class Adapters(C.Structure):
 class Problem(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("in_", C.c_int64), ("out", C.c_int64),
                 ("tp_kind", C.c_int32), ("tp", C.c_void_p), ("dA_ld", C.c_int64)]
+
+
+class GroupProblem(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("in_", C.c_int64), ("num_proj", C.c_int32), ("out", _i64p),
+                ("tp_kind", C.c_int32), ("tp", C.c_void_p), ("dA_ld", C.c_int64)]
+
+
+class GroupAdapters(C.Structure):
+    _fields_ = [("num_tasks", C.c_int32), ("ranks", _i32p), ("scales", _f32p),
+                ("A", C.POINTER(C.c_void_p)), ("B", C.POINTER(C.c_void_p))]
 
 
 class Deployment(C.Structure):
@@ -117,6 +129,19 @@ def load() -> C.CDLL:
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                    C.c_size_t, C.c_void_p]
+    _gp, _gb, _ga = C.POINTER(GroupProblem), C.POINTER(Batch), C.POINTER(GroupAdapters)
+    _vpp = C.POINTER(C.c_void_p)
+    lib.lobra_lora_group_workspace_bytes.restype = C.c_size_t
+    lib.lobra_lora_group_workspace_bytes.argtypes = [_gp, _gb, _ga]
+    lib.lobra_lora_group_saved_bytes.restype = C.c_size_t
+    lib.lobra_lora_group_saved_bytes.argtypes = [_gp, _gb, _ga]
+    lib.lobra_lora_group_fwd.restype = C.c_int
+    lib.lobra_lora_group_fwd.argtypes = [_gp, _gb, _ga, C.c_void_p, _vpp, _vpp, C.c_void_p,
+                                         C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.lobra_lora_group_bwd.restype = C.c_int
+    lib.lobra_lora_group_bwd.argtypes = [_gp, _gb, _ga, C.c_void_p, _vpp, C.c_void_p, _vpp,
+                                         C.c_void_p, C.c_int, _vpp, _vpp, C.c_int, C.c_void_p,
+                                         C.c_size_t, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
     lib.lobra_dispatch.argtypes = [C.POINTER(Deployment), C.POINTER(Batch), C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int32, C.c_int32, C.c_int64,
@@ -198,6 +223,77 @@ class _Args:
                            self.scales.ctypes.data_as(_f32p), _ptr(A) or 1, _ptr(B) or 1)
         self.prob = Problem(dtype, d_in, d_out, tp_kind, comm.handle if comm is not None else None,
                             dA_ld)
+
+
+def _vp(ptrs):
+    arr = (C.c_void_p * len(ptrs))(*[_ptr(p) or None for p in ptrs])
+    return arr
+
+
+class _GroupArgs:
+    """Projection-group structs (include/lobra.h); keeps every array alive."""
+
+    def __init__(self, dtype, d_in, outs, seq_lens, seq_task, ranks, scales, A=None, B=None,
+                 tp_kind=LOBRA_TP_NONE, comm=None, dA_ld=0):
+        n = len(outs)
+        self.lens = _i32(seq_lens)
+        self.tasks = _i32(seq_task)
+        self.ranks = _i32(ranks)
+        self.scales = np.ascontiguousarray(np.asarray(scales, dtype=np.float32))
+        self.outs = np.ascontiguousarray(np.asarray(outs, dtype=np.int64))
+        self.batch = Batch(len(self.lens), self.lens.ctypes.data_as(_i32p),
+                           self.tasks.ctypes.data_as(_i32p))
+        self.A = _vp(A if A is not None else [1] * n)
+        self.B = _vp(B if B is not None else [1] * n)
+        self.ad = GroupAdapters(len(self.ranks), self.ranks.ctypes.data_as(_i32p),
+                                self.scales.ctypes.data_as(_f32p), self.A, self.B)
+        self.prob = GroupProblem(dtype, d_in, n, self.outs.ctypes.data_as(_i64p), tp_kind,
+                                 comm.handle if comm is not None else None, dA_ld)
+
+
+def lobra_lora_group_workspace_bytes(dtype: int, d_in: int, outs, seq_lens, seq_task, ranks,
+                                     scales) -> int:
+    a = _GroupArgs(dtype, d_in, outs, seq_lens, seq_task, ranks, scales)
+    n = load().lobra_lora_group_workspace_bytes(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad))
+    if n == 0:
+        raise LobraError(LOBRA_ERR_INPUT, load().lobra_last_error().decode())
+    return int(n)
+
+
+def lobra_lora_group_saved_bytes(dtype: int, d_in: int, outs, seq_lens, seq_task, ranks,
+                                 scales) -> int:
+    a = _GroupArgs(dtype, d_in, outs, seq_lens, seq_task, ranks, scales)
+    n = load().lobra_lora_group_saved_bytes(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad))
+    if n == 0:
+        raise LobraError(LOBRA_ERR_INPUT, load().lobra_last_error().decode())
+    return int(n)
+
+
+def lobra_lora_group_fwd(X, Ws, As, Bs, ranks, scales, seq_lens, seq_task, Ys, Hs, ws,
+                         ws_bytes=None, tp_kind=LOBRA_TP_NONE, comm=None, stream=None, dtype=None):
+    """Projection group sharing X (include/lobra.h): Y_p = X W_p^T + s_t (X A_p,t^T) B_p,t^T."""
+    dt = dtype_code(X.dtype) if dtype is None else dtype
+    outs = [int(W.shape[0]) for W in Ws]
+    a = _GroupArgs(dt, int(X.shape[1]), outs, seq_lens, seq_task, ranks, scales, As, Bs, tp_kind, comm)
+    W, Y = _vp(Ws), _vp(Ys)
+    nb = ws.numel() * ws.element_size() if ws_bytes is None else ws_bytes
+    _check(load().lobra_lora_group_fwd(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad), _ptr(X), W, Y,
+                                       _ptr(Hs), _ptr(ws), nb, _stream(stream)))
+
+
+def lobra_lora_group_bwd(X, Ws, As, Bs, ranks, scales, seq_lens, seq_task, Hs, dYs, dX, dAs, dBs, ws,
+                         accumulate_dx=False, accumulate_dadb=False, ws_bytes=None, dA_ld=0,
+                         tp_kind=LOBRA_TP_NONE, comm=None, stream=None, dtype=None):
+    """dX (+)= sum_p [dY_p W_p + s_t (dY_p B_p,t) A_p,t]; dA_p, dB_p (+)= token sums."""
+    dt = dtype_code(X.dtype) if dtype is None else dtype
+    outs = [int(W.shape[0]) for W in Ws]
+    a = _GroupArgs(dt, int(X.shape[1]), outs, seq_lens, seq_task, ranks, scales, As, Bs, tp_kind, comm,
+                   dA_ld)
+    W, dY, dA, dB = _vp(Ws), _vp(dYs), _vp(dAs), _vp(dBs)
+    nb = ws.numel() * ws.element_size() if ws_bytes is None else ws_bytes
+    _check(load().lobra_lora_group_bwd(C.byref(a.prob), C.byref(a.batch), C.byref(a.ad), _ptr(X), W,
+                                       _ptr(Hs), dY, _ptr(dX), int(bool(accumulate_dx)), dA, dB,
+                                       int(bool(accumulate_dadb)), _ptr(ws), nb, _stream(stream)))
 
 
 def dtype_code(torch_dtype) -> int:

@@ -13,6 +13,7 @@
 // See DESIGN.md "Kernels" for layouts and the roofline of each.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           for (int k = 0; k < nk16; ++k) {
             const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
                                      : sdesc_sw128(b0 + k * 32, 16, 1024);
-            mma_bf16(d, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id_main, 1u);
+            mma_bf16(d, sdesc_sw128(a0 + (meta.band / 16 + k) * 32, 16, 1024), bd, id_main, 1u);
           }
           mma_commit(&empty[stage]);
           if (++stage == G_STAGES) stage = 0, phase ^= 1;
@@ -397,7 +398,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           for (int k = 0; k < nk16; ++k) {
             const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
                                      : sdesc_sw128(b0 + k * 32, 16, 1024);
-            mma_bf16_pair(d, sdesc_sw128(a0 + k * 32, 16, 1024), bd, id, 1u);
+            // the slot's columns [band, band + 16 nk16) hold this projection's H_s / G_s
+            mma_bf16_pair(d, sdesc_sw128(a0 + (meta.band / 16 + k) * 32, 16, 1024), bd, id, 1u);
           }
           mma_commit_pair(&empty[stage], 0x3);
           if (++stage == P_STAGES) stage = 0, phase ^= 1;
@@ -1204,7 +1206,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int h = 0; h < 2; ++h) {
           if (h * 32 >= rp) break;
           float v[32];
-          tmem_ld32(tmem + ((q * 32u) << 16) + b * 64 + h * 32, v);
+          tmem_ld32(tmem + ((q * 32u) << 16) + b * 64 + meta.band + h * 32, v);   // dB vs H band
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (h * 32 + j < rp) dst[(size_t)(h * 32 + j) * 128] = v[j];
@@ -1223,22 +1225,24 @@ __global__ void __launch_bounds__(256, 1)
 
 // G slots from the chunk partials: slot[s][row][q] = s_t * sum_c gpart[s][c][row][q] for
 // rows of the slot's task and q < r_t, zero otherwise; also the all-zero slot nslots.
-// One thread per (slot row, 8 output columns): float4 loads of the chunk partials, summed in
-// chunk order (the order the single-thread form used), scaled, masked, one 16-byte store.
+// One thread per (slot row, 8 output columns of this projection's band): float4 loads of the
+// chunk partials, summed in chunk order, scaled, masked, one 16-byte store at column
+// band + 8 g (a projection group's other bands are left untouched).
 __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Meta meta,
                        __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_launch_dependents();
-  const int total = (meta.nslots + 1) * kTileM * (kSlotW / 8);
+  const int ng = qp / 8;
+  const int total = (meta.nslots + 1) * kTileM * ng;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int g = i & 7, r = i >> 3;
+    const int g = i % ng, r = i / ng;
     const int s = r / kTileM, lrow = r % kTileM;
     float v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) v[e] = 0.0f;
     int rp = 0;
     float sc = 0.0f;
-    if (s < meta.nslots && g * 8 < qp) {
+    if (s < meta.nslots) {
       const int t = meta.slot_task[s];
       const int row = meta.slot_tile[s] * kTileM + lrow;
       if (row < meta.T && row_task(meta, row) == t && g * 8 < meta.ranks[t]) {
@@ -1262,7 +1266,30 @@ __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Met
     o.y = pack_bf16x2(w[2], w[3]);
     o.z = pack_bf16x2(w[4], w[5]);
     o.w = pack_bf16x2(w[6], w[7]);
-    reinterpret_cast<uint4*>(out + ((size_t)s * kTileM + lrow) * kSlotW)[g] = o;
+    reinterpret_cast<uint4*>(out + ((size_t)s * kTileM + lrow) * kSlotW + meta.band)[g] = o;
+  }
+}
+
+// Projection group: A_grp[(t * np + p) * qp + j, :] = A_p[roff[t] + j, :] for j < r_t, zero
+// rows for r_t <= j < qp (the band layout of the shared H/G slots).
+struct GroupA {
+  const __nv_bfloat16* A[4];
+};
+__global__ void k_pack_a_group(GroupA src, int np, int qp, int in, Meta meta,
+                               __nv_bfloat16* __restrict__ dst) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int vpr = in / 8;   // uint4 per row
+  const long long total = (long long)meta.ntasks * np * qp * vpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % vpr);
+    const long long row = i / vpr;
+    const int j = (int)(row % qp), p = (int)((row / qp) % np), t = (int)(row / ((long long)qp * np));
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (j < meta.ranks[t])
+      val = __ldg(reinterpret_cast<const uint4*>(src.A[p] + (size_t)(meta.roff[t] + j) * in) + v);
+    reinterpret_cast<uint4*>(dst + (size_t)row * in)[v] = val;
   }
 }
 
@@ -1299,7 +1326,8 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
     const int c = col >> 7, ci = col & 127;
     float s = 0.0f;
-    for (int u = u0; u < u1; ++u) s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + q) * 128 + ci);
+    for (int u = u0; u < u1; ++u)
+      s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + meta.band + q) * 128 + ci);
     float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
     *dst = accumulate ? *dst + s : s;
   }
@@ -1438,6 +1466,15 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
     case 10: launch_rp<false, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
     default: launch_rp<true, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
   }
+}
+
+void launch_pack_a_group(const __nv_bfloat16* const* A, int np, int qp, int in, const Meta& meta,
+                         __nv_bfloat16* dst, cudaStream_t st) {
+  GroupA g{};
+  for (int p = 0; p < np && p < 4; ++p) g.A[p] = A[p];
+  const long long total = (long long)meta.ntasks * np * qp * (in / 8);
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  launch_k(k_pack_a_group, dim3(std::max(blocks, 1)), dim3(256), 0, st, g, np, qp, in, meta, dst);
 }
 
 void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int rsum, cudaStream_t st) {

@@ -216,7 +216,8 @@ struct Plan {
   int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
       o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_boff,
       o_dy_unit_task, o_dy_unit_s0, o_dy_unit_s1, o_dy_task_unit_off,
-      o_scales;
+      o_scales, o_ranks_g, o_roff_g;
+  int np = 1;       // projections sharing the slots (projection group)
   int ld8 = 0;      // row stride of the B operand the kernels read (rsum if direct)
   bool bdirect = true;
   int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16, ndyunits = 0;
@@ -258,9 +259,10 @@ lobra_status validate(const lobra_problem* prob, const lobra_batch* b, const lob
 }
 
 void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int dy_width,
-                int num_sms, Plan& P) {
+                int num_sms, Plan& P, int np = 1) {
   const int n = b->num_seqs, G = ad->num_tasks;
   P.ntasks = G;
+  P.np = np;
   std::vector<int> seg_off{0}, seg_task;
   int T = 0;
   for (int k = 0; k < n; ++k) {
@@ -370,6 +372,11 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   std::vector<int> sc(G);
   std::memcpy(sc.data(), ad->scales, sizeof(float) * G);
   P.o_scales = put(sc);
+  // projection group: the packed A_grp holds np bands of qp rows per task
+  std::vector<int> rg(G, np * P.qp), rog(G + 1, 0);
+  for (int t = 0; t < G; ++t) rog[t + 1] = rog[t] + np * P.qp;
+  P.o_ranks_g = put(rg);
+  P.o_roff_g = put(rog);
 }
 
 Meta device_meta(const Plan& P, const void* dev_base) {
@@ -405,6 +412,19 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.roff = d + P.o_roff;
   m.boff = d + P.o_boff;
   m.scales = reinterpret_cast<const float*>(d + P.o_scales);
+  m.band = 0;
+  return m;
+}
+
+// The shrink / dA view of a projection group: every task has np * qp "rows" (the bands) at
+// roff_g in the packed A_grp, partial stride np * qp.
+Meta group_meta(const Plan& P, const void* dev_base) {
+  Meta m = device_meta(P, dev_base);
+  const int32_t* d = reinterpret_cast<const int32_t*>(dev_base);
+  m.ranks = d + P.o_ranks_g;
+  m.roff = d + P.o_roff_g;
+  m.rsum = P.ntasks * P.np * P.qp;
+  m.qp = P.np * P.qp;
   return m;
 }
 
@@ -713,6 +733,319 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     return prob->dtype == LOBRA_BF16 ? comm_tp_allreduce_bf16(prob->tp, dX, cnt, st)
                                      : comm_tp_allreduce_f32(prob->tp, static_cast<float*>(dX), cnt, st);
   }
+  return LOBRA_OK;
+}
+
+// ======================================================================================
+// Projection groups (include/lobra.h): projections sharing X read it once for the shrink
+// and once for the dA reduction; H_s / G_s slots hold one qp-wide band per projection.
+// ======================================================================================
+namespace lobra {
+namespace {
+
+lobra_status validate_group(const lobra_group_problem* g, const lobra_batch* b,
+                            const lobra_group_adapters* ga) {
+  if (!g || !b || !ga) return fail(LOBRA_ERR_INPUT, "null problem/batch/adapters");
+  if (g->num_proj < 1 || g->num_proj > 4 || !g->out)
+    return fail(LOBRA_ERR_INPUT, "num_proj must be 1..4 with an out[] array");
+  if (!ga->A || !ga->B) return fail(LOBRA_ERR_INPUT, "A[] / B[] pointer arrays missing");
+  for (int p = 0; p < g->num_proj; ++p) {
+    lobra_problem sp{g->dtype, g->in, g->out[p], g->tp_kind, g->tp, g->dA_ld};
+    lobra_adapters sa{ga->num_tasks, ga->ranks, ga->scales, ga->A[p], ga->B[p]};
+    lobra_status s = validate(&sp, b, &sa);
+    if (s != LOBRA_OK) return s;
+  }
+  return LOBRA_OK;
+}
+
+lobra_problem single_problem(const lobra_group_problem* g, int p, lobra_tp_kind kind) {
+  return lobra_problem{g->dtype, g->in, g->out[p], kind, g->tp, g->dA_ld};
+}
+lobra_adapters single_adapters(const lobra_group_adapters* ga, int p) {
+  return lobra_adapters{ga->num_tasks, ga->ranks, ga->scales, ga->A[p], ga->B[p]};
+}
+
+int64_t max_out(const lobra_group_problem* g) {
+  int64_t m = 0;
+  for (int p = 0; p < g->num_proj; ++p) m = std::max<int64_t>(m, g->out[p]);
+  return m;
+}
+int64_t min_out(const lobra_group_problem* g) {
+  int64_t m = g->out[0];
+  for (int p = 0; p < g->num_proj; ++p) m = std::min<int64_t>(m, g->out[p]);
+  return m;
+}
+
+// Banded path applies: bf16, the bands fit the 64-wide slot, default backward kernels.
+bool group_fused(const lobra_group_problem* g, const lobra_group_adapters* ga) {
+  if (g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld() || !gemm_uses_pair()) return false;
+  int qp = 16;
+  for (int t = 0; t < ga->num_tasks; ++t) qp = std::max(qp, (ga->ranks[t] + 15) & ~15);
+  return g->num_proj * qp <= kSlotW;
+}
+
+struct GroupLayout {
+  size_t meta = 0, bpad = 0, agrp = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0,
+         gpart = 0, total = 0, saved = 0;
+};
+
+GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
+  GroupLayout L;
+  const size_t in = g->in, omax = max_out(g), qg = (size_t)P.np * P.qp;
+  size_t off = 0;
+  L.meta = off;
+  off += align256(P.buf.size() * 4);
+  L.bpad = off;
+  if (!P.bdirect) off += align256(omax * P.ld8 * 2);
+  L.agrp = off;
+  off += align256((size_t)P.ntasks * qg * in * 2);
+  L.gslots = off;
+  off += align256((size_t)(P.nslots + 1) * kTileM * kSlotW * 2);
+  const int sp = rowproj_splits(P.ntiles, (int)in);
+  L.rpart = off;
+  if (sp > 1) off += align256((size_t)sp * P.nslots * kTileM * 64 * 4);
+  L.counters = off;
+  off += align256((size_t)P.ntiles * 4);
+  L.partA = off;
+  off += align256((size_t)P.nunits * ((in + 127) / 128) * qg * 128 * 4);
+  L.partB = off;
+  off += align256((size_t)P.ndyunits * ((omax + 127) / 128) * P.qp * 128 * 4);
+  L.gpart = off;
+  off += align256((size_t)P.nslots * ((omax + 511) / 512) * kTileM * P.qp * 4);
+  L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * 2;
+  L.total = off;
+  return L;
+}
+
+void group_plan(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga,
+                int num_sms, Plan& P) {
+  lobra_adapters a0 = single_adapters(ga, 0);
+  build_plan(b, &a0, (int)std::min<int64_t>(g->in, min_out(g)), (int)max_out(g), num_sms, P, g->num_proj);
+}
+
+// workspace / saved sizes of the fallback (per-projection sequences)
+size_t fallback_ws(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga) {
+  size_t m = 0;
+  for (int p = 0; p < g->num_proj; ++p) {
+    lobra_problem sp = single_problem(g, p, g->tp_kind);
+    lobra_adapters sa = single_adapters(ga, p);
+    m = std::max(m, lobra_lora_workspace_bytes(&sp, b, &sa));
+  }
+  return m;
+}
+size_t fallback_saved_each(const lobra_group_problem* g, const lobra_batch* b,
+                           const lobra_group_adapters* ga) {
+  size_t m = 0;
+  for (int p = 0; p < g->num_proj; ++p) {
+    lobra_problem sp = single_problem(g, p, g->tp_kind);
+    lobra_adapters sa = single_adapters(ga, p);
+    m = std::max(m, lobra_lora_saved_bytes(&sp, b, &sa));
+  }
+  return (m + 255) & ~size_t(255);
+}
+
+}  // namespace
+}  // namespace lobra
+
+extern "C" size_t lobra_lora_group_workspace_bytes(const lobra_group_problem* g, const lobra_batch* b,
+                                                   const lobra_group_adapters* ga) {
+  clear_error();
+  if (validate_group(g, b, ga) != LOBRA_OK) return 0;
+  if (!group_fused(g, ga)) return fallback_ws(g, b, ga);
+  Plan P;
+  group_plan(g, b, ga, sms_hint(), P);
+  return group_layout(g, P).total;
+}
+
+extern "C" size_t lobra_lora_group_saved_bytes(const lobra_group_problem* g, const lobra_batch* b,
+                                               const lobra_group_adapters* ga) {
+  clear_error();
+  if (validate_group(g, b, ga) != LOBRA_OK) return 0;
+  if (!group_fused(g, ga)) return fallback_saved_each(g, b, ga) * g->num_proj;
+  Plan P;
+  group_plan(g, b, ga, 1 << 20, P);
+  return std::max<size_t>(group_layout(g, P).saved, 256);
+}
+
+extern "C" lobra_status lobra_lora_group_fwd(const lobra_group_problem* g, const lobra_batch* batch,
+                                             const lobra_group_adapters* ga, const void* X,
+                                             const void* const* W, void* const* Y, void* Hs, void* ws,
+                                             size_t ws_bytes, lobra_stream_t stream_) {
+  clear_error();
+  lobra_status s = validate_group(g, batch, ga);
+  if (s != LOBRA_OK) return s;
+  if (!W || !Y) return fail(LOBRA_ERR_INPUT, "W[] / Y[] pointer arrays missing");
+  const int np = g->num_proj;
+  if (!group_fused(g, ga)) {
+    // fallback: np single-projection forwards, each with its own band of Hs
+    const size_t each = fallback_saved_each(g, batch, ga);
+    for (int p = 0; p < np; ++p) {
+      lobra_problem sp = single_problem(g, p, g->tp_kind);
+      lobra_adapters sa = single_adapters(ga, p);
+      if ((s = lobra_lora_fwd(&sp, batch, &sa, X, W[p], Y[p], static_cast<uint8_t*>(Hs) + p * each, ws,
+                              ws_bytes, stream_)) != LOBRA_OK)
+        return s;
+    }
+    return LOBRA_OK;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  DevCtx* ctx = nullptr;
+  if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
+  Plan P;
+  group_plan(g, batch, ga, sms_hint(), P);
+  const GroupLayout L = group_layout(g, P);
+  if (!X || !Hs || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");
+  if (ws_bytes < L.total) return fail(LOBRA_ERR_INPUT, "workspace too small: %zu < %zu", ws_bytes, L.total);
+  bool al = (reinterpret_cast<uintptr_t>(ws) & 255) == 0 && aligned16(X) && aligned16(Hs);
+  for (int p = 0; p < np; ++p)
+    al = al && W[p] && Y[p] && aligned16(W[p]) && aligned16(Y[p]) && aligned16(ga->A[p]) && aligned16(ga->B[p]);
+  if (!al) return fail(LOBRA_ERR_INPUT, "device pointers must be non-null and 16-byte aligned (ws 256-byte)");
+  if (g->tp_kind == LOBRA_TP_ROW && g->tp == nullptr)
+    return fail(LOBRA_ERR_INPUT, "row-parallel problem without a comm");
+  if (P.T == 0) return LOBRA_OK;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  if ((s = upload_meta(ctx, P.buf, w + L.meta, st)) != LOBRA_OK) return s;
+  const Meta meta = device_meta(P, w + L.meta);
+  const Meta meta_g = group_meta(P, w + L.meta);
+  const int in = (int)g->in;
+  auto* Ag = reinterpret_cast<__nv_bfloat16*>(w + L.agrp);
+  {
+    const __nv_bfloat16* As[4];
+    for (int p = 0; p < np; ++p) As[p] = static_cast<const __nv_bfloat16*>(ga->A[p]);
+    Prof p_(LOBRA_K_PAD, st);
+    launch_pack_a_group(As, np, P.qp, in, meta, Ag, st);
+  }
+  CUtensorMap mX, mAg, mSlot;
+  if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_map(&mAg, Ag, in, (uint64_t)P.ntasks * np * P.qp, 64, 64)) != LOBRA_OK) return s;
+  if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
+  {
+    // a1: every projection's H_s from ONE pass over X (band p = columns [p qp, (p+1) qp))
+    Prof p_(LOBRA_K_ROWPROJ, st);
+    launch_rowproj(false, mX, mAg, in, meta_g, static_cast<__nv_bfloat16*>(Hs),
+                   reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);
+  }
+  for (int p = 0; p < np; ++p) {
+    const int out = (int)g->out[p];
+    const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ga->B[p]);
+    if (!P.bdirect) {
+      auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.ld8, meta, st); }
+      Bop = Bp;
+    }
+    CUtensorMap mW, mB;
+    if ((s = make_map(&mW, W[p], in, out, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mB, Bop, P.ld8, out, 64, 128)) != LOBRA_OK) return s;
+    Meta mp = meta;
+    mp.band = p * P.qp;
+    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in, static_cast<__nv_bfloat16*>(Y[p]),
+                                                   0, mp, ctx->num_sms, st); }
+    if ((s = check_launch("lobra_lora_group_fwd")) != LOBRA_OK) return s;
+    if (g->tp_kind == LOBRA_TP_ROW)
+      if ((s = comm_tp_allreduce_bf16(g->tp, Y[p], (size_t)P.T * out, st)) != LOBRA_OK) return s;
+  }
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const lobra_batch* batch,
+                                             const lobra_group_adapters* ga, const void* X,
+                                             const void* const* W, const void* Hs,
+                                             const void* const* dY, void* dX, int accumulate_dx,
+                                             float* const* dA, float* const* dB, int accumulate_dadb,
+                                             void* ws, size_t ws_bytes, lobra_stream_t stream_) {
+  clear_error();
+  lobra_status s = validate_group(g, batch, ga);
+  if (s != LOBRA_OK) return s;
+  if (!W || !dY || !dA || !dB) return fail(LOBRA_ERR_INPUT, "W[] / dY[] / dA[] / dB[] pointer arrays missing");
+  const int np = g->num_proj;
+  if (!group_fused(g, ga)) {
+    const size_t each = fallback_saved_each(g, batch, ga);
+    for (int p = 0; p < np; ++p) {
+      // dX accumulates across the group; a column-parallel group all-reduces once, last
+      lobra_problem sp = single_problem(g, p, p == np - 1 || g->tp_kind != LOBRA_TP_COLUMN
+                                                  ? g->tp_kind : LOBRA_TP_NONE);
+      lobra_adapters sa = single_adapters(ga, p);
+      if ((s = lobra_lora_bwd(&sp, batch, &sa, X, W[p], static_cast<const uint8_t*>(Hs) + p * each, dY[p], dX,
+                              p > 0 ? 1 : accumulate_dx, dA[p], dB[p], accumulate_dadb, ws, ws_bytes,
+                              stream_)) != LOBRA_OK)
+        return s;
+    }
+    return LOBRA_OK;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  DevCtx* ctx = nullptr;
+  if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
+  Plan P;
+  group_plan(g, batch, ga, ctx->num_sms, P);
+  const GroupLayout L = group_layout(g, P);
+  if (!X || !Hs || !dX || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");
+  if (ws_bytes < L.total) return fail(LOBRA_ERR_INPUT, "workspace too small: %zu < %zu", ws_bytes, L.total);
+  bool al = (reinterpret_cast<uintptr_t>(ws) & 255) == 0 && aligned16(X) && aligned16(Hs) && aligned16(dX);
+  for (int p = 0; p < np; ++p)
+    al = al && W[p] && dY[p] && dA[p] && dB[p] && aligned16(W[p]) && aligned16(dY[p]) && aligned16(dA[p]) &&
+         aligned16(dB[p]) && aligned16(ga->A[p]) && aligned16(ga->B[p]);
+  if (!al) return fail(LOBRA_ERR_INPUT, "device pointers must be non-null and 16-byte aligned (ws 256-byte)");
+  if (g->tp_kind == LOBRA_TP_COLUMN && g->tp == nullptr)
+    return fail(LOBRA_ERR_INPUT, "column-parallel problem without a comm");
+  const int in = (int)g->in;
+  const long long ldA = g->dA_ld ? g->dA_ld : g->in;
+  if (P.T == 0) {
+    if (!accumulate_dadb)
+      for (int p = 0; p < np; ++p) {
+        for (int r = 0; r < P.rsum; ++r) cudaMemsetAsync(dA[p] + (size_t)r * ldA, 0, sizeof(float) * in, st);
+        cudaMemsetAsync(dB[p], 0, sizeof(float) * (size_t)g->out[p] * P.rsum, st);
+      }
+    return check_launch("lobra_lora_group_bwd(empty)");
+  }
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  if ((s = upload_meta(ctx, P.buf, w + L.meta, st)) != LOBRA_OK) return s;
+  const Meta meta = device_meta(P, w + L.meta);
+  const Meta meta_g = group_meta(P, w + L.meta);
+  auto* Gs = reinterpret_cast<__nv_bfloat16*>(w + L.gslots);
+  float* partA = reinterpret_cast<float*>(w + L.partA);
+  float* partB = reinterpret_cast<float*>(w + L.partB);
+  CUtensorMap mX, mG, mHs;
+  if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_map(&mG, Gs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
+  for (int p = 0; p < np; ++p) {
+    const int out = (int)g->out[p];
+    const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ga->B[p]);
+    if (!P.bdirect) {
+      auto* Bp = reinterpret_cast<__nv_bfloat16*>(w + L.bpad);
+      { Prof p_(LOBRA_K_PAD, st); launch_pad_cols(Bop, Bp, out, P.ld8, meta, st); }
+      Bop = Bp;
+    }
+    CUtensorMap mdY, mBt, mWmn, mAt;
+    if ((s = make_map(&mdY, dY[p], out, P.T, 64, 128)) != LOBRA_OK) return s;
+    if ((s = make_map(&mBt, Bop, P.ld8, out, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mWmn, W[p], in, out, 64, 64)) != LOBRA_OK) return s;
+    if ((s = make_map(&mAt, ga->A[p], in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
+    Meta mp = meta;
+    mp.band = p * P.qp;
+    {
+      // a3 for projection p: G_s into band p, dB partials against band p of H_s
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
+                    ctx->num_sms, st);
+    }
+    { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
+                                                   p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st); }
+    Meta mb = meta;
+    mb.use_dy_units = 1;
+    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, mb, dB[p], 0, accumulate_dadb, st); }
+  }
+  // a5 for the whole group: ONE pass over X against all bands of G_s
+  if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta_g, partA, ctx->num_sms, st); }
+  for (int p = 0; p < np; ++p) {
+    Meta ma = meta;
+    ma.qp = np * P.qp;
+    ma.band = p * P.qp;
+    Prof p_(LOBRA_K_FINALIZE, st);
+    launch_finalize(0, partA, in, ma, dA[p], ldA, accumulate_dadb, st);
+  }
+  if ((s = check_launch("lobra_lora_group_bwd")) != LOBRA_OK) return s;
+  if (g->tp_kind == LOBRA_TP_COLUMN) return comm_tp_allreduce_bf16(g->tp, dX, (size_t)P.T * in, st);
   return LOBRA_OK;
 }
 

@@ -22,6 +22,8 @@ constexpr int kSlotW = 64;      // slot width: ranks padded to 64 columns (r_t <
 struct Meta {
   int T, nseg, ntiles, nslots, ntasks, nunits, rsum, max_slots_per_tile;
   int qp;                    // max over tasks of rank padded to 16 (partials' q stride)
+  int band;                  // projection group: this projection's first column in the 64-wide
+                             // H/G slots (0 for a single projection); multiple of 16
   const int* seg_off;        // [nseg+1]
   const int* seg_task;       // [nseg]
   const int* tile_slot_off;  // [ntiles+1]
@@ -76,6 +78,10 @@ bool rowproj_uses_ld();
 void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, int qp,
                        const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
                        cudaStream_t st);
+// Projection group (np <= 4 projections sharing X and the task ranks): A_grp rows
+// (t * np + p) * qp + j = A_p[roff[t] + j] for j < r_t, zero otherwise.
+void launch_pack_a_group(const __nv_bfloat16* const* A, int np, int qp, int in, const Meta& meta,
+                         __nv_bfloat16* dst, cudaStream_t st);
 // B [out, rsum] -> Bt [rsum, out]
 void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int rsum, cudaStream_t st);
 // C[T, N] (+)= Z[T,K] . Wop  +  sum over tile slots: Slot[128, r] . Vext_t
