@@ -329,7 +329,8 @@ def main():
     tasks = synth.c2_tasks()
     ranks = [t.rank for t in tasks]
     scales = [t.scale for t in tasks]
-    layer = LoraLayer(LLAMA2_7B, ranks, scales, dev, torch.bfloat16, tp_size, tp_rank, comm, seed=1234)
+    layer = LoraLayer(LLAMA2_7B, ranks, scales, dev, torch.bfloat16, tp_size, tp_rank, comm, seed=1234,
+                      group_inputs=os.environ.get("LOBRA_NO_GROUPS") != "1")
     max_tok = groups[my_group][2]
     io = layer.alloc_io(max_tok, seed=99 + rank)
 

@@ -518,6 +518,13 @@ int sms_hint() {
   return 148;   // B200
 }
 
+// Width the token-reduction units are balanced for: with the fused dY pass they only serve
+// the dA reduction (over `in`); the two-pass backward also reduces dB (over `out`) with them.
+int unit_width(const lobra_problem* prob) {
+  if (!prob) return 1;
+  return (int)(dy_fused() ? prob->in : std::min(prob->in, prob->out));
+}
+
 lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobra_adapters* ad,
                      int width_hint, int num_sms, Plan& P, Layout& L) {
   lobra_status st = validate(prob, b, ad);
@@ -541,7 +548,7 @@ extern "C" size_t lobra_lora_workspace_bytes(const lobra_problem* prob, const lo
   Plan P;
   Layout L;
   // the reduction-unit split depends on the SM count of the current device
-  if (prepare(prob, batch, ad, (int)std::min(prob ? prob->in : 1, prob ? prob->out : 1),
+  if (prepare(prob, batch, ad, unit_width(prob),
               sms_hint(), P, L) != LOBRA_OK)
     return 0;
   return L.total;
@@ -567,7 +574,7 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
   Layout L;
   lobra_status s = validate(prob, batch, ad);
   if (s != LOBRA_OK) return s;
-  s = prepare(prob, batch, ad, (int)std::min(prob->in, prob->out), sms_hint(), P, L);
+  s = prepare(prob, batch, ad, unit_width(prob), sms_hint(), P, L);
   if (s != LOBRA_OK) return s;
   if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
   if (!X || !W || !Y || !Hs || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");
@@ -641,7 +648,7 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
   Plan P;
   Layout L;
   // units sized for the wider of the two reductions (dA over `in`, dB over `out`)
-  if ((s = prepare(prob, batch, ad, (int)std::min(prob->in, prob->out), ctx->num_sms, P, L)) != LOBRA_OK)
+  if ((s = prepare(prob, batch, ad, unit_width(prob), ctx->num_sms, P, L)) != LOBRA_OK)
     return s;
   if (!X || !W || !Hs || !dY || !dX || !dA || !dB || !ws)
     return fail(LOBRA_ERR_INPUT, "null device pointer");
@@ -820,7 +827,7 @@ GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
 void group_plan(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga,
                 int num_sms, Plan& P) {
   lobra_adapters a0 = single_adapters(ga, 0);
-  build_plan(b, &a0, (int)std::min<int64_t>(g->in, min_out(g)), (int)max_out(g), num_sms, P, g->num_proj);
+  build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj);   // units: dA over in
 }
 
 // workspace / saved sizes of the fallback (per-projection sequences)

@@ -1,7 +1,10 @@
 """One Llama-shaped decoder layer's seven LoRA projections driven through the C ABI.
 
 This is plumbing around ``liblobra.so``: PyTorch allocates device memory, every step of
-the hot path runs in the library's kernels (``lobra_lora_fwd`` / ``lobra_lora_bwd``).
+the hot path runs in the library's kernels.  Projections that read the same input (q/k/v,
+gate/up) go through ``lobra_lora_group_fwd`` / ``lobra_lora_group_bwd`` (SURVEY §8(a) a1:
+one pass over X for the shrinks and one for the dA reductions); o and down through
+``lobra_lora_fwd`` / ``lobra_lora_bwd``.
 Projections: q, k, v, gate, up are column-parallel and o, down
 row-parallel under Megatron TP; every projection carries all tasks' adapters
 (reading Q3).
@@ -85,7 +88,7 @@ class _Proj:
 
 class LoraLayer:
     def __init__(self, shapes, ranks, scales, device, dtype=torch.bfloat16, tp_size=1, tp_rank=0,
-                 comm=None, seed=0):
+                 comm=None, seed=0, group_inputs=True):
         self.device = torch.device(device)
         self.dtype = dtype
         self.code = _lib.dtype_code(dtype)
@@ -93,6 +96,8 @@ class LoraLayer:
         self.scales = np.asarray(scales, np.float32)
         self.rsum = int(self.ranks.sum())
         self.tp_size, self.tp_rank, self.comm = tp_size, tp_rank, comm
+        self.group_inputs = group_inputs
+        self.group_Hs = {}
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
         self.projs = []
@@ -153,15 +158,31 @@ class LoraLayer:
             io["Y"][p.name] = torch.empty((T, p.out_l), device=self.device, dtype=self.dtype)
         return io
 
+    def members(self, group: str):
+        return [p for p in self.projs if p.group == group]
+
+    def _grouped(self, group: str) -> bool:
+        return self.group_inputs and len(self.members(group)) > 1
+
     def _ensure(self, seq_lens, seq_task):
         need = 0
-        for p in self.projs:
-            need = max(need, _lib.lobra_lora_workspace_bytes(self.code, p.in_l, p.out_l, seq_lens,
-                                                             seq_task, self.ranks, self.scales))
-            hs = _lib.lobra_lora_saved_bytes(self.code, p.in_l, p.out_l, seq_lens, seq_task,
-                                             self.ranks, self.scales)
-            if p.Hs is None or p.Hs.numel() < hs:
-                p.Hs = torch.empty(hs, dtype=torch.uint8, device=self.device)
+        for grp in self.groups():
+            ms = self.members(grp)
+            if self._grouped(grp):
+                args = (self.code, ms[0].in_l, [p.out_l for p in ms], seq_lens, seq_task, self.ranks,
+                        self.scales)
+                need = max(need, _lib.lobra_lora_group_workspace_bytes(*args))
+                hs = _lib.lobra_lora_group_saved_bytes(*args)
+                if grp not in self.group_Hs or self.group_Hs[grp].numel() < hs:
+                    self.group_Hs[grp] = torch.empty(hs, dtype=torch.uint8, device=self.device)
+                continue
+            for p in ms:
+                need = max(need, _lib.lobra_lora_workspace_bytes(self.code, p.in_l, p.out_l, seq_lens,
+                                                                 seq_task, self.ranks, self.scales))
+                hs = _lib.lobra_lora_saved_bytes(self.code, p.in_l, p.out_l, seq_lens, seq_task,
+                                                 self.ranks, self.scales)
+                if p.Hs is None or p.Hs.numel() < hs:
+                    p.Hs = torch.empty(hs, dtype=torch.uint8, device=self.device)
         if self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
 
@@ -180,30 +201,47 @@ class LoraLayer:
     # ------------------------------------------------------------------ the hot path
     def forward(self, seq_lens, seq_task, io, T: int, stream=None):
         self._ensure(seq_lens, seq_task)
-        for p in self.projs:
-            kind, comm = self._tp(p)
-            X = io["X"][p.group][:T]
-            _lib.lobra_lora_fwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task,
-                                io["Y"][p.name][:T], p.Hs, self.ws, tp_kind=kind, comm=comm,
-                                stream=stream)
+        for grp in self.groups():
+            ms = self.members(grp)
+            X = io["X"][grp][:T]
+            if self._grouped(grp):
+                kind, comm = self._tp(ms[0])
+                _lib.lobra_lora_group_fwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms],
+                                          self.ranks, self.scales, seq_lens, seq_task,
+                                          [io["Y"][p.name][:T] for p in ms], self.group_Hs[grp], self.ws,
+                                          tp_kind=kind, comm=comm, stream=stream)
+                continue
+            for p in ms:
+                kind, comm = self._tp(p)
+                _lib.lobra_lora_fwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task,
+                                    io["Y"][p.name][:T], p.Hs, self.ws, tp_kind=kind, comm=comm,
+                                    stream=stream)
 
     def backward(self, seq_lens, seq_task, io, T: int, accumulate_dadb: bool, stream=None):
-        """q/k/v (and gate/up) accumulate into one dX in the kernel epilogue
-        (accumulate_dx); for column-parallel TP only the LAST projection of a group asks
-        the library for the dX all-reduce, which then sums every projection's partial."""
-        last = {p.group: p.name for p in self.projs}
-        seen = set()
-        for p in self.projs:
-            kind, comm = self._tp(p)
-            if kind == _lib.LOBRA_TP_COLUMN and last[p.group] != p.name:
-                kind, comm = _lib.LOBRA_TP_NONE, None
-            dA, dB, dA_ld = self._grads(p)
-            _lib.lobra_lora_bwd(io["X"][p.group][:T], p.W, p.A, p.B, self.ranks, self.scales,
-                                seq_lens, seq_task, p.Hs, io["dY"][p.name][:T],
-                                io["dX"][p.group][:T], dA, dB, self.ws,
-                                accumulate_dx=p.group in seen, accumulate_dadb=accumulate_dadb,
-                                dA_ld=dA_ld, tp_kind=kind, comm=comm, stream=stream)
-            seen.add(p.group)
+        """A group's projections sum into one dX (the group call, or accumulate_dx on the
+        single calls); for column-parallel TP the dX all-reduce runs once per group, after
+        its last projection, and then sums every projection's partial."""
+        for grp in self.groups():
+            ms = self.members(grp)
+            X, dX = io["X"][grp][:T], io["dX"][grp][:T]
+            if self._grouped(grp):
+                kind, comm = self._tp(ms[0])
+                gr = [self._grads(p) for p in ms]
+                _lib.lobra_lora_group_bwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms],
+                                          self.ranks, self.scales, seq_lens, seq_task, self.group_Hs[grp],
+                                          [io["dY"][p.name][:T] for p in ms], dX, [g[0] for g in gr],
+                                          [g[1] for g in gr], self.ws, accumulate_dadb=accumulate_dadb,
+                                          dA_ld=gr[0][2], tp_kind=kind, comm=comm, stream=stream)
+                continue
+            for i, p in enumerate(ms):
+                kind, comm = self._tp(p)
+                if kind == _lib.LOBRA_TP_COLUMN and i != len(ms) - 1:
+                    kind, comm = _lib.LOBRA_TP_NONE, None
+                dA, dB, dA_ld = self._grads(p)
+                _lib.lobra_lora_bwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task, p.Hs,
+                                    io["dY"][p.name][:T], dX, dA, dB, self.ws, accumulate_dx=i > 0,
+                                    accumulate_dadb=accumulate_dadb, dA_ld=dA_ld, tp_kind=kind,
+                                    comm=comm, stream=stream)
 
     def sync_adapter_grads(self, stream=None):
         if self.comm is not None and self.comm.world > 1:

@@ -173,20 +173,25 @@ def test_group_empty_batch_zeroes_grads():
                      device=dev, dtype=torch.uint8)
     Hs = torch.empty(_lib.lobra_lora_group_saved_bytes(_lib.LOBRA_BF16, d_in, outs, L, K, r, s), device=dev,
                      dtype=torch.uint8)
-    X = torch.empty(0, d_in, device=dev, dtype=torch.bfloat16)
+    X = torch.zeros(1, d_in, device=dev, dtype=torch.bfloat16)   # non-null dummies (T = 0)
     Ws = [torch.zeros(o, d_in, device=dev, dtype=torch.bfloat16) for o in outs]
     As = [torch.zeros(24, d_in, device=dev, dtype=torch.bfloat16) for _ in outs]
     Bs = [torch.zeros(o, 24, device=dev, dtype=torch.bfloat16) for o in outs]
-    Ys = [torch.empty(0, o, device=dev, dtype=torch.bfloat16) for o in outs]
-    dYs = [torch.empty(0, o, device=dev, dtype=torch.bfloat16) for o in outs]
+    Ys = [torch.zeros(1, o, device=dev, dtype=torch.bfloat16) for o in outs]
+    dYs = [torch.zeros(1, o, device=dev, dtype=torch.bfloat16) for o in outs]
     dA = [torch.full((24, d_in), 3.0, device=dev) for _ in outs]
     dB = [torch.full((o, 24), 3.0, device=dev) for o in outs]
-    dX = torch.empty(0, d_in, device=dev, dtype=torch.bfloat16)
+    dX = torch.zeros(1, d_in, device=dev, dtype=torch.bfloat16)
     _lib.lobra_lora_group_fwd(X, Ws, As, Bs, r, s, L, K, Ys, Hs, ws)
     _lib.lobra_lora_group_bwd(X, Ws, As, Bs, r, s, L, K, Hs, dYs, dX, dA, dB, ws)
     torch.cuda.synchronize()
     for a, b in zip(dA, dB):
         assert not a.any() and not b.any()
+    for a in dA:
+        a.fill_(3.0)
+    _lib.lobra_lora_group_bwd(X, Ws, As, Bs, r, s, L, K, Hs, dYs, dX, dA, dB, ws, accumulate_dadb=True)
+    torch.cuda.synchronize()
+    assert all((a == 3.0).all() for a in dA)
 
 
 def test_group_errors():
@@ -196,3 +201,31 @@ def test_group_errors():
         _lib.lobra_lora_group_workspace_bytes(_lib.LOBRA_BF16, 128, [128, 100], [5], [0], [8], [1.0])
     with pytest.raises(_lib.LobraError):     # more than 4 projections
         _lib.lobra_lora_group_workspace_bytes(_lib.LOBRA_BF16, 128, [128] * 5, [5], [0], [8], [1.0])
+
+
+def test_layer_grouped_equals_ungrouped():
+    """LoraLayer drives q/k/v and gate/up through the group calls: the outputs, dX and the
+    flat adapter-gradient buffer are bitwise those of the per-projection calls."""
+    torch = _torch()
+    from paper_2509_01193_b200.layer import LoraLayer
+    shapes = [("q", 256, 256, "col", "attn"), ("k", 256, 128, "col", "attn"), ("v", 256, 128, "col", "attn"),
+              ("o", 256, 256, "row", "o_in"), ("gate", 256, 512, "col", "mlp"), ("up", 256, 512, "col", "mlp"),
+              ("down", 512, 256, "row", "down_in")]
+    wl = _workload(12, (16, 8, 16), (2.0, 1.0, 0.5), 9, 200)
+    out = []
+    for grouped in (True, False):
+        layer = LoraLayer(shapes, wl.ranks, wl.scales, "cuda:0", seed=3, group_inputs=grouped)
+        io = layer.alloc_io(wl.T, seed=4)
+        for acc in (False, True):
+            layer.forward(wl.seq_lens, wl.seq_task, io, wl.T)
+            layer.backward(wl.seq_lens, wl.seq_task, io, wl.T, accumulate_dadb=acc)
+        torch.cuda.synchronize()
+        out.append(({k: v.clone() for k, v in io["Y"].items()}, {k: v.clone() for k, v in io["dX"].items()},
+                    layer.flat_grad.clone()))
+    (Yg, dXg, fg), (Yu, dXu, fu) = out
+    for k in Yg:
+        assert torch.equal(Yg[k], Yu[k]), k
+    for k in dXg:
+        assert torch.equal(dXg[k], dXu[k]), k
+    assert torch.equal(fg, fu)
+    assert torch.isfinite(fg).all()
