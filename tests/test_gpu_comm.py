@@ -49,6 +49,29 @@ for kind in (_lib.LOBRA_TP_NONE, _lib.LOBRA_TP_COLUMN, _lib.LOBRA_TP_ROW):
 for kind in (_lib.LOBRA_TP_COLUMN, _lib.LOBRA_TP_ROW):
     for a, b in zip(outs[_lib.LOBRA_TP_NONE], outs[kind]):
         assert torch.equal(a, b), kind
+# projection group (q/k/v-like, 3 bands) through the group calls: COLUMN all-reduces dX
+# once, ROW every Y_p; with forced 1-rank collectives both equal the no-TP run
+outs_g = [192, 128, 64]
+tg = [synth.layer_tensors(wl, 256, o, seed=9 + p) for p, o in enumerate(outs_g)]
+up = lambda a: torch.from_numpy(synth.round_bf16(a)).to(dev).to(torch.bfloat16)
+Ws = [up(x["W"]) for x in tg]; As = [up(x["A"]) for x in tg]; Bs = [up(x["B"]) for x in tg]
+dYs = [up(x["dY"]) for x in tg]
+wsg = torch.empty(_lib.lobra_lora_group_workspace_bytes(code, 256, outs_g, lens, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+Hg = torch.empty(_lib.lobra_lora_group_saved_bytes(code, 256, outs_g, lens, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+res = {}
+for kind in (_lib.LOBRA_TP_NONE, _lib.LOBRA_TP_COLUMN, _lib.LOBRA_TP_ROW):
+    c = None if kind == _lib.LOBRA_TP_NONE else comm
+    Ys = [torch.empty(T, o, dtype=torch.bfloat16, device=dev) for o in outs_g]
+    dX = torch.empty(T, 256, dtype=torch.bfloat16, device=dev)
+    dA = [torch.empty(24, 256, dtype=torch.float32, device=dev) for _ in outs_g]
+    dB = [torch.empty(o, 24, dtype=torch.float32, device=dev) for o in outs_g]
+    _lib.lobra_lora_group_fwd(d["X"], Ws, As, Bs, ranks, scales, lens, tasks, Ys, Hg, wsg, tp_kind=kind, comm=c)
+    _lib.lobra_lora_group_bwd(d["X"], Ws, As, Bs, ranks, scales, lens, tasks, Hg, dYs, dX, dA, dB, wsg, tp_kind=kind, comm=c)
+    torch.cuda.synchronize()
+    res[kind] = [x.float().cpu() for x in Ys + [dX] + dA + dB]
+for kind in (_lib.LOBRA_TP_COLUMN, _lib.LOBRA_TP_ROW):
+    for a, b in zip(res[_lib.LOBRA_TP_NONE], res[kind]):
+        assert torch.equal(a, b), ("group", kind)
 comm.destroy()
 print("COMM_OK")
 '''
