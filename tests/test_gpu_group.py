@@ -229,3 +229,17 @@ def test_layer_grouped_equals_ungrouped():
         assert torch.equal(dXg[k], dXu[k]), k
     assert torch.equal(fg, fu)
     assert torch.isfinite(fg).all()
+
+
+def test_group_c2_qkv_full_size_equals_single_sequence():
+    """BASELINE config 2 at full size (T = 16384, 4 tasks r = 16, s = 2; 7B q/k/v 4096 ->
+    4096 sharing X), in the launch configuration bench.py times: the group call gives
+    bitwise the single-projection sequence (which test_gpu_lora checks against the oracle
+    at this size)."""
+    wl = synth.config_c2()
+    d_in, outs = 4096, [4096, 4096, 4096]
+    g, _, _, _ = _run(wl, d_in, outs, seed=31)
+    s, _, _, _ = _run(wl, d_in, outs, seed=31, group=False)
+    _same(g, s)
+    for y in g["Y"]:
+        assert np.isfinite(y).all()
