@@ -224,6 +224,44 @@ LOBRA_API lobra_status lobra_lora_group_bwd(const lobra_group_problem* prob,
                                             lobra_stream_t stream);
 
 /* ------------------------------------------------------------------------------
+ * Decoder-layer operations around the LoRA projections (one Llama layer,
+ * the unit the paper's cost model profiles, App. D).  Public Llama-2 definitions
+ * (reading Q27); bf16 tensors, fp32 arithmetic, one rounding per output.
+ * Device pointers 16-byte aligned; widths multiples of 8.  Host-side checks run before any
+ * launch (LOBRA_ERR_INPUT); launch failures -> LOBRA_ERR_CUDA.
+ *
+ * lobra_rmsnorm_fwd: S = X + R (R may be NULL: S = X; when R != NULL S is written to S_out),
+ *   Y = S / sqrt(mean_row(S^2) + eps) * g, rstd[row] = 1 / sqrt(mean_row(S^2) + eps) (fp32,
+ *   saved for the backward).  X, R, S_out, Y [T, h]; g [h]; h <= 16384.
+ * lobra_rmsnorm_bwd: with u = g * dY (g frozen, no dg):
+ *   dS = rstd u - S rstd^3 (u . S) / h  (+ dRes when dRes != NULL: the residual stream's
+ *   gradient, fused), written to dS [T, h].
+ * ------------------------------------------------------------------------------ */
+LOBRA_API lobra_status lobra_rmsnorm_fwd(int64_t T, int64_t h, const void* X, const void* R,
+                                         void* S_out, const void* g, float eps, void* Y,
+                                         float* rstd, lobra_stream_t stream);
+LOBRA_API lobra_status lobra_rmsnorm_bwd(int64_t T, int64_t h, const void* dY, const void* S,
+                                         const void* g, const float* rstd, const void* dRes,
+                                         void* dS, lobra_stream_t stream);
+/* lobra_rope: rotary position embedding IN PLACE on Q [T, n_heads * head_dim] (row stride
+ *   ldq elements) and, if K != NULL, on K (stride ldk): the position of a token is its index
+ *   inside its own packed sequence (restarts at 0, cu_seqlens: device int32 [num_seqs + 1]
+ *   prefix offsets), angle_j = pos * theta^(-2j / head_dim) for j < head_dim / 2, pairs
+ *   (j, j + head_dim/2): (a, b) -> (a cos - b sin, b cos + a sin); inverse != 0 rotates by
+ *   -angle (the backward).  head_dim % 16 == 0. */
+LOBRA_API lobra_status lobra_rope(int32_t num_seqs, const int32_t* cu_seqlens, int64_t T,
+                                  int32_t n_heads, int32_t head_dim, float theta, void* Q,
+                                  int64_t ldq, void* K, int64_t ldk, int inverse,
+                                  lobra_stream_t stream);
+/* lobra_swiglu_fwd: act = silu(gate) * up, elementwise over n (n % 8 == 0).
+ * lobra_swiglu_bwd: with s = sigmoid(gate): d_gate = d up s (1 + gate (1 - s)),
+ *   d_up = d gate s. */
+LOBRA_API lobra_status lobra_swiglu_fwd(int64_t n, const void* gate, const void* up, void* act,
+                                        lobra_stream_t stream);
+LOBRA_API lobra_status lobra_swiglu_bwd(int64_t n, const void* d, const void* gate, const void* up,
+                                        void* d_gate, void* d_up, lobra_stream_t stream);
+
+/* ------------------------------------------------------------------------------
  * Per-step dispatch (host only, deterministic; every rank may compute it locally).
  * Implements P:591-619 (dynamic bucketing DP over the grid u_k = k*grid_step,
  * k = 1..grid_max/grid_step, empty intervals ignored, lexicographically smallest optimal
@@ -403,7 +441,8 @@ enum {
   LOBRA_K_PAD = 5,        /* adapter operand packing                            */
   LOBRA_K_FP32 = 6,       /* fp32 SIMT path kernels                             */
   LOBRA_K_OPT = 7,        /* adapter optimizer (AdamW)                          */
-  LOBRA_K_NUM = 8
+  LOBRA_K_LAYER = 8,      /* decoder-layer elementwise ops (RMSNorm, RoPE, SwiGLU) */
+  LOBRA_K_NUM = 9
 };
 typedef struct {
   int64_t count[LOBRA_K_NUM];   /* launches per class since the last reset        */

@@ -27,9 +27,10 @@ EXPORTED = [
     "lobra_shutdown", "lobra_profile_enable", "lobra_profile_read", "lobra_launch_count",
     "lobra_adamw_step", "lobra_plan_deployment", "lobra_propose_configs",
     "lobra_lora_group_workspace_bytes", "lobra_lora_group_saved_bytes", "lobra_lora_group_fwd",
-    "lobra_lora_group_bwd",
+    "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
+    "lobra_swiglu_bwd",
 ]
-K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim"]
+K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -94,7 +95,7 @@ class AdamHP(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("count", C.c_int64 * 8), ("ms", C.c_double * 8)]
+    _fields_ = [("count", C.c_int64 * len(K_NAMES)), ("ms", C.c_double * len(K_NAMES))]
 
 
 _LIB = None
@@ -142,6 +143,18 @@ def load() -> C.CDLL:
     lib.lobra_lora_group_bwd.argtypes = [_gp, _gb, _ga, C.c_void_p, _vpp, C.c_void_p, _vpp,
                                          C.c_void_p, C.c_int, _vpp, _vpp, C.c_int, C.c_void_p,
                                          C.c_size_t, C.c_void_p]
+    _vp_ = C.c_void_p
+    lib.lobra_rmsnorm_fwd.restype = C.c_int
+    lib.lobra_rmsnorm_fwd.argtypes = [C.c_int64, C.c_int64, _vp_, _vp_, _vp_, _vp_, C.c_float, _vp_, _vp_, _vp_]
+    lib.lobra_rmsnorm_bwd.restype = C.c_int
+    lib.lobra_rmsnorm_bwd.argtypes = [C.c_int64, C.c_int64, _vp_, _vp_, _vp_, _vp_, _vp_, _vp_, _vp_]
+    lib.lobra_rope.restype = C.c_int
+    lib.lobra_rope.argtypes = [C.c_int32, _vp_, C.c_int64, C.c_int32, C.c_int32, C.c_float, _vp_, C.c_int64,
+                               _vp_, C.c_int64, C.c_int, _vp_]
+    lib.lobra_swiglu_fwd.restype = C.c_int
+    lib.lobra_swiglu_fwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_]
+    lib.lobra_swiglu_bwd.restype = C.c_int
+    lib.lobra_swiglu_bwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_, _vp_, _vp_]
     lib.lobra_dispatch.restype = C.c_int
     lib.lobra_dispatch.argtypes = [C.POINTER(Deployment), C.POINTER(Batch), C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int32, C.c_int32, C.c_int64,
@@ -428,7 +441,7 @@ def lobra_profile_read(reset: bool = True) -> dict:
     """{kernel class: (launches, device ms)} since the last reset (synchronises)."""
     p = Profile()
     _check(load().lobra_profile_read(C.byref(p), int(bool(reset))))
-    return {K_NAMES[k]: (int(p.count[k]), float(p.ms[k])) for k in range(8)}
+    return {K_NAMES[k]: (int(p.count[k]), float(p.ms[k])) for k in range(len(K_NAMES))}
 
 
 def lobra_launch_count() -> int:
@@ -487,3 +500,34 @@ def lobra_propose_configs(tp, pp, seq_lens, thruput, gpu_counts):
     if st != LOBRA_OK:
         raise LobraError(st, load().lobra_last_error().decode())
     return win, keep
+
+
+# ------------------------------------------------------------------ decoder-layer ops
+def lobra_rmsnorm_fwd(X, g, eps, Y, rstd, R=None, S_out=None, stream=None):
+    """Y = rmsnorm(X (+ R)) * g; S_out = X + R when R is given (include/lobra.h)."""
+    T, h = int(X.shape[0]), int(X.shape[1])
+    _check(load().lobra_rmsnorm_fwd(T, h, _ptr(X), _ptr(R) or None, _ptr(S_out) or None, _ptr(g), float(eps),
+                                    _ptr(Y), _ptr(rstd), _stream(stream)))
+
+
+def lobra_rmsnorm_bwd(dY, S, g, rstd, dS, dRes=None, stream=None):
+    T, h = int(S.shape[0]), int(S.shape[1])
+    _check(load().lobra_rmsnorm_bwd(T, h, _ptr(dY), _ptr(S), _ptr(g), _ptr(rstd), _ptr(dRes) or None, _ptr(dS),
+                                    _stream(stream)))
+
+
+def lobra_rope(cu_seqlens, T, n_heads, head_dim, theta, Q, K=None, inverse=False, stream=None):
+    """In-place rotary embedding on Q (and K), positions restarted per packed sequence."""
+    ldq = int(Q.stride(0))
+    ldk = int(K.stride(0)) if K is not None else 0
+    _check(load().lobra_rope(int(cu_seqlens.numel()) - 1, _ptr(cu_seqlens), int(T), int(n_heads), int(head_dim),
+                             float(theta), _ptr(Q), ldq, _ptr(K) or None, ldk, int(bool(inverse)), _stream(stream)))
+
+
+def lobra_swiglu_fwd(gate, up, act, stream=None):
+    _check(load().lobra_swiglu_fwd(int(gate.numel()), _ptr(gate), _ptr(up), _ptr(act), _stream(stream)))
+
+
+def lobra_swiglu_bwd(d, gate, up, d_gate, d_up, stream=None):
+    _check(load().lobra_swiglu_bwd(int(gate.numel()), _ptr(d), _ptr(gate), _ptr(up), _ptr(d_gate), _ptr(d_up),
+                                   _stream(stream)))
