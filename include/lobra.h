@@ -260,6 +260,9 @@ LOBRA_API lobra_status lobra_swiglu_fwd(int64_t n, const void* gate, const void*
                                         lobra_stream_t stream);
 LOBRA_API lobra_status lobra_swiglu_bwd(int64_t n, const void* d, const void* gate, const void* up,
                                         void* d_gate, void* d_up, lobra_stream_t stream);
+/* lobra_add: C = A + B elementwise over n bf16 (n % 8 == 0; C may alias A or B): the
+ * layer's last residual add. */
+LOBRA_API lobra_status lobra_add(int64_t n, const void* A, const void* B, void* C, lobra_stream_t stream);
 
 /* ------------------------------------------------------------------------------
  * Per-step dispatch (host only, deterministic; every rank may compute it locally).

@@ -28,7 +28,7 @@ EXPORTED = [
     "lobra_adamw_step", "lobra_plan_deployment", "lobra_propose_configs",
     "lobra_lora_group_workspace_bytes", "lobra_lora_group_saved_bytes", "lobra_lora_group_fwd",
     "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
-    "lobra_swiglu_bwd",
+    "lobra_swiglu_bwd", "lobra_add",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer"]
 
@@ -155,6 +155,8 @@ def load() -> C.CDLL:
     lib.lobra_swiglu_fwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_]
     lib.lobra_swiglu_bwd.restype = C.c_int
     lib.lobra_swiglu_bwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_, _vp_, _vp_]
+    lib.lobra_add.restype = C.c_int
+    lib.lobra_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
     lib.lobra_dispatch.argtypes = [C.POINTER(Deployment), C.POINTER(Batch), C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int32, C.c_int32, C.c_int64,
@@ -531,3 +533,7 @@ def lobra_swiglu_fwd(gate, up, act, stream=None):
 def lobra_swiglu_bwd(d, gate, up, d_gate, d_up, stream=None):
     _check(load().lobra_swiglu_bwd(int(gate.numel()), _ptr(d), _ptr(gate), _ptr(up), _ptr(d_gate), _ptr(d_up),
                                    _stream(stream)))
+
+
+def lobra_add(A, B, C_, stream=None):
+    _check(load().lobra_add(int(A.numel()), _ptr(A), _ptr(B), _ptr(C_), _stream(stream)))

@@ -206,6 +206,17 @@ __global__ void k_swiglu_bwd(long long nv, const __nv_bfloat16* __restrict__ d, 
   }
 }
 
+__global__ void k_add(long long nv, const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* C) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    float a[8], b[8];
+    unpack8(reinterpret_cast<const uint4*>(A)[i], a);
+    unpack8(reinterpret_cast<const uint4*>(B)[i], b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] += b[e];
+    reinterpret_cast<uint4*>(C)[i] = pack8(a);
+  }
+}
+
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int sm_count() {
@@ -322,4 +333,17 @@ extern "C" lobra_status lobra_swiglu_bwd(int64_t n, const void* d, const void* g
                                                 static_cast<__nv_bfloat16*>(d_gate), static_cast<__nv_bfloat16*>(d_up));
   count_launch(LOBRA_K_LAYER, st, false);
   return done("lobra_swiglu_bwd");
+}
+
+extern "C" lobra_status lobra_add(int64_t n, const void* A, const void* B, void* C, lobra_stream_t stream) {
+  clear_error();
+  if (n < 0 || n % 8 || !A || !B || !C) return fail(LOBRA_ERR_INPUT, "add: n % 8 == 0 and non-null pointers");
+  if (!al16(A) || !al16(B) || !al16(C)) return fail(LOBRA_ERR_INPUT, "add: pointers must be 16-byte aligned");
+  if (n == 0) return LOBRA_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  count_launch(LOBRA_K_LAYER, st, true);
+  k_add<<<4 * sm_count(), 256, 0, st>>>(n / 8, static_cast<const __nv_bfloat16*>(A),
+                                         static_cast<const __nv_bfloat16*>(B), static_cast<__nv_bfloat16*>(C));
+  count_launch(LOBRA_K_LAYER, st, false);
+  return done("lobra_add");
 }

@@ -164,6 +164,9 @@ class LoraLayer:
     def _grouped(self, group: str) -> bool:
         return self.group_inputs and len(self.members(group)) > 1
 
+    def ensure(self, seq_lens, seq_task):
+        self._ensure(seq_lens, seq_task)
+
     def _ensure(self, seq_lens, seq_task):
         need = 0
         for grp in self.groups():
@@ -199,49 +202,56 @@ class LoraLayer:
         return (_lib.LOBRA_TP_COLUMN if p.kind == "col" else _lib.LOBRA_TP_ROW), self.comm
 
     # ------------------------------------------------------------------ the hot path
-    def forward(self, seq_lens, seq_task, io, T: int, stream=None):
-        self._ensure(seq_lens, seq_task)
-        for grp in self.groups():
-            ms = self.members(grp)
-            X = io["X"][grp][:T]
-            if self._grouped(grp):
-                kind, comm = self._tp(ms[0])
-                _lib.lobra_lora_group_fwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms],
-                                          self.ranks, self.scales, seq_lens, seq_task,
-                                          [io["Y"][p.name][:T] for p in ms], self.group_Hs[grp], self.ws,
-                                          tp_kind=kind, comm=comm, stream=stream)
-                continue
-            for p in ms:
-                kind, comm = self._tp(p)
-                _lib.lobra_lora_fwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task,
-                                    io["Y"][p.name][:T], p.Hs, self.ws, tp_kind=kind, comm=comm,
-                                    stream=stream)
+    def forward_group(self, grp, seq_lens, seq_task, X, Ys: dict, stream=None):
+        """The projections of input group `grp` over X [T, in] into Ys[name] [T, out]."""
+        ms = self.members(grp)
+        if self._grouped(grp):
+            kind, comm = self._tp(ms[0])
+            _lib.lobra_lora_group_fwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms],
+                                      self.ranks, self.scales, seq_lens, seq_task, [Ys[p.name] for p in ms],
+                                      self.group_Hs[grp], self.ws, tp_kind=kind, comm=comm, stream=stream)
+            return
+        for p in ms:
+            kind, comm = self._tp(p)
+            _lib.lobra_lora_fwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task, Ys[p.name], p.Hs,
+                                self.ws, tp_kind=kind, comm=comm, stream=stream)
 
-    def backward(self, seq_lens, seq_task, io, T: int, accumulate_dadb: bool, stream=None):
+    def backward_group(self, grp, seq_lens, seq_task, X, dYs: dict, dX, accumulate_dadb: bool, stream=None):
         """A group's projections sum into one dX (the group call, or accumulate_dx on the
         single calls); for column-parallel TP the dX all-reduce runs once per group, after
         its last projection, and then sums every projection's partial."""
+        ms = self.members(grp)
+        if self._grouped(grp):
+            kind, comm = self._tp(ms[0])
+            gr = [self._grads(p) for p in ms]
+            _lib.lobra_lora_group_bwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms], self.ranks,
+                                      self.scales, seq_lens, seq_task, self.group_Hs[grp],
+                                      [dYs[p.name] for p in ms], dX, [g[0] for g in gr], [g[1] for g in gr],
+                                      self.ws, accumulate_dadb=accumulate_dadb, dA_ld=gr[0][2], tp_kind=kind,
+                                      comm=comm, stream=stream)
+            return
+        for i, p in enumerate(ms):
+            kind, comm = self._tp(p)
+            if kind == _lib.LOBRA_TP_COLUMN and i != len(ms) - 1:
+                kind, comm = _lib.LOBRA_TP_NONE, None
+            dA, dB, dA_ld = self._grads(p)
+            _lib.lobra_lora_bwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task, p.Hs, dYs[p.name],
+                                dX, dA, dB, self.ws, accumulate_dx=i > 0, accumulate_dadb=accumulate_dadb,
+                                dA_ld=dA_ld, tp_kind=kind, comm=comm, stream=stream)
+
+    def forward(self, seq_lens, seq_task, io, T: int, stream=None):
+        """Every projection on synthetic per-group inputs io["X"][group] (the north-star
+        step: the seven projections of one layer)."""
+        self._ensure(seq_lens, seq_task)
         for grp in self.groups():
-            ms = self.members(grp)
-            X, dX = io["X"][grp][:T], io["dX"][grp][:T]
-            if self._grouped(grp):
-                kind, comm = self._tp(ms[0])
-                gr = [self._grads(p) for p in ms]
-                _lib.lobra_lora_group_bwd(X, [p.W for p in ms], [p.A for p in ms], [p.B for p in ms],
-                                          self.ranks, self.scales, seq_lens, seq_task, self.group_Hs[grp],
-                                          [io["dY"][p.name][:T] for p in ms], dX, [g[0] for g in gr],
-                                          [g[1] for g in gr], self.ws, accumulate_dadb=accumulate_dadb,
-                                          dA_ld=gr[0][2], tp_kind=kind, comm=comm, stream=stream)
-                continue
-            for i, p in enumerate(ms):
-                kind, comm = self._tp(p)
-                if kind == _lib.LOBRA_TP_COLUMN and i != len(ms) - 1:
-                    kind, comm = _lib.LOBRA_TP_NONE, None
-                dA, dB, dA_ld = self._grads(p)
-                _lib.lobra_lora_bwd(X, p.W, p.A, p.B, self.ranks, self.scales, seq_lens, seq_task, p.Hs,
-                                    io["dY"][p.name][:T], dX, dA, dB, self.ws, accumulate_dx=i > 0,
-                                    accumulate_dadb=accumulate_dadb, dA_ld=dA_ld, tp_kind=kind,
-                                    comm=comm, stream=stream)
+            self.forward_group(grp, seq_lens, seq_task, io["X"][grp][:T],
+                               {p.name: io["Y"][p.name][:T] for p in self.members(grp)}, stream)
+
+    def backward(self, seq_lens, seq_task, io, T: int, accumulate_dadb: bool, stream=None):
+        for grp in self.groups():
+            self.backward_group(grp, seq_lens, seq_task, io["X"][grp][:T],
+                                {p.name: io["dY"][p.name][:T] for p in self.members(grp)}, io["dX"][grp][:T],
+                                accumulate_dadb, stream)
 
     def sync_adapter_grads(self, stream=None):
         if self.comm is not None and self.comm.world > 1:
