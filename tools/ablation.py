@@ -18,6 +18,11 @@
    with every dispatch computed by lobra_dispatch (the exact C++ solver), the deployment
    for B-D chosen by enumerating all TP{1,2,4} mixes of 8 GPUs (a small stage-1 search).
 GPU-seconds per step = N x max over replicas of the sum of its chunk times.
+
+--layer-cost profiles/r1_layer_cost.json (tools/bench_layer.py --fit) replaces step 1 by the
+full decoder layer's measured App. D cost t = c0 + c1 sum(s) + c2 sum(s^2) per chunk
+(attention's s^2 term real); TP-k replicas divide the token-dependent part
+by k.  Output then goes to profiles/r1_ablation_layer.json.
 """
 from __future__ import annotations
 
@@ -69,15 +74,19 @@ def measure_layer(Ts=(1024, 2048, 4096, 8192, 16384), reps=5):
     return {"points_s": {int(k): v for k, v in out.items()}, "a0_s": float(a0), "a1_s_per_token": float(a1)}
 
 
-def t_rep(k, T, a0, a1):
+QUAD = {"c2": 0.0}   # s^2 coefficient (seconds per token x length) when --layer-cost is given
+
+
+def t_rep(k, T, a0, a1, S2=0.0):
+    """Chunk time on a TP-k replica: T tokens, S2 = sum of squared sequence lengths."""
     comm = 0.0 if k == 1 else 4 * 2 * (k - 1) / k * T * 4096 * 2 / BUS_BW
-    return a0 + a1 * T / k + comm
+    return a0 + (a1 * T + QUAD["c2"] * S2) / k + comm
 
 
 def cost_table(groups, a0, a1, grid_step, grid_max, unit=1e-5):
     U = grid_max // grid_step
-    return [[max(1, int(round(t_rep(tp, (u + 1) * grid_step, 0.0, a1) / unit))) for u in range(U)]
-            for tp, _, _ in groups]
+    return [[max(1, int(round(t_rep(tp, (u + 1) * grid_step, 0.0, a1, float((u + 1) * grid_step) ** 2) / unit)))
+             for u in range(U)] for tp, _, _ in groups]
 
 
 def step_time(groups, wl, mode, grid_step, R, a0, a1):
@@ -94,8 +103,8 @@ def step_time(groups, wl, mode, grid_step, R, a0, a1):
         mine = d["seq_replica"] == rep
         t = 0.0
         for c in set(d["seq_chunk"][mine].tolist()):
-            T = int(wl.seq_lens[mine & (d["seq_chunk"] == c)].sum())
-            t += t_rep(tp[gi], T, a0, a1)
+            ls = wl.seq_lens[mine & (d["seq_chunk"] == c)].astype(np.float64)
+            t += t_rep(tp[gi], float(ls.sum()), a0, a1, float((ls ** 2).sum()))
         times.append(t)
     return max(times), float(np.mean(times))
 
@@ -115,8 +124,16 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_ablation.json"))
     ap.add_argument("--a0", type=float, default=None, help="skip the GPU measurement (seconds)")
     ap.add_argument("--a1", type=float, default=None)
+    ap.add_argument("--layer-cost", default=None, help="App. D fit of the full layer (tools/bench_layer.py)")
     args = ap.parse_args()
-    if args.a0 is None:
+    if args.layer_cost:
+        lc = json.load(open(args.layer_cost))
+        cal = {"source": args.layer_cost, "model": lc["model"], "a0_s": lc["c0_ms"] / 1e3,
+               "a1_s_per_token": lc["c1_ms_per_token"] / 1e3, "c2_s_per_token_len": lc["c2_ms_per_token_len"] / 1e3}
+        QUAD["c2"] = cal["c2_s_per_token_len"]
+        if args.out.endswith("r1_ablation.json"):
+            args.out = args.out.replace("r1_ablation.json", "r1_ablation_layer.json")
+    elif args.a0 is None:
         cal = measure_layer()
     else:
         cal = {"points_s": {}, "a0_s": args.a0, "a1_s_per_token": args.a1}
