@@ -11,33 +11,24 @@ Public Llama-2 layer (reading Q27; oracle/decoder.py is its fp64 defin
 
 Our kernels (C ABI, liblobra.so): the seven LoRA projections (q/k/v and gate/up as
 projection groups), RMSNorm with the fused residual add / residual-gradient add, RoPE,
-SwiGLU, the last residual add.  Attention: FlashAttention-2's varlen kernels from the image
-(`flash_attn`, a library call like cuBLAS; our own tcgen05 attention is the next step,
-DESIGN.md §10).  PyTorch only allocates memory.
+SwiGLU, the last residual add.  Attention: a library call like cuBLAS (attention.py: cuDNN's
+ragged SDPA by default, FlashAttention-2 varlen as the alternative; our own tcgen05
+attention is the next step).  PyTorch only allocates memory.
 """
 from __future__ import annotations
-
-import math
 
 import numpy as np
 import torch
 
 from . import _lib
+from .attention import make_attention
 from .layer import LLAMA2_7B, LoraLayer
-
-
-def _fa():
-    try:
-        from flash_attn import flash_attn_interface as fa
-    except Exception as e:   # pragma: no cover - environment specific
-        raise RuntimeError(f"flash_attn (varlen attention library) unavailable: {e}")
-    return fa
 
 
 class DecoderLayer:
     def __init__(self, shapes=LLAMA2_7B, n_heads=32, ranks=(16,), scales=(2.0,), device="cuda:0",
                  dtype=torch.bfloat16, seed=0, eps=1e-5, theta=10000.0, group_inputs=True,
-                 deterministic_attn=False):
+                 deterministic_attn=False, attn_backend="cudnn"):
         assert dtype == torch.bfloat16, "the decoder layer runs the bf16 path"
         self.dev = torch.device(device)
         self.lora = LoraLayer(shapes, ranks, scales, self.dev, dtype, seed=seed, group_inputs=group_inputs)
@@ -46,7 +37,7 @@ class DecoderLayer:
         self.n_heads = n_heads
         self.head_dim = self.h // n_heads
         self.eps, self.theta = eps, theta
-        self.deterministic_attn = deterministic_attn
+        self.attn = make_attention(attn_backend, n_heads, self.head_dim, self.dev, deterministic_attn)
         g = torch.Generator(device=self.dev)
         g.manual_seed(seed + 7)
         # frozen RMSNorm gains (synthetic: 1 + N(0, 0.1^2))
@@ -66,7 +57,6 @@ class DecoderLayer:
     # ------------------------------------------------------------------ forward
     def forward(self, seq_lens, seq_task, X, stream=None):
         """X [T, h] bf16 (device) -> Y [T, h]; keeps the activations for backward()."""
-        fa = _fa()
         seq_lens = np.asarray(seq_lens, np.int32)
         seq_task = np.asarray(seq_task, np.int32)
         T, h, f = int(seq_lens.sum()), self.h, self.f
@@ -84,21 +74,20 @@ class DecoderLayer:
         _lib.lobra_rmsnorm_fwd(X, self.g_attn, self.eps, h1, r1, stream=stream)
         L.forward_group("attn", seq_lens, seq_task, h1, {"q": q, "k": k, "v": v}, stream)
         _lib.lobra_rope(cu, T, H, D, self.theta, q, k, stream=stream)
-        att, lse, _, _ = fa._flash_attn_varlen_forward(q.view(T, H, D), k.view(T, H, D), v.view(T, H, D), cu, cu,
-                                                       maxlen, maxlen, 0.0, 1.0 / math.sqrt(D), True)
+        att, lse, actx = self.attn.forward(q.view(T, H, D), k.view(T, H, D), v.view(T, H, D), seq_lens)
         L.forward_group("o_in", seq_lens, seq_task, att.view(T, h), {"o": o}, stream)
         _lib.lobra_rmsnorm_fwd(X, self.g_mlp, self.eps, h2, r2, R=o, S_out=x2, stream=stream)
         L.forward_group("mlp", seq_lens, seq_task, h2, {"gate": gate, "up": up}, stream)
         _lib.lobra_swiglu_fwd(gate, up, act, stream=stream)
         L.forward_group("down_in", seq_lens, seq_task, act, {"down": down}, stream)
         _lib.lobra_add(x2, down, Y, stream=stream)
-        self.saved = dict(seq_lens=seq_lens, seq_task=seq_task, cu=cu, maxlen=maxlen, X=X, att=att, lse=lse, T=T)
+        self.saved = dict(seq_lens=seq_lens, seq_task=seq_task, cu=cu, maxlen=maxlen, X=X, att=att, lse=lse, T=T,
+                          actx=actx)
         return Y
 
     # ------------------------------------------------------------------ backward
     def backward(self, dY, accumulate_dadb=False, stream=None):
         """dY [T, h] -> dX [T, h]; adapter gradients (+)= into self.lora.flat_grad."""
-        fa = _fa()
         s = self.saved
         seq_lens, seq_task, cu, maxlen, T = s["seq_lens"], s["seq_task"], s["cu"], s["maxlen"], s["T"]
         h, f, H, D = self.h, self.f, self.n_heads, self.head_dim
@@ -117,10 +106,8 @@ class DecoderLayer:
         L.backward_group("mlp", seq_lens, seq_task, h2, {"gate": d_gate, "up": d_up}, dh2, accumulate_dadb, stream)
         _lib.lobra_rmsnorm_bwd(dh2, x2, self.g_mlp, c["r2"][:T], dx2, dRes=dY, stream=stream)
         L.backward_group("o_in", seq_lens, seq_task, s["att"].view(T, h), {"o": dx2}, d_att, accumulate_dadb, stream)
-        fa._flash_attn_varlen_backward(d_att.view(T, H, D), q.view(T, H, D), k.view(T, H, D), v.view(T, H, D),
-                                       s["att"], s["lse"], dq.view(T, H, D), dk.view(T, H, D), dv.view(T, H, D),
-                                       cu, cu, maxlen, maxlen, 0.0, 1.0 / math.sqrt(D), True, -1, -1, 0.0, None,
-                                       self.deterministic_attn)
+        self.attn.backward(d_att.view(T, H, D), q.view(T, H, D), k.view(T, H, D), v.view(T, H, D), s["att"],
+                           s["lse"], s["actx"], dq.view(T, H, D), dk.view(T, H, D), dv.view(T, H, D))
         _lib.lobra_rope(cu, T, H, D, self.theta, dq, dk, inverse=True, stream=stream)
         L.backward_group("attn", seq_lens, seq_task, h1, {"q": dq, "k": dk, "v": dv}, dh1, accumulate_dadb, stream)
         _lib.lobra_rmsnorm_bwd(dh1, s["X"], self.g_attn, c["r1"][:T], dX, dRes=dx2, stream=stream)

@@ -32,25 +32,27 @@ def _torch():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    try:
-        import flash_attn  # noqa: F401
-    except Exception:
-        pytest.skip("flash_attn unavailable")
     return torch
+
+
+def _backend(name):
+    mod = "cudnn" if name == "cudnn" else "flash_attn"
+    pytest.importorskip(mod)
+    return name
 
 
 def _f64(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def _run(group_inputs=True, seed=0):
+def _run(group_inputs=True, seed=0, backend="flash_attn"):
     torch = _torch()
     from paper_2509_01193_b200.decoder import DecoderLayer
     ranks, scales = [16, 8, 16], [2.0, 0.5, 1.0]
     lens = np.array([1, 300, 57, 129, 200, 33], np.int32)
     tasks = np.array([0, 0, 1, 1, 2, 2], np.int32)
     layer = DecoderLayer(SMALL, n_heads=2, ranks=ranks, scales=scales, seed=seed, group_inputs=group_inputs,
-                         deterministic_attn=True)
+                         deterministic_attn=True, attn_backend=_backend(backend))
     for p in layer.lora.projs:          # B_t ~ N(0, 1/(16 r)): O(1) attention logits (see above)
         p.B.mul_(0.25)
     T = int(lens.sum())
@@ -64,8 +66,9 @@ def _run(group_inputs=True, seed=0):
     return layer, lens, tasks, ranks, scales, X, dY, Y, dX
 
 
-def test_decoder_layer_matches_oracle():
-    layer, lens, tasks, ranks, scales, X, dY, Y, dX = _run()
+@pytest.mark.parametrize("backend", ["cudnn", "flash_attn"])
+def test_decoder_layer_matches_oracle(backend):
+    layer, lens, tasks, ranks, scales, X, dY, Y, dX = _run(backend=backend)
     P = {"g_attn": _f64(layer.g_attn), "g_mlp": _f64(layer.g_mlp)}
     for p in layer.lora.projs:
         P[p.name] = (_f64(p.W), _f64(p.A), _f64(p.B))
@@ -89,7 +92,7 @@ def test_decoder_layer_matches_oracle():
 
 def test_decoder_layer_grouped_equals_ungrouped():
     """The projection-group path and the per-projection path give the same layer
-    (bitwise: deterministic attention, group == single calls)."""
+    (bitwise: deterministic FlashAttention backward, group == single calls)."""
     torch = _torch()
     a = _run(group_inputs=True, seed=3)
     b = _run(group_inputs=False, seed=3)
@@ -97,7 +100,8 @@ def test_decoder_layer_grouped_equals_ungrouped():
     assert torch.equal(a[0].lora.flat_grad, b[0].lora.flat_grad)
 
 
-def test_attention_stage_on_its_own_inputs():
+@pytest.mark.parametrize("backend", ["cudnn", "flash_attn"])
+def test_attention_stage_on_its_own_inputs(backend):
     """The library attention inside the layer (forward and backward) against the oracle
     evaluated on the GPU's own bf16 q / k / v / dO: isolates that stage from the rounding
     of its inputs (valid for any logit scale; the layer here uses the unscaled B_t)."""
@@ -106,7 +110,7 @@ def test_attention_stage_on_its_own_inputs():
     lens = np.array([1, 300, 57, 129, 200, 33], np.int32)
     tasks = np.array([0, 0, 1, 1, 2, 2], np.int32)
     layer = DecoderLayer(SMALL, n_heads=2, ranks=[16, 8, 16], scales=[2.0, 0.5, 1.0], seed=5,
-                         deterministic_attn=True)
+                         deterministic_attn=True, attn_backend=_backend(backend))
     T = int(lens.sum())
     g = torch.Generator(device="cuda")
     g.manual_seed(6)

@@ -52,6 +52,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--fit", action="store_true")
+    ap.add_argument("--attn", default="cudnn", choices=["cudnn", "flash_attn"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_layer_cost.json"))
     args = ap.parse_args()
     import torch
@@ -62,7 +63,7 @@ def main():
     torch.cuda.set_device(0)
     tasks = synth.c2_tasks()
     ranks, scales = [t.rank for t in tasks], [t.scale for t in tasks]
-    layer = DecoderLayer(LLAMA2_7B, n_heads=32, ranks=ranks, scales=scales, seed=11)
+    layer = DecoderLayer(LLAMA2_7B, n_heads=32, ranks=ranks, scales=scales, seed=11, attn_backend=args.attn)
     Tmax = 16384
     g = torch.Generator(device="cuda")
     g.manual_seed(12)
@@ -77,7 +78,8 @@ def main():
     line = {"metric": "Llama-2-7B decoder layer fwd+bwd tokens/s (NEXT-3, 1 GPU)", "value": T / (ms / 1e3),
             "unit": "tokens/s", "ms_per_step": ms, "steps": args.steps, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "C2 (T=16384, 4 tasks r=16, lengths <= 4096)", "layer": "llama2-7b",
-                       "attention": "flash_attn 2.8 varlen (library)"},
+                       "attention": {"cudnn": "cuDNN 9 ragged SDPA (library)",
+                                     "flash_attn": "flash_attn 2.8 varlen (library)"}[args.attn]},
             "algorithmic_tflops": fl["total"] / (ms / 1e3) / 1e12,
             "flops_share": {k: fl[k] / fl["total"] for k in ("proj", "lora", "attn")},
             "ms_by_class": cls, "ms_attention_and_glue": ms - ours}
@@ -107,6 +109,7 @@ def main():
         c, *_ = np.linalg.lstsq(A[m], y[m], rcond=None)
         loo.append(abs(A[i] @ c - y[i]) / y[i])
     res = {"model": "t_ms = c0 + c1 * b s + c2 * b s^2 (App. D P:1485, one 7B layer fwd+bwd, 1 B200)",
+           "attention": args.attn,
            "c0_ms": coef[0], "c1_ms_per_token": coef[1], "c2_ms_per_token_len": coef[2],
            "points": pts, "fit_rel_err": [abs(A[i] @ coef - y[i]) / y[i] for i in range(len(pts))],
            "loo_rel_err_max": max(loo), "loo_rel_err_mean": float(np.mean(loo)), "c2_layer_line": line,
