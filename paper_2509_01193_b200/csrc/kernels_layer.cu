@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "common.h"
 
@@ -48,16 +49,21 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // One CTA per row; the row stays in registers between the reduction and the output.
-__global__ void k_rmsnorm_fwd(int h, const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ R,
-                              __nv_bfloat16* __restrict__ S_out, const __nv_bfloat16* __restrict__ g, float eps,
-                              __nv_bfloat16* __restrict__ Y, float* __restrict__ rstd) {
+// VPT = 16-byte vectors per thread (h = 8 * VPT * blockDim): a small VPT keeps the
+// register file (and so the rows in flight per SM) large.
+template <int VPT>
+__global__ void __launch_bounds__(1024) k_rmsnorm_fwd(int h, const __nv_bfloat16* __restrict__ X,
+                                                      const __nv_bfloat16* __restrict__ R,
+                                                      __nv_bfloat16* __restrict__ S_out,
+                                                      const __nv_bfloat16* __restrict__ g, float eps,
+                                                      __nv_bfloat16* __restrict__ Y, float* __restrict__ rstd) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const int nv = h / 8;
-  float s[kMaxVec][8];
+  float s[VPT][8];
   float ss = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
+  for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
     if (c < nv) {
       unpack8(__ldg(reinterpret_cast<const uint4*>(X + row * h) + c), s[k]);
@@ -75,7 +81,7 @@ __global__ void k_rmsnorm_fwd(int h, const __nv_bfloat16* __restrict__ X, const 
   const float rs = rsqrtf(block_sum(ss, red) / (float)h + eps);
   if (threadIdx.x == 0) rstd[row] = rs;
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
+  for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
     if (c < nv) {
       float gg[8], y[8];
@@ -87,16 +93,20 @@ __global__ void k_rmsnorm_fwd(int h, const __nv_bfloat16* __restrict__ X, const 
   }
 }
 
-__global__ void k_rmsnorm_bwd(int h, const __nv_bfloat16* __restrict__ dY, const __nv_bfloat16* __restrict__ S,
-                              const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
-                              const __nv_bfloat16* __restrict__ dRes, __nv_bfloat16* __restrict__ dS) {
+template <int VPT>
+__global__ void __launch_bounds__(1024) k_rmsnorm_bwd(int h, const __nv_bfloat16* __restrict__ dY,
+                                                      const __nv_bfloat16* __restrict__ S,
+                                                      const __nv_bfloat16* __restrict__ g,
+                                                      const float* __restrict__ rstd,
+                                                      const __nv_bfloat16* __restrict__ dRes,
+                                                      __nv_bfloat16* __restrict__ dS) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const int nv = h / 8;
-  float u[kMaxVec][8], x[kMaxVec][8];
+  float u[VPT][8], x[VPT][8];
   float dot = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
+  for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
     if (c < nv) {
       float gg[8];
@@ -113,7 +123,7 @@ __global__ void k_rmsnorm_bwd(int h, const __nv_bfloat16* __restrict__ dY, const
   const float r = rstd[row];
   const float coef = block_sum(dot, red) * r * r * r / (float)h;
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
+  for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
     if (c < nv) {
       float o[8];
@@ -130,18 +140,20 @@ __global__ void k_rmsnorm_bwd(int h, const __nv_bfloat16* __restrict__ dY, const
   }
 }
 
-// One thread per (token, head, 8 consecutive pair indices j).
+// One thread per (token, 8 consecutive pair indices j, group of kRopeHG heads): the 8
+// (cos, sin) pairs are computed once and applied to the group's heads of Q and K; the loads
+// of 4 heads are issued before their stores so the read-modify-writes overlap.
+constexpr int kRopeHG = 8;
 __global__ void k_rope(int num_seqs, const int32_t* __restrict__ cu, long long T, int nh, int D, float log2theta,
                        __nv_bfloat16* __restrict__ Q, long long ldq, __nv_bfloat16* __restrict__ K, long long ldk,
                        float sign) {
-  const int half = D / 2, per_head = half / 8;
-  const long long total = T * nh * per_head;
+  const int half = D / 2, per_tok = half / 8, ngrp = (nh + kRopeHG - 1) / kRopeHG;
+  const long long total = T * per_tok * ngrp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int jv = (int)(i % per_head);
-    const long long th = i / per_head;
-    const int hd = (int)(th % nh);
-    const long long tok = th / nh;
+    const int jv = (int)(i % per_tok);
+    const int hg = (int)((i / per_tok) % ngrp);
+    const long long tok = i / ((long long)per_tok * ngrp);
     int lo = 0, hi = num_seqs - 1;   // last sequence with cu[s] <= tok
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -156,21 +168,33 @@ __global__ void k_rope(int num_seqs, const int32_t* __restrict__ cu, long long T
       sincosf(pos * inv, &s[e], &c[e]);
       s[e] *= sign;
     }
+    const int h0 = hg * kRopeHG, h1 = min(nh, h0 + kRopeHG);
     for (int which = 0; which < 2; ++which) {
       __nv_bfloat16* base = which == 0 ? Q + tok * ldq : (K ? K + tok * ldk : nullptr);
       if (!base) continue;
-      uint4* pa = reinterpret_cast<uint4*>(base + hd * D) + jv;
-      uint4* pb = reinterpret_cast<uint4*>(base + hd * D + half) + jv;
-      float a[8], b[8], oa[8], ob[8];
-      unpack8(*pa, a);
-      unpack8(*pb, b);
+      for (int hb = h0; hb < h1; hb += 4) {
+        uint4 ua[4], ub[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        oa[e] = a[e] * c[e] - b[e] * s[e];
-        ob[e] = b[e] * c[e] + a[e] * s[e];
+        for (int u = 0; u < 4; ++u)
+          if (hb + u < h1) {
+            ua[u] = reinterpret_cast<const uint4*>(base + (hb + u) * D)[jv];
+            ub[u] = reinterpret_cast<const uint4*>(base + (hb + u) * D + half)[jv];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (hb + u < h1) {
+            float a[8], b[8], oa[8], ob[8];
+            unpack8(ua[u], a);
+            unpack8(ub[u], b);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              oa[e] = a[e] * c[e] - b[e] * s[e];
+              ob[e] = b[e] * c[e] + a[e] * s[e];
+            }
+            reinterpret_cast<uint4*>(base + (hb + u) * D)[jv] = pack8(oa);
+            reinterpret_cast<uint4*>(base + (hb + u) * D + half)[jv] = pack8(ob);
+          }
       }
-      *pa = pack8(oa);
-      *pb = pack8(ob);
     }
   }
 }
@@ -232,10 +256,27 @@ lobra_status done(const char* what) {
   return LOBRA_OK;
 }
 
-// threads per row: ~4 vectors each, a multiple of 32, at most 256 (h <= 256 * 8 * kMaxVec)
-int row_threads(int64_t h) {
-  const int t = (int)((h / 8 + 3) / 4 + 31) / 32 * 32;
-  return t < 32 ? 32 : (t > 256 ? 256 : t);
+// Row kernels: VPT vectors per thread with blockDim = ceil(h / 8 / VPT) rounded to 32,
+// VPT the smallest of {1, 2, 4, 8} keeping blockDim <= 256.
+int row_vpt(int64_t h) {
+  const int64_t nv = h / 8;
+  for (int v : {1, 2, 4, 8})
+    if ((nv + v - 1) / v <= 256) return v;
+  return kMaxVec;
+}
+int row_threads(int64_t h, int vpt) {
+  const int t = (int)(((h / 8 + vpt - 1) / vpt + 31) / 32 * 32);
+  return t < 32 ? 32 : t;
+}
+
+template <typename F>
+void dispatch_vpt(int vpt, F&& f) {
+  switch (vpt) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    default: f(std::integral_constant<int, 8>{}); break;
+  }
 }
 
 }  // namespace
@@ -254,11 +295,13 @@ extern "C" lobra_status lobra_rmsnorm_fwd(int64_t T, int64_t h, const void* X, c
   if (T == 0) return LOBRA_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   count_launch(LOBRA_K_LAYER, st, true);
-  k_rmsnorm_fwd<<<(unsigned)T, row_threads(h), 0, st>>>((int)h, static_cast<const __nv_bfloat16*>(X),
-                                                         static_cast<const __nv_bfloat16*>(R),
-                                                         static_cast<__nv_bfloat16*>(S_out),
-                                                         static_cast<const __nv_bfloat16*>(g), eps,
-                                                         static_cast<__nv_bfloat16*>(Y), rstd);
+  const int vpt = row_vpt(h);
+  dispatch_vpt(vpt, [&](auto V) {
+    k_rmsnorm_fwd<decltype(V)::value><<<(unsigned)T, row_threads(h, vpt), 0, st>>>(
+        (int)h, static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(R),
+        static_cast<__nv_bfloat16*>(S_out), static_cast<const __nv_bfloat16*>(g), eps,
+        static_cast<__nv_bfloat16*>(Y), rstd);
+  });
   count_launch(LOBRA_K_LAYER, st, false);
   return done("lobra_rmsnorm_fwd");
 }
@@ -273,11 +316,13 @@ extern "C" lobra_status lobra_rmsnorm_bwd(int64_t T, int64_t h, const void* dY, 
   if (T == 0) return LOBRA_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   count_launch(LOBRA_K_LAYER, st, true);
-  k_rmsnorm_bwd<<<(unsigned)T, row_threads(h), 0, st>>>((int)h, static_cast<const __nv_bfloat16*>(dY),
-                                                         static_cast<const __nv_bfloat16*>(S),
-                                                         static_cast<const __nv_bfloat16*>(g), rstd,
-                                                         static_cast<const __nv_bfloat16*>(dRes),
-                                                         static_cast<__nv_bfloat16*>(dS));
+  const int vpt = row_vpt(h);
+  dispatch_vpt(vpt, [&](auto V) {
+    k_rmsnorm_bwd<decltype(V)::value><<<(unsigned)T, row_threads(h, vpt), 0, st>>>(
+        (int)h, static_cast<const __nv_bfloat16*>(dY), static_cast<const __nv_bfloat16*>(S),
+        static_cast<const __nv_bfloat16*>(g), rstd, static_cast<const __nv_bfloat16*>(dRes),
+        static_cast<__nv_bfloat16*>(dS));
+  });
   count_launch(LOBRA_K_LAYER, st, false);
   return done("lobra_rmsnorm_bwd");
 }
@@ -294,7 +339,7 @@ extern "C" lobra_status lobra_rope(int32_t num_seqs, const int32_t* cu_seqlens, 
   if (T == 0) return LOBRA_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   count_launch(LOBRA_K_LAYER, st, true);
-  const long long total = T * n_heads * (head_dim / 16);
+  const long long total = T * (head_dim / 16) * ((n_heads + 7) / 8);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 16LL * sm_count());
   k_rope<<<blocks, 256, 0, st>>>(num_seqs, cu_seqlens, T, n_heads, head_dim, std::log2(theta),
                                  static_cast<__nv_bfloat16*>(Q), ldq, static_cast<__nv_bfloat16*>(K), ldk,
