@@ -63,10 +63,17 @@ def rope(x, pos, theta, inverse=False):
     return np.concatenate([a * c - b * s, b * c + a * s], axis=-1)
 
 
+def _kv_heads(x, H):
+    """Grouped-query attention (Llama-2-70B): query head i reads kv head i // (H / H_kv)."""
+    return np.repeat(x, H // x.shape[1], axis=1)
+
+
 def attention(q, k, v, seq_lens):
-    """Causal softmax attention inside every packed sequence; q, k, v [T, H, D].
-    Returns (O [T, H, D], P list per sequence [H, n, n])."""
+    """Causal softmax attention inside every packed sequence; q [T, H, D], k, v [T, H_kv, D]
+    with H_kv | H (H_kv = H: multi-head).  Returns (O [T, H, D], P list per sequence
+    [H, n, n])."""
     q, k, v = (np.asarray(a, np.float64) for a in (q, k, v))
+    k, v = _kv_heads(k, q.shape[1]), _kv_heads(v, q.shape[1])
     D = q.shape[-1]
     O = np.zeros_like(q)
     Ps = []
@@ -87,8 +94,11 @@ def attention(q, k, v, seq_lens):
 
 def attention_bwd(dO, q, k, v, Ps, seq_lens):
     """dV = P^T dO; dP = dO V^T; dS = P * (dP - rowsum(dP * P)); dQ = dS K / sqrt(D);
-    dK = dS^T Q / sqrt(D)  (per sequence and head)."""
+    dK = dS^T Q / sqrt(D)  (per sequence and query head; with grouped kv heads the dK, dV
+    of a kv head sum over the query heads that read it)."""
     dO, q, k, v = (np.asarray(a, np.float64) for a in (dO, q, k, v))
+    Hkv = k.shape[1]
+    k, v = _kv_heads(k, q.shape[1]), _kv_heads(v, q.shape[1])
     D = q.shape[-1]
     dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
     off = 0
@@ -103,7 +113,9 @@ def attention_bwd(dO, q, k, v, Ps, seq_lens):
         dk[sl] = (dS.transpose(0, 2, 1) @ qs / np.sqrt(D)).transpose(1, 0, 2)
         dv[sl] = dV.transpose(1, 0, 2)
         off += n
-    return dq, dk, dv
+    T, H = dk.shape[0], dk.shape[1]
+    g = H // Hkv
+    return dq, dk.reshape(T, Hkv, g, D).sum(axis=2), dv.reshape(T, Hkv, g, D).sum(axis=2)
 
 
 def silu(x):
@@ -125,8 +137,8 @@ def swiglu_bwd(d, gate, up):
 # ------------------------------------------------------------------ the layer
 def layer_fwd(X, P, cfg, ranks, scales, seq_lens, seq_task):
     """One Llama decoder layer over the packed batch X [T, h].  P: dict with g_attn,
-    g_mlp and, per projection p, (W_p, A_p, B_p).  cfg: n_heads, eps, theta.
-    Returns (Y, cache)."""
+    g_mlp and, per projection p, (W_p, A_p, B_p).  cfg: n_heads, eps, theta (n_kv_heads:
+    from the k projection's width).  Returns (Y, cache)."""
     H, eps, theta = cfg["n_heads"], cfg["eps"], cfg["theta"]
     X = np.asarray(X, np.float64)
     T, h = X.shape
@@ -134,10 +146,11 @@ def layer_fwd(X, P, cfg, ranks, scales, seq_lens, seq_task):
     lo = lambda Z, p: L.lora_fwd(Z, P[p][0], P[p][1], P[p][2], ranks, scales, seq_lens, seq_task)
     h1, _ = rmsnorm(X, P["g_attn"], eps)
     q, k, v = lo(h1, "q"), lo(h1, "k"), lo(h1, "v")
+    Hkv = k.shape[1] // D
     pos = positions(seq_lens)
     qr = rope(q.reshape(T, H, D), pos, theta)
-    kr = rope(k.reshape(T, H, D), pos, theta)
-    vv = v.reshape(T, H, D)
+    kr = rope(k.reshape(T, Hkv, D), pos, theta)
+    vv = v.reshape(T, Hkv, D)
     att, Ps = attention(qr, kr, vv, seq_lens)
     att = att.reshape(T, h)
     o = lo(att, "o")
@@ -173,7 +186,7 @@ def layer_bwd(dY, P, cfg, ranks, scales, seq_lens, seq_task, cache):
     d_att = lb(c["att"], "o", dx2)
     dqr, dkr, dv = attention_bwd(d_att.reshape(T, H, D), c["qr"], c["kr"], c["vv"], c["Ps"], seq_lens)
     dq = rope(dqr, c["pos"], theta, inverse=True).reshape(T, h)
-    dk = rope(dkr, c["pos"], theta, inverse=True).reshape(T, h)
-    dh1 = lb(c["h1"], "q", dq) + lb(c["h1"], "k", dk) + lb(c["h1"], "v", dv.reshape(T, h))
+    dk = rope(dkr, c["pos"], theta, inverse=True).reshape(T, -1)
+    dh1 = lb(c["h1"], "q", dq) + lb(c["h1"], "k", dk) + lb(c["h1"], "v", dv.reshape(T, -1))
     dX = dx2 + rmsnorm_bwd(dh1, c["X"], P["g_attn"], eps)      # X feeds x2 and h1
     return dX, grads

@@ -23,10 +23,11 @@ def _bucket(x: int, q: int) -> int:
 
 
 class CudnnVarlenAttention:
-    def __init__(self, n_heads: int, head_dim: int, device):
+    def __init__(self, n_heads: int, head_dim: int, device, n_kv_heads: int | None = None):
         import cudnn
         self.cudnn = cudnn
         self.H, self.D = n_heads, head_dim
+        self.Hkv = n_kv_heads or n_heads      # grouped-query attention when < n_heads
         self.dev = torch.device(device)
         self.handle = cudnn.create_handle()
         self.graphs = {}
@@ -38,21 +39,22 @@ class CudnnVarlenAttention:
         if key in self.graphs:
             return self.graphs[key]
         c = self.cudnn
-        H, D = self.H, self.D
+        H, Hk, D = self.H, self.Hkv, self.D
         g = c.pygraph(io_data_type=c.data_type.BFLOAT16, intermediate_data_type=c.data_type.FLOAT,
                       compute_data_type=c.data_type.FLOAT, handle=self.handle)
         dim, stride = [B, H, S, D], [S * H * D, D, H * D, 1]
+        dimk, stridek = [B, Hk, S, D], [S * Hk * D, D, Hk * D, 1]
 
-        def ragged(name):
+        def ragged(name, kv=False):
             off = g.tensor(name=name + "_off", dim=[B + 1, 1, 1, 1], stride=[1, 1, 1, 1],
                            data_type=c.data_type.INT32)
-            return g.tensor(name=name, dim=dim, stride=stride, data_type=c.data_type.BFLOAT16,
-                            ragged_offset=off), off
+            return g.tensor(name=name, dim=dimk if kv else dim, stride=stridek if kv else stride,
+                            data_type=c.data_type.BFLOAT16, ragged_offset=off), off
 
         t = {}
         t["q"], t["q_off"] = ragged("q")
-        t["k"], t["k_off"] = ragged("k")
-        t["v"], t["v_off"] = ragged("v")
+        t["k"], t["k_off"] = ragged("k", True)
+        t["v"], t["v_off"] = ragged("v", True)
         t["sq"] = g.tensor(name="seq_q", dim=[B, 1, 1, 1], stride=[1, 1, 1, 1], data_type=c.data_type.INT32)
         t["skv"] = g.tensor(name="seq_kv", dim=[B, 1, 1, 1], stride=[1, 1, 1, 1], data_type=c.data_type.INT32)
         scale = 1.0 / math.sqrt(D)
@@ -75,7 +77,9 @@ class CudnnVarlenAttention:
             for n, x in (("dq", dq), ("dk", dk), ("dv", dv)):
                 t[n + "_off"] = g.tensor(name=n + "_off", dim=[B + 1, 1, 1, 1], stride=[1, 1, 1, 1],
                                          data_type=c.data_type.INT32)
-                x.set_output(True).set_dim(dim).set_stride(stride).set_ragged_offset(t[n + "_off"])
+                kv = n != "dq"
+                x.set_output(True).set_dim(dimk if kv else dim).set_stride(stridek if kv else stride) \
+                    .set_ragged_offset(t[n + "_off"])
                 t[n] = x
         g.validate()
         g.build_operation_graph()
@@ -94,8 +98,9 @@ class CudnnVarlenAttention:
         lens[:n] = seq_lens
         cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
         off = torch.from_numpy((cu * self.H * self.D).astype(np.int32)).to(self.dev).view(B + 1, 1, 1, 1)
+        offk = torch.from_numpy((cu * self.Hkv * self.D).astype(np.int32)).to(self.dev).view(B + 1, 1, 1, 1)
         sl = torch.from_numpy(lens).to(self.dev).view(B, 1, 1, 1)
-        return B, S, off, sl
+        return B, S, (off, offk), sl
 
     def _run(self, g, pack):
         need = g.get_workspace_size()
@@ -107,20 +112,20 @@ class CudnnVarlenAttention:
     # -------------------------------------------------------------- public
     def forward(self, q, k, v, seq_lens):
         """q, k, v [T, H, D] bf16 -> (o [T, H, D], stats [B, H, S, 1] fp32, ctx)."""
-        B, S, off, sl = self._meta(seq_lens)
+        B, S, (off, offk), sl = self._meta(seq_lens)
         g, t = self._graph("fwd", B, S)
         o = torch.empty_like(q)
         stats = torch.empty(B, self.H, S, 1, dtype=torch.float32, device=self.dev)
         self._run(g, {t["q"]: q, t["k"]: k, t["v"]: v, t["o"]: o, t["stats"]: stats, t["q_off"]: off,
-                      t["k_off"]: off, t["v_off"]: off, t["o_off"]: off, t["sq"]: sl, t["skv"]: sl})
-        return o, stats, (B, S, off, sl)
+                      t["k_off"]: offk, t["v_off"]: offk, t["o_off"]: off, t["sq"]: sl, t["skv"]: sl})
+        return o, stats, (B, S, (off, offk), sl)
 
     def backward(self, dO, q, k, v, o, stats, ctx, dq, dk, dv):
-        B, S, off, sl = ctx
+        B, S, (off, offk), sl = ctx
         g, t = self._graph("bwd", B, S)
         self._run(g, {t["q"]: q, t["k"]: k, t["v"]: v, t["o"]: o, t["dO"]: dO, t["stats"]: stats,
-                      t["dq"]: dq, t["dk"]: dk, t["dv"]: dv, t["q_off"]: off, t["k_off"]: off, t["v_off"]: off,
-                      t["o_off"]: off, t["dO_off"]: off, t["dq_off"]: off, t["dk_off"]: off, t["dv_off"]: off,
+                      t["dq"]: dq, t["dk"]: dk, t["dv"]: dv, t["q_off"]: off, t["k_off"]: offk, t["v_off"]: offk,
+                      t["o_off"]: off, t["dO_off"]: off, t["dq_off"]: off, t["dk_off"]: offk, t["dv_off"]: offk,
                       t["sq"]: sl, t["skv"]: sl})
 
 
@@ -144,9 +149,11 @@ class FlashVarlenAttention:
                                             1.0 / math.sqrt(self.D), True, -1, -1, 0.0, None, self.det)
 
 
-def make_attention(backend: str, n_heads: int, head_dim: int, device, deterministic=False):
+def make_attention(backend: str, n_heads: int, head_dim: int, device, deterministic=False,
+                   n_kv_heads: int | None = None):
+    """q [T, n_heads, D]; k, v [T, n_kv_heads, D] (grouped-query attention when fewer)."""
     if backend == "cudnn":
-        return CudnnVarlenAttention(n_heads, head_dim, device)
+        return CudnnVarlenAttention(n_heads, head_dim, device, n_kv_heads)
     if backend == "flash_attn":
         return FlashVarlenAttention(n_heads, head_dim, device, deterministic)
     raise ValueError(f"unknown attention backend {backend!r}")

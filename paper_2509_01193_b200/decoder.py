@@ -36,8 +36,11 @@ class DecoderLayer:
         self.f = next(p.d_out for p in self.lora.projs if p.name == "gate")
         self.n_heads = n_heads
         self.head_dim = self.h // n_heads
+        self.hk = next(p.d_out for p in self.lora.projs if p.name == "k")    # kv width
+        self.n_kv_heads = self.hk // self.head_dim      # < n_heads: grouped-query attention (70B)
         self.eps, self.theta = eps, theta
-        self.attn = make_attention(attn_backend, n_heads, self.head_dim, self.dev, deterministic_attn)
+        self.attn = make_attention(attn_backend, n_heads, self.head_dim, self.dev, deterministic_attn,
+                                   self.n_kv_heads)
         g = torch.Generator(device=self.dev)
         g.manual_seed(seed + 7)
         # frozen RMSNorm gains (synthetic: 1 + N(0, 0.1^2))
@@ -59,22 +62,26 @@ class DecoderLayer:
         """X [T, h] bf16 (device) -> Y [T, h]; keeps the activations for backward()."""
         seq_lens = np.asarray(seq_lens, np.int32)
         seq_task = np.asarray(seq_task, np.int32)
-        T, h, f = int(seq_lens.sum()), self.h, self.f
-        H, D = self.n_heads, self.head_dim
+        T, h, f, hk = int(seq_lens.sum()), self.h, self.f, self.hk
+        H, D, Hk = self.n_heads, self.head_dim, self.n_kv_heads
         L = self.lora
         L.ensure(seq_lens, seq_task)
         cu = torch.from_numpy(np.concatenate([[0], np.cumsum(seq_lens)]).astype(np.int32)).to(self.dev)
         maxlen = int(seq_lens.max()) if len(seq_lens) else 0
         b = self._buf
         h1, x2, h2 = b("h1", (T, h)), b("x2", (T, h)), b("h2", (T, h))
-        q, k, v, o = b("q", (T, h)), b("k", (T, h)), b("v", (T, h)), b("o", (T, h))
+        q, k, v, o = b("q", (T, h)), b("k", (T, hk)), b("v", (T, hk)), b("o", (T, h))
         gate, up, act, down = b("gate", (T, f)), b("up", (T, f)), b("act", (T, f)), b("down", (T, h))
         r1, r2 = b("r1", (T,), torch.float32), b("r2", (T,), torch.float32)
         Y = b("Y", (T, h))
         _lib.lobra_rmsnorm_fwd(X, self.g_attn, self.eps, h1, r1, stream=stream)
         L.forward_group("attn", seq_lens, seq_task, h1, {"q": q, "k": k, "v": v}, stream)
-        _lib.lobra_rope(cu, T, H, D, self.theta, q, k, stream=stream)
-        att, lse, actx = self.attn.forward(q.view(T, H, D), k.view(T, H, D), v.view(T, H, D), seq_lens)
+        if Hk == H:
+            _lib.lobra_rope(cu, T, H, D, self.theta, q, k, stream=stream)
+        else:
+            _lib.lobra_rope(cu, T, H, D, self.theta, q, stream=stream)
+            _lib.lobra_rope(cu, T, Hk, D, self.theta, k, stream=stream)
+        att, lse, actx = self.attn.forward(q.view(T, H, D), k.view(T, Hk, D), v.view(T, Hk, D), seq_lens)
         L.forward_group("o_in", seq_lens, seq_task, att.view(T, h), {"o": o}, stream)
         _lib.lobra_rmsnorm_fwd(X, self.g_mlp, self.eps, h2, r2, R=o, S_out=x2, stream=stream)
         L.forward_group("mlp", seq_lens, seq_task, h2, {"gate": gate, "up": up}, stream)
@@ -90,15 +97,15 @@ class DecoderLayer:
         """dY [T, h] -> dX [T, h]; adapter gradients (+)= into self.lora.flat_grad."""
         s = self.saved
         seq_lens, seq_task, cu, maxlen, T = s["seq_lens"], s["seq_task"], s["cu"], s["maxlen"], s["T"]
-        h, f, H, D = self.h, self.f, self.n_heads, self.head_dim
+        h, f, H, D, hk, Hk = self.h, self.f, self.n_heads, self.head_dim, self.hk, self.n_kv_heads
         L = self.lora
         b = self._buf
         c = self.cache
         d_act, d_gate, d_up = b("d_act", (T, f)), b("d_gate", (T, f)), b("d_up", (T, f))
         dh2, dx2, d_att, dh1 = b("dh2", (T, h)), b("dx2", (T, h)), b("d_att", (T, h)), b("dh1", (T, h))
-        dq, dk, dv = b("dq", (T, h)), b("dk", (T, h)), b("dv", (T, h))
+        dq, dk, dv = b("dq", (T, h)), b("dk", (T, hk)), b("dv", (T, hk))
         dX = b("dX", (T, h))
-        q, k, v = c["q"][:T * h].view(T, h), c["k"][:T * h].view(T, h), c["v"][:T * h].view(T, h)
+        q, k, v = c["q"][:T * h].view(T, h), c["k"][:T * hk].view(T, hk), c["v"][:T * hk].view(T, hk)
         gate, up = c["gate"][:T * f].view(T, f), c["up"][:T * f].view(T, f)
         act, h2, x2, h1 = (c[n][:T * w].view(T, w) for n, w in (("act", f), ("h2", h), ("x2", h), ("h1", h)))
         L.backward_group("down_in", seq_lens, seq_task, act, {"down": dY}, d_act, accumulate_dadb, stream)
@@ -106,9 +113,13 @@ class DecoderLayer:
         L.backward_group("mlp", seq_lens, seq_task, h2, {"gate": d_gate, "up": d_up}, dh2, accumulate_dadb, stream)
         _lib.lobra_rmsnorm_bwd(dh2, x2, self.g_mlp, c["r2"][:T], dx2, dRes=dY, stream=stream)
         L.backward_group("o_in", seq_lens, seq_task, s["att"].view(T, h), {"o": dx2}, d_att, accumulate_dadb, stream)
-        self.attn.backward(d_att.view(T, H, D), q.view(T, H, D), k.view(T, H, D), v.view(T, H, D), s["att"],
-                           s["lse"], s["actx"], dq.view(T, H, D), dk.view(T, H, D), dv.view(T, H, D))
-        _lib.lobra_rope(cu, T, H, D, self.theta, dq, dk, inverse=True, stream=stream)
+        self.attn.backward(d_att.view(T, H, D), q.view(T, H, D), k.view(T, Hk, D), v.view(T, Hk, D), s["att"],
+                           s["lse"], s["actx"], dq.view(T, H, D), dk.view(T, Hk, D), dv.view(T, Hk, D))
+        if Hk == H:
+            _lib.lobra_rope(cu, T, H, D, self.theta, dq, dk, inverse=True, stream=stream)
+        else:
+            _lib.lobra_rope(cu, T, H, D, self.theta, dq, inverse=True, stream=stream)
+            _lib.lobra_rope(cu, T, Hk, D, self.theta, dk, inverse=True, stream=stream)
         L.backward_group("attn", seq_lens, seq_task, h1, {"q": dq, "k": dk, "v": dv}, dh1, accumulate_dadb, stream)
         _lib.lobra_rmsnorm_bwd(dh1, s["X"], self.g_attn, c["r1"][:T], dX, dRes=dx2, stream=stream)
         return dX
@@ -122,5 +133,5 @@ class DecoderLayer:
         r = float(np.mean(self.lora.ranks))
         lora = 6 * T * r * sum(p.d_in + p.d_out for p in self.lora.projs)
         s2 = float(np.sum(np.asarray(seq_lens, np.float64) ** 2)) / 2
-        att_f = 4 * s2 * self.h
+        att_f = 4 * s2 * self.h          # per query head (GQA shares k, v but not the matmuls)
         return {"proj": proj, "lora": lora, "attn": att_f * 3.5, "total": proj + lora + att_f * 3.5}

@@ -28,6 +28,13 @@ SMALL = [("q", 256, 256, "col", "attn"), ("k", 256, 256, "col", "attn"), ("v", 2
          ("down", 512, 256, "row", "down_in")]
 
 
+# grouped-query attention (Llama-2-70B style): 4 query heads of 64, 2 kv heads (k, v: 256 -> 128)
+SMALL_GQA = [("q", 256, 256, "col", "attn"), ("k", 256, 128, "col", "attn"), ("v", 256, 128, "col", "attn"),
+             ("o", 256, 256, "row", "o_in"), ("gate", 256, 512, "col", "mlp"), ("up", 256, 512, "col", "mlp"),
+             ("down", 512, 256, "row", "down_in")]
+ARCH = {"mha": (SMALL, 2), "gqa": (SMALL_GQA, 4)}
+
+
 def _torch():
     import torch
     if not torch.cuda.is_available():
@@ -45,13 +52,14 @@ def _f64(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def _run(group_inputs=True, seed=0, backend="flash_attn"):
+def _run(group_inputs=True, seed=0, backend="flash_attn", arch="mha"):
     torch = _torch()
+    shapes, heads = ARCH[arch]
     from paper_2509_01193_b200.decoder import DecoderLayer
     ranks, scales = [16, 8, 16], [2.0, 0.5, 1.0]
     lens = np.array([1, 300, 57, 129, 200, 33], np.int32)
     tasks = np.array([0, 0, 1, 1, 2, 2], np.int32)
-    layer = DecoderLayer(SMALL, n_heads=2, ranks=ranks, scales=scales, seed=seed, group_inputs=group_inputs,
+    layer = DecoderLayer(shapes, n_heads=heads, ranks=ranks, scales=scales, seed=seed, group_inputs=group_inputs,
                          deterministic_attn=True, attn_backend=_backend(backend))
     for p in layer.lora.projs:          # B_t ~ N(0, 1/(16 r)): O(1) attention logits (see above)
         p.B.mul_(0.25)
@@ -66,13 +74,14 @@ def _run(group_inputs=True, seed=0, backend="flash_attn"):
     return layer, lens, tasks, ranks, scales, X, dY, Y, dX
 
 
+@pytest.mark.parametrize("arch", ["mha", "gqa"])
 @pytest.mark.parametrize("backend", ["cudnn", "flash_attn"])
-def test_decoder_layer_matches_oracle(backend):
-    layer, lens, tasks, ranks, scales, X, dY, Y, dX = _run(backend=backend)
+def test_decoder_layer_matches_oracle(backend, arch):
+    layer, lens, tasks, ranks, scales, X, dY, Y, dX = _run(backend=backend, arch=arch)
     P = {"g_attn": _f64(layer.g_attn), "g_mlp": _f64(layer.g_mlp)}
     for p in layer.lora.projs:
         P[p.name] = (_f64(p.W), _f64(p.A), _f64(p.B))
-    cfg = {"n_heads": 2, "eps": layer.eps, "theta": layer.theta}
+    cfg = {"n_heads": layer.n_heads, "eps": layer.eps, "theta": layer.theta}
     Yo, cache = Dd.layer_fwd(_f64(X), P, cfg, ranks, scales, lens, tasks)
     dXo, grads = Dd.layer_bwd(_f64(dY), P, cfg, ranks, scales, lens, tasks, cache)
     errs = {"Y": O.max_rel_err(_f64(Y), Yo), "dX": O.max_rel_err(_f64(dX), dXo)}

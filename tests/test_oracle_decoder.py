@@ -23,11 +23,11 @@ SHAPES = {"q": (H_, H_), "k": (H_, H_), "v": (H_, H_), "o": (H_, H_), "gate": (H
           "down": (F_, H_)}
 
 
-def _params(seed, ranks, zero_B=False):
+def _params(seed, ranks, zero_B=False, shapes=None):
     rng = np.random.default_rng(seed)
     R = int(sum(ranks))
     P = {"g_attn": 1.0 + 0.1 * rng.standard_normal(H_), "g_mlp": 1.0 + 0.1 * rng.standard_normal(H_)}
-    for p, (i, o) in SHAPES.items():
+    for p, (i, o) in (shapes or SHAPES).items():
         W = rng.standard_normal((o, i)) / np.sqrt(i)
         A = rng.standard_normal((R, i)) / np.sqrt(i)
         B = np.zeros((o, R)) if zero_B else rng.standard_normal((o, R)) / 2
@@ -38,20 +38,26 @@ def _params(seed, ranks, zero_B=False):
 BATCH = dict(ranks=[2, 3], scales=[1.5, 0.5], seq_lens=np.array([3, 5, 2]), seq_task=np.array([0, 1, 0]))
 
 
+# grouped-query attention (Llama-2-70B style): 2 query heads share 1 kv head (k, v: 16 -> 8)
+GQA = dict(SHAPES, k=(H_, H_ // 2), v=(H_, H_ // 2))
+
+
 def _run(P, X, b=BATCH):
     return Dd.layer_fwd(X, P, CFG, b["ranks"], b["scales"], b["seq_lens"], b["seq_task"])
 
 
-def test_matches_hf_llama_layer_with_zero_lora():
+@pytest.mark.parametrize("kv_heads", [2, 1])
+def test_matches_hf_llama_layer_with_zero_lora(kv_heads):
+    """MHA (Llama-2-7B) and grouped-query attention (Llama-2-70B: kv heads shared)."""
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
     from transformers.models.llama import modeling_llama as M
-    cfg = tr.LlamaConfig(hidden_size=H_, intermediate_size=F_, num_attention_heads=2, num_key_value_heads=2,
+    cfg = tr.LlamaConfig(hidden_size=H_, intermediate_size=F_, num_attention_heads=2, num_key_value_heads=kv_heads,
                          rms_norm_eps=CFG["eps"], rope_theta=CFG["theta"], attention_bias=False, mlp_bias=False)
     cfg._attn_implementation = "eager"
     layer = M.LlamaDecoderLayer(cfg, 0).double()
     rot = M.LlamaRotaryEmbedding(cfg).double()
-    P = _params(1, BATCH["ranks"], zero_B=True)
+    P = _params(1, BATCH["ranks"], zero_B=True, shapes=SHAPES if kv_heads == 2 else GQA)
     names = {"q": "self_attn.q_proj", "k": "self_attn.k_proj", "v": "self_attn.v_proj", "o": "self_attn.o_proj",
              "gate": "mlp.gate_proj", "up": "mlp.up_proj", "down": "mlp.down_proj"}
     sd = {f"{names[p]}.weight": torch.from_numpy(P[p][0]) for p in names}
@@ -74,8 +80,9 @@ def test_matches_hf_llama_layer_with_zero_lora():
         off += n
 
 
-def test_backward_equals_finite_differences():
-    P = _params(3, BATCH["ranks"])
+@pytest.mark.parametrize("shapes", [SHAPES, GQA], ids=["mha", "gqa"])
+def test_backward_equals_finite_differences(shapes):
+    P = _params(3, BATCH["ranks"], shapes=shapes)
     rng = np.random.default_rng(4)
     T = int(BATCH["seq_lens"].sum())
     X = rng.standard_normal((T, H_))

@@ -53,31 +53,34 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--fit", action="store_true")
     ap.add_argument("--attn", default="cudnn", choices=["cudnn", "flash_attn"])
+    ap.add_argument("--model", default="7b", choices=["7b", "70b"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_layer_cost.json"))
     args = ap.parse_args()
     import torch
     from paper_2509_01193_b200.decoder import DecoderLayer
-    from paper_2509_01193_b200.layer import LLAMA2_7B
+    from paper_2509_01193_b200.layer import LLAMA2_7B, LLAMA2_70B
     from workloads import synth
 
     torch.cuda.set_device(0)
     tasks = synth.c2_tasks()
     ranks, scales = [t.rank for t in tasks], [t.scale for t in tasks]
-    layer = DecoderLayer(LLAMA2_7B, n_heads=32, ranks=ranks, scales=scales, seed=11, attn_backend=args.attn)
+    shapes, heads, hid = (LLAMA2_7B, 32, 4096) if args.model == "7b" else (LLAMA2_70B, 64, 8192)
+    layer = DecoderLayer(shapes, n_heads=heads, ranks=ranks, scales=scales, seed=11, attn_backend=args.attn)
     Tmax = 16384
     g = torch.Generator(device="cuda")
     g.manual_seed(12)
-    Xb = torch.randn(Tmax, 4096, generator=g, device="cuda").to(torch.bfloat16)
-    dYb = torch.randn(Tmax, 4096, generator=g, device="cuda").to(torch.bfloat16)
+    Xb = torch.randn(Tmax, hid, generator=g, device="cuda").to(torch.bfloat16)
+    dYb = torch.randn(Tmax, hid, generator=g, device="cuda").to(torch.bfloat16)
 
     wl = synth.config_c2()
     T = wl.T
     ms, cls = timed_layer(layer, wl.seq_lens, wl.seq_task, Xb[:T], dYb[:T], args.steps)
     fl = layer.flops(wl.seq_lens)
     ours = sum(cls.values())
-    line = {"metric": "Llama-2-7B decoder layer fwd+bwd tokens/s (NEXT-3, 1 GPU)", "value": T / (ms / 1e3),
+    line = {"metric": f"Llama-2-{args.model.upper()} decoder layer fwd+bwd tokens/s (NEXT-3, 1 GPU)",
+            "value": T / (ms / 1e3),
             "unit": "tokens/s", "ms_per_step": ms, "steps": args.steps, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2 (T=16384, 4 tasks r=16, lengths <= 4096)", "layer": "llama2-7b",
+            "config": {"workload": "C2 (T=16384, 4 tasks r=16, lengths <= 4096)", "layer": f"llama2-{args.model}" + (" (GQA 64/8 heads, TP1)" if args.model == "70b" else ""),
                        "attention": {"cudnn": "cuDNN 9 ragged SDPA (library)",
                                      "flash_attn": "flash_attn 2.8 varlen (library)"}[args.attn]},
             "algorithmic_tflops": fl["total"] / (ms / 1e3) / 1e12,
@@ -108,7 +111,7 @@ def main():
         m = np.arange(len(pts)) != i
         c, *_ = np.linalg.lstsq(A[m], y[m], rcond=None)
         loo.append(abs(A[i] @ c - y[i]) / y[i])
-    res = {"model": "t_ms = c0 + c1 * b s + c2 * b s^2 (App. D P:1485, one 7B layer fwd+bwd, 1 B200)",
+    res = {"model": f"t_ms = c0 + c1 * b s + c2 * b s^2 (App. D P:1485, one {args.model} layer fwd+bwd, 1 B200)",
            "attention": args.attn,
            "c0_ms": coef[0], "c1_ms_per_token": coef[1], "c2_ms_per_token_len": coef[2],
            "points": pts, "fit_rel_err": [abs(A[i] @ coef - y[i]) / y[i] for i in range(len(pts))],
