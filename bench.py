@@ -515,28 +515,39 @@ def main():
             for ci, (lens, tsk) in enumerate(chunks):
                 items.append((i, lens, tsk, ci == len(chunks) - 1))
         h2d = d2h = 0
-        comp, copy_s = stream, torch.cuda.Stream(device=dev)
-        ready = [torch.cuda.Event() for _ in range(2)]
+        # NC copy streams (LOBRA_E2E_COPY_STREAMS, default 2): the H2D tensors of a micro-batch
+        # are spread over them so that several copy engines share the PCIe link
+        nc = max(1, int(os.environ.get("LOBRA_E2E_COPY_STREAMS", "2")))
+        comp = stream
+        copy_ss = [torch.cuda.Stream(device=dev) for _ in range(nc)]
+        ready = [[torch.cuda.Event() for _ in range(nc)] for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(comp)
-        copy_s.wait_event(f0)
+        for cs in copy_ss:
+            cs.wait_event(f0)
 
         def issue_copy(k):
             nonlocal h2d
             b = k % 2
             T = int(items[k][1].sum())
-            if k >= 2:
-                copy_s.wait_event(free[b])
-            with torch.cuda.stream(copy_s):
-                for g in host_x:
-                    bufs[b]["X"][g][:T].copy_(host_x[g][:T], non_blocking=True)
-                    h2d += host_x[g][:T].numel() * host_x[g].element_size()
-                for kk in host_dy:
-                    bufs[b]["dY"][kk][:T].copy_(host_dy[kk][:T], non_blocking=True)
-                    h2d += host_dy[kk][:T].numel() * host_dy[kk].element_size()
-            ready[b].record(copy_s)
+            jobs = [(bufs[b]["X"][g], host_x[g]) for g in host_x] + \
+                   [(bufs[b]["dY"][kk], host_dy[kk]) for kk in host_dy]
+            jobs.sort(key=lambda j: -j[1][:T].numel())
+            load = [0] * nc
+            for ci, cs in enumerate(copy_ss):
+                if k >= 2:
+                    cs.wait_event(free[b])
+            for dst, src in jobs:                    # largest first onto the least loaded stream
+                ci = load.index(min(load))
+                n = src[:T].numel() * src.element_size()
+                load[ci] += n
+                with torch.cuda.stream(copy_ss[ci]):
+                    dst[:T].copy_(src[:T], non_blocking=True)
+                h2d += n
+            for ci, cs in enumerate(copy_ss):
+                ready[b][ci].record(cs)
 
         if items:
             issue_copy(0)
@@ -544,7 +555,8 @@ def main():
             if k + 1 < len(items):
                 issue_copy(k + 1)
             b = k % 2
-            comp.wait_event(ready[b])
+            for ev in ready[b]:
+                comp.wait_event(ev)
             T = int(lens.sum())
             first_of_step = k == 0 or items[k - 1][0] != step_i
             if first_of_step and tp_size > 1:
@@ -569,7 +581,7 @@ def main():
             e_ms = float(t.item())
         e2e = {"value": e2e_tokens / (e_ms / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d // ke), "d2h_bytes_per_step": int(d2h // ke),
-               "steps": ke, "overlap": "H2D of micro-batch k+1 on a copy stream during micro-batch k"}
+               "steps": ke, "overlap": f"H2D of micro-batch k+1 on {nc} copy stream(s) during micro-batch k"}
 
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu and not args.profile_only:
