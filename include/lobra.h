@@ -406,6 +406,32 @@ LOBRA_API lobra_status lobra_comm_tp_info(lobra_comm comm, int32_t* tp_size, int
  * the flat fp32 buffer over the WORLD communicator (reading Q7: sum, not mean).  Every
  * rank passes a buffer with the identical full-size layout holding its partial sums
  * (zeros where it owns nothing). */
+/* ------------------------------------------------------------------------------
+ * Own TP collective over peer memory (Megatron row-parallel Y and
+ * column-parallel dX all-reduces).  Every rank of a group allocates one
+ * symmetric device buffer of `bytes` data bytes (lobra_symm_create returns its 64-byte CUDA
+ * IPC handle), the caller exchanges the handles (any transport, e.g. torch.distributed) and
+ * lobra_symm_open maps the peers' buffers (NVLink / NVSwitch peer access inside a node).
+ * lobra_symm_allreduce: dst = sum over ranks of src, two-shot (reduce-scatter in rank order
+ *   0..P-1 with fp32 accumulation, then all-gather) with epoch-flag barriers, so every rank
+ *   gets bitwise the same result; src / dst local device buffers (src may be the data area:
+ *   lobra_symm_data, then no staging copy), count * sizeof(dtype) <= bytes, multiple of 16.
+ *   Every rank must call it with the same count, in the same order.
+ * lobra_comm_from_symm: a comm whose TP group (and world) is the symmetric group (no NCCL);
+ * lobra_comm_attach_symm: route an NCCL comm's TP all-reduces through the symmetric group.
+ * The TP all-reduces of lobra_lora_fwd/bwd (and the group calls) then run on these kernels.
+ * ------------------------------------------------------------------------------ */
+typedef struct lobra_symm_s* lobra_symm;
+LOBRA_API lobra_status lobra_symm_create(int32_t rank, int32_t world, size_t bytes, lobra_symm* out,
+                                         void* ipc_handle_out);
+LOBRA_API lobra_status lobra_symm_open(lobra_symm s, const void* handles /* world x 64 bytes */);
+LOBRA_API lobra_status lobra_symm_destroy(lobra_symm s);
+LOBRA_API void* lobra_symm_data(lobra_symm s);
+LOBRA_API lobra_status lobra_symm_allreduce(lobra_symm s, int32_t dtype, const void* src, void* dst,
+                                            size_t count, lobra_stream_t stream);
+LOBRA_API lobra_status lobra_comm_from_symm(lobra_symm s, lobra_comm* out);
+LOBRA_API lobra_status lobra_comm_attach_symm(lobra_comm comm, lobra_symm s);
+
 LOBRA_API lobra_status lobra_adapter_allreduce(lobra_comm comm, float* flat_grads, size_t count,
                                      lobra_stream_t stream);
 
@@ -445,7 +471,8 @@ enum {
   LOBRA_K_FP32 = 6,       /* fp32 SIMT path kernels                             */
   LOBRA_K_OPT = 7,        /* adapter optimizer (AdamW)                          */
   LOBRA_K_LAYER = 8,      /* decoder-layer elementwise ops (RMSNorm, RoPE, SwiGLU) */
-  LOBRA_K_NUM = 9
+  LOBRA_K_COMM = 9,       /* own peer-memory collectives (lobra_symm_*)          */
+  LOBRA_K_NUM = 10
 };
 typedef struct {
   int64_t count[LOBRA_K_NUM];   /* launches per class since the last reset        */

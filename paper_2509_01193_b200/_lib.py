@@ -28,9 +28,10 @@ EXPORTED = [
     "lobra_adamw_step", "lobra_plan_deployment", "lobra_propose_configs",
     "lobra_lora_group_workspace_bytes", "lobra_lora_group_saved_bytes", "lobra_lora_group_fwd",
     "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
-    "lobra_swiglu_bwd", "lobra_add",
+    "lobra_swiglu_bwd", "lobra_add", "lobra_symm_create", "lobra_symm_open", "lobra_symm_destroy",
+    "lobra_symm_data", "lobra_symm_allreduce", "lobra_comm_from_symm", "lobra_comm_attach_symm",
 ]
-K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer"]
+K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer", "comm"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -155,6 +156,20 @@ def load() -> C.CDLL:
     lib.lobra_swiglu_fwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_]
     lib.lobra_swiglu_bwd.restype = C.c_int
     lib.lobra_swiglu_bwd.argtypes = [C.c_int64, _vp_, _vp_, _vp_, _vp_, _vp_, _vp_]
+    lib.lobra_symm_create.restype = C.c_int
+    lib.lobra_symm_create.argtypes = [C.c_int32, C.c_int32, C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p]
+    lib.lobra_symm_open.restype = C.c_int
+    lib.lobra_symm_open.argtypes = [C.c_void_p, C.c_void_p]
+    lib.lobra_symm_destroy.restype = C.c_int
+    lib.lobra_symm_destroy.argtypes = [C.c_void_p]
+    lib.lobra_symm_data.restype = C.c_void_p
+    lib.lobra_symm_data.argtypes = [C.c_void_p]
+    lib.lobra_symm_allreduce.restype = C.c_int
+    lib.lobra_symm_allreduce.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.lobra_comm_from_symm.restype = C.c_int
+    lib.lobra_comm_from_symm.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.lobra_comm_attach_symm.restype = C.c_int
+    lib.lobra_comm_attach_symm.argtypes = [C.c_void_p, C.c_void_p]
     lib.lobra_add.restype = C.c_int
     lib.lobra_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
@@ -537,3 +552,44 @@ def lobra_swiglu_bwd(d, gate, up, d_gate, d_up, stream=None):
 
 def lobra_add(A, B, C_, stream=None):
     _check(load().lobra_add(int(A.numel()), _ptr(A), _ptr(B), _ptr(C_), _stream(stream)))
+
+
+# ------------------------------------------------------------------ own peer-memory collectives
+class Symm:
+    """Symmetric device buffer of one rank of a TP group (include/lobra.h lobra_symm_*).
+    Usage: s = Symm(rank, world, nbytes); handles = all_gather(s.handle); s.open(handles)."""
+
+    def __init__(self, rank: int, world: int, nbytes: int):
+        h = C.c_void_p(0)
+        buf = C.create_string_buffer(64)
+        _check(load().lobra_symm_create(rank, world, nbytes, C.byref(h), buf))
+        self.ptr, self.handle = h.value, buf.raw
+        self.rank, self.world, self.nbytes = rank, world, nbytes
+
+    def open(self, handles):
+        blob = b"".join(handles)
+        assert len(blob) == 64 * self.world
+        _check(load().lobra_symm_open(C.c_void_p(self.ptr), C.create_string_buffer(blob, len(blob))))
+
+    def data_ptr(self) -> int:
+        return int(load().lobra_symm_data(C.c_void_p(self.ptr)))
+
+    def allreduce(self, src, dst=None, stream=None):
+        dst = src if dst is None else dst
+        _check(load().lobra_symm_allreduce(C.c_void_p(self.ptr), dtype_code(src.dtype), _ptr(src), _ptr(dst),
+                                           int(src.numel()), _stream(stream)))
+
+    def destroy(self):
+        if self.ptr:
+            load().lobra_symm_destroy(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+def lobra_comm_from_symm(symm: Symm) -> Comm:
+    h = C.c_void_p(0)
+    _check(load().lobra_comm_from_symm(C.c_void_p(symm.ptr), C.byref(h)))
+    return Comm(h.value, symm.world, symm.rank, 0)
+
+
+def lobra_comm_attach_symm(comm: Comm, symm: Symm | None):
+    _check(load().lobra_comm_attach_symm(C.c_void_p(comm.handle), C.c_void_p(symm.ptr if symm else 0)))

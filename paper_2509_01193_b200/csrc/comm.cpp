@@ -3,6 +3,7 @@
 // and the per-step adapter-gradient all-reduce across FT replicas (P:170,
 // P:306).  NCCL is resolved at run time with dlopen so that the process uses the single
 // libnccl.so.2 that torch already loaded (NCCL 2.28 in this image).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -80,10 +81,18 @@ struct lobra_comm_s {
   ncclComm_t world = nullptr;
   ncclComm_t tp = nullptr;
   int world_size = 0, rank = 0, tp_size = 0, tp_rank = 0;
+  lobra_symm symm = nullptr;   // own peer-memory TP collectives (symm.cu), not owned
 };
 
 namespace lobra {
+// symm.cu
+template <typename T>
+lobra_status symm_allreduce(lobra_symm s, const void* src, void* dst, size_t count, cudaStream_t st);
+int symm_world(lobra_symm s);
+int symm_rank(lobra_symm s);
+
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st) {
+  if (c && c->symm) return symm_allreduce<__nv_bfloat16>(c->symm, buf, buf, count, st);
   lobra_status s = need_nccl();
   if (s != LOBRA_OK) return s;
   if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
@@ -92,6 +101,7 @@ lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaS
                     "TP all-reduce");
 }
 lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st) {
+  if (c && c->symm) return symm_allreduce<float>(c->symm, buf, buf, count, st);
   lobra_status s = need_nccl();
   if (s != LOBRA_OK) return s;
   if (!c || !c->tp) return fail(LOBRA_ERR_INPUT, "comm has no TP communicator");
@@ -143,6 +153,26 @@ extern "C" lobra_status lobra_comm_init(const void* id128, int32_t world, int32_
   return LOBRA_OK;
 }
 
+extern "C" lobra_status lobra_comm_from_symm(lobra_symm s, lobra_comm* out) {
+  clear_error();
+  if (!s || !out) return fail(LOBRA_ERR_INPUT, "null argument");
+  lobra_comm c = new lobra_comm_s();
+  c->symm = s;
+  c->world_size = c->tp_size = symm_world(s);
+  c->rank = c->tp_rank = symm_rank(s);
+  *out = c;
+  return LOBRA_OK;
+}
+
+extern "C" lobra_status lobra_comm_attach_symm(lobra_comm c, lobra_symm s) {
+  clear_error();
+  if (!c) return fail(LOBRA_ERR_INPUT, "null comm");
+  if (s && symm_world(s) != c->tp_size)
+    return fail(LOBRA_ERR_INPUT, "symmetric group size %d != TP size %d", symm_world(s), c->tp_size);
+  c->symm = s;
+  return LOBRA_OK;
+}
+
 extern "C" lobra_status lobra_comm_destroy(lobra_comm c) {
   clear_error();
   if (!c) return LOBRA_OK;
@@ -165,6 +195,11 @@ extern "C" lobra_status lobra_comm_tp_info(lobra_comm c, int32_t* tp_size, int32
 extern "C" lobra_status lobra_adapter_allreduce(lobra_comm c, float* flat, size_t count,
                                                 lobra_stream_t stream) {
   clear_error();
+  if (c && !c->world && c->symm) {   // symmetric-group comm: the group is the world
+    if (!flat && count) return fail(LOBRA_ERR_INPUT, "null buffer");
+    if (c->world_size == 1 || count == 0) return LOBRA_OK;
+    return symm_allreduce<float>(c->symm, flat, flat, count, reinterpret_cast<cudaStream_t>(stream));
+  }
   if (!c || !c->world) return fail(LOBRA_ERR_INPUT, "null comm");
   if (!flat && count) return fail(LOBRA_ERR_INPUT, "null buffer");
   lobra_status s = need_nccl();
