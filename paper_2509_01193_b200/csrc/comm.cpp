@@ -91,6 +91,25 @@ lobra_status symm_allreduce(lobra_symm s, const void* src, void* dst, size_t cou
 int symm_world(lobra_symm s);
 int symm_rank(lobra_symm s);
 
+void* symm_data(lobra_symm s);
+size_t symm_capacity(lobra_symm s);
+lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
+
+// The symmetric data area of the comm's TP group when it can hold `bytes` (the projection
+// GEMMs then write their partial straight into peer-visible memory), else nullptr.
+void* comm_tp_stage(lobra_comm c, size_t bytes) {
+  if (!c || !c->symm || symm_capacity(c->symm) < bytes) return nullptr;
+  return symm_data(c->symm);
+}
+
+// dst = sum over the TP group of src (src may be the stage area); bf16.
+lobra_status comm_tp_allreduce_bf16_to(lobra_comm c, const void* src, void* dst, size_t count, cudaStream_t st) {
+  if (c && c->symm) return symm_allreduce<__nv_bfloat16>(c->symm, src, dst, count, st);
+  if (src != dst && cudaMemcpyAsync(dst, src, count * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return fail(LOBRA_ERR_CUDA, "TP staging copy failed");
+  return comm_tp_allreduce_bf16(c, dst, count, st);
+}
+
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st) {
   if (c && c->symm) return symm_allreduce<__nv_bfloat16>(c->symm, buf, buf, count, st);
   lobra_status s = need_nccl();

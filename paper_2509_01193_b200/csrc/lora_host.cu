@@ -34,6 +34,8 @@ void clear_error() { g_err.clear(); }
 // comm.cpp
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
 lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st);
+void* comm_tp_stage(lobra_comm c, size_t bytes);
+lobra_status comm_tp_allreduce_bf16_to(lobra_comm c, const void* src, void* dst, size_t count, cudaStream_t st);
 
 // ------------------------------------------------------------------ tracing
 namespace {
@@ -622,15 +624,19 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
       launch_rowproj(false, mX, mA, in, meta, static_cast<__nv_bfloat16*>(Hs),
                      reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);
     }
-    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in, static_cast<__nv_bfloat16*>(Y), 0, meta,
-                ctx->num_sms, st); }
+    // row-parallel with a symmetric TP group: the GEMM writes its partial straight into the
+    // peer-visible stage area, the own all-reduce then reduces it into Y (no staging copy)
+    void* stage = prob->tp_kind == LOBRA_TP_ROW ? comm_tp_stage(prob->tp, (size_t)P.T * out * 2) : nullptr;
+    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in,
+                                                   static_cast<__nv_bfloat16*>(stage ? stage : Y), 0, meta,
+                                                   ctx->num_sms, st); }
+    if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
+    if (prob->tp_kind == LOBRA_TP_ROW) return comm_tp_allreduce_bf16_to(prob->tp, stage ? stage : Y, Y, (size_t)P.T * out, st);
+    return LOBRA_OK;
   }
   if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
-  if (prob->tp_kind == LOBRA_TP_ROW) {
-    const size_t cnt = (size_t)P.T * out;
-    return prob->dtype == LOBRA_BF16 ? comm_tp_allreduce_bf16(prob->tp, Y, cnt, st)
-                                     : comm_tp_allreduce_f32(prob->tp, static_cast<float*>(Y), cnt, st);
-  }
+  if (prob->tp_kind == LOBRA_TP_ROW)
+    return comm_tp_allreduce_f32(prob->tp, static_cast<float*>(Y), (size_t)P.T * out, st);
   return LOBRA_OK;
 }
 
@@ -945,11 +951,14 @@ extern "C" lobra_status lobra_lora_group_fwd(const lobra_group_problem* g, const
     if ((s = make_map(&mB, Bop, P.ld8, out, 64, 128)) != LOBRA_OK) return s;
     Meta mp = meta;
     mp.band = p * P.qp;
-    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in, static_cast<__nv_bfloat16*>(Y[p]),
-                                                   0, mp, ctx->num_sms, st); }
+    void* stage = g->tp_kind == LOBRA_TP_ROW ? comm_tp_stage(g->tp, (size_t)P.T * out * 2) : nullptr;
+    { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in,
+                                                   static_cast<__nv_bfloat16*>(stage ? stage : Y[p]), 0, mp,
+                                                   ctx->num_sms, st); }
     if ((s = check_launch("lobra_lora_group_fwd")) != LOBRA_OK) return s;
     if (g->tp_kind == LOBRA_TP_ROW)
-      if ((s = comm_tp_allreduce_bf16(g->tp, Y[p], (size_t)P.T * out, st)) != LOBRA_OK) return s;
+      if ((s = comm_tp_allreduce_bf16_to(g->tp, stage ? stage : Y[p], Y[p], (size_t)P.T * out, st)) != LOBRA_OK)
+        return s;
   }
   return LOBRA_OK;
 }
@@ -1015,6 +1024,13 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
   if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
   if ((s = make_map(&mG, Gs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
   if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
+  // column-parallel with a symmetric TP group: the group's dX GEMMs accumulate straight into
+  // the peer-visible stage area, the own all-reduce then reduces it into dX
+  void* stage = g->tp_kind == LOBRA_TP_COLUMN ? comm_tp_stage(g->tp, (size_t)P.T * in * 2) : nullptr;
+  if (stage && accumulate_dx &&
+      cudaMemcpyAsync(stage, dX, (size_t)P.T * in * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return fail(LOBRA_ERR_CUDA, "TP stage copy failed");
+  auto* dXacc = static_cast<__nv_bfloat16*>(stage ? stage : dX);
   for (int p = 0; p < np; ++p) {
     const int out = (int)g->out[p];
     const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ga->B[p]);
@@ -1036,7 +1052,7 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
       launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
                     ctx->num_sms, st);
     }
-    { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
+    { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, dXacc,
                                                    p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st); }
     Meta mb = meta;
     mb.use_dy_units = 1;
@@ -1052,7 +1068,7 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
     launch_finalize(0, partA, in, ma, dA[p], ldA, accumulate_dadb, st);
   }
   if ((s = check_launch("lobra_lora_group_bwd")) != LOBRA_OK) return s;
-  if (g->tp_kind == LOBRA_TP_COLUMN) return comm_tp_allreduce_bf16(g->tp, dX, (size_t)P.T * in, st);
+  if (g->tp_kind == LOBRA_TP_COLUMN) return comm_tp_allreduce_bf16_to(g->tp, dXacc, dX, (size_t)P.T * in, st);
   return LOBRA_OK;
 }
 

@@ -100,6 +100,37 @@ torch.cuda.synchronize()
 fa = flat[:24 * d_in].view(24, d_in).cpu().numpy().astype(np.float64)
 fb = flat[24 * d_in:].view(d_out, 24).cpu().numpy().astype(np.float64)
 assert O.max_rel_err(fa, dAo) <= 2e-2 and O.max_rel_err(fb, dBo) <= 2e-2
+# projection group (q/k/v-like, column-parallel): the group's dX GEMMs accumulate in the
+# symmetric stage area and one own all-reduce produces dX; row-parallel group forward
+outs_full = [256, 128, 128]
+tg = [synth.layer_tensors(wl, d_in, of, seed=9 + p) for p, of in enumerate(outs_full)]
+bg = [{k: synth.round_bf16(v) for k, v in x.items()} for x in tg]
+sh = [(rank * of // world, (rank + 1) * of // world) for of in outs_full]
+Wg = [up(x["W"][a:c]) for x, (a, c) in zip(bg, sh)]
+Ag = [up(x["A"]) for x in bg]
+Bg = [up(x["B"][a:c]) for x, (a, c) in zip(bg, sh)]
+dYg = [up(x["dY"][:, a:c]) for x, (a, c) in zip(bg, sh)]
+outs_l = [c - a for a, c in sh]
+wsg = torch.empty(_lib.lobra_lora_group_workspace_bytes(code, d_in, outs_l, lens, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+Hg = torch.empty(_lib.lobra_lora_group_saved_bytes(code, d_in, outs_l, lens, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+Ys = [torch.empty(T, ol, dtype=torch.bfloat16, device=dev) for ol in outs_l]
+dXg = torch.empty(T, d_in, dtype=torch.bfloat16, device=dev)
+dAs = [torch.empty(24, d_in, dtype=torch.float32, device=dev) for _ in outs_l]
+dBs = [torch.empty(ol, 24, dtype=torch.float32, device=dev) for ol in outs_l]
+Xg = up(bg[0]["X"])
+_lib.lobra_lora_group_fwd(Xg, Wg, Ag, Bg, ranks, scales, lens, tasks, Ys, Hg, wsg, tp_kind=_lib.LOBRA_TP_COLUMN, comm=comm)
+_lib.lobra_lora_group_bwd(Xg, Wg, Ag, Bg, ranks, scales, lens, tasks, Hg, dYg, dXg, dAs, dBs, wsg,
+                          tp_kind=_lib.LOBRA_TP_COLUMN, comm=comm)
+torch.cuda.synchronize()
+ref = np.zeros((T, d_in))
+og = [{k: v.astype(np.float64) for k, v in x.items()} for x in bg]
+for x in og:
+    ref += O.lora_bwd(og[0]["X"], x["W"], x["A"], x["B"], ranks, scales, lens, tasks, x["dY"])[0]
+err = O.max_rel_err(dXg.float().cpu().numpy().astype(np.float64), ref)
+assert err <= 2e-2, ("group column bwd dX", err)
+got = [None] * world
+dist.all_gather_object(got, dXg.float().cpu().numpy().tobytes())
+assert all(g == got[0] for g in got)
 comm.destroy()
 S.destroy()
 print("SYMM_OK", rank)
