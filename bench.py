@@ -326,6 +326,38 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = _lib.lobra_comm_init(uid[0], world, rank, my_rep)
 
+    # TP all-reduces through the library's own peer-memory collective (lobra_symm_*: CUDA IPC
+    # buffers over NVLink) unless LOBRA_TP_COLLECTIVE=nccl; NCCL if any rank fails
+    # to set it up.  Handles travel over the world process group; every rank takes part.
+    symm = None
+    any_tp = any(g[0] > 1 for g in groups)
+    tp_coll = "nccl" if any_tp else "none"
+    if comm is not None and os.environ.get("LOBRA_TP_COLLECTIVE", "own") != "nccl":
+        mine, err = None, ""
+        if tp_size > 1:
+            try:
+                symm = _lib.Symm(tp_rank, tp_size, groups[my_group][2] * 4096 * 2)
+                mine = symm.handle
+            except Exception as e:   # setup failure -> NCCL on every rank
+                err = str(e)
+        allh = [None] * world
+        dist.all_gather_object(allh, (mine, err))
+        ok = all(not e for _, e in allh)
+        if ok and symm is not None:
+            try:
+                symm.open([allh[r][0] for r in reps[my_rep]])
+            except Exception:
+                ok = False
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1 and any_tp:
+            tp_coll = "own (CUDA IPC peer memory, two-shot, lobra_symm)"
+        if int(flag.item()) == 1 and symm is not None:
+            _lib.lobra_comm_attach_symm(comm, symm)
+        elif symm is not None:
+            symm.destroy()
+            symm = None
+
     tasks = synth.c2_tasks()
     ranks = [t.rank for t in tasks]
     scales = [t.scale for t in tasks]
@@ -598,7 +630,8 @@ def main():
                 "config": {"workload": "C2: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
                                        "4 tasks r=16 s=2, lengths<=4096 packed",
                            "global_batch_tokens": int(tokens / args.steps), "seq_len_max": 4096,
-                           "parallelism": par, "l2": "inputs > L2 (each projection input >= 128 MiB)"},
+                           "parallelism": par, "l2": "inputs > L2 (each projection input >= 128 MiB)",
+                           "tp_collective": tp_coll},
                 "per_gpu": value / n_gpus,
                 "algorithmic_tflops": step_tflops,
                 "frac_of_bf16_peak": {"burst": step_tflops / float(peaks["bf16_tflops"]),
@@ -611,6 +644,10 @@ def main():
     if comm is not None:
         torch.cuda.synchronize()
         comm.destroy()
+    if world > 1:
+        dist.barrier()
+    if symm is not None:          # after every peer stopped using the mapped buffers
+        symm.destroy()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
