@@ -95,6 +95,8 @@ void* symm_data(lobra_symm s);
 size_t symm_capacity(lobra_symm s);
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
 
+lobra_symm comm_symm(lobra_comm c) { return c ? c->symm : nullptr; }
+
 // The symmetric data area of the comm's TP group when it can hold `bytes` (the projection
 // GEMMs then write their partial straight into peer-visible memory), else nullptr.
 void* comm_tp_stage(lobra_comm c, size_t bytes) {

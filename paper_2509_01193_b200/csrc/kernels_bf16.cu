@@ -239,6 +239,7 @@ struct Gemm2Args {
   int T, N, K, ntm2, ntn, accumulate, group_m;
   __nv_bfloat16* C;
   Meta meta;
+  TpScatter tp;   // tp.peer != nullptr: fused GEMM -> reduce-scatter over peer memory
 };
 
 __device__ __forceinline__ int tile_slot_begin(const Meta& m, int tile) {
@@ -424,7 +425,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
         tmem_ld32(tmem + ((q * 32u) << 16) + acc * 256 + c * 32, v);
         const int col0 = n * 256 + c * 32;
         if (row < args.T && col0 < args.N) {
-          uint4* dst = reinterpret_cast<uint4*>(args.C + (size_t)row * args.N + col0);
+          // fused TP reduce-scatter: row r goes to its owner rank (r / chunk) into the slot of
+          // this rank -- a store over NVLink that overlaps the next tile's MMAs
+          __nv_bfloat16* crow =
+              args.tp.peer ? reinterpret_cast<__nv_bfloat16*>(args.tp.peer[row / args.tp.chunk_rows] + args.tp.data_off) +
+                                 ((size_t)args.tp.rank * args.tp.chunk_rows + row % args.tp.chunk_rows) * args.N
+                           : args.C + (size_t)row * args.N;
+          uint4* dst = reinterpret_cast<uint4*>(crow + col0);
           if (args.accumulate) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -1549,7 +1556,7 @@ bool gemm_uses_pair() {
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms,
-                 cudaStream_t st) {
+                 cudaStream_t st, const TpScatter* tp) {
   static int use_pair = -1;
   if (use_pair < 0) {
     use_pair = gemm_uses_pair() ? 1 : 0;
@@ -1568,6 +1575,7 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
     a.accumulate = accumulate;
     a.C = C;
     a.meta = meta;
+    a.tp = tp ? *tp : TpScatter{};
     {
       // measured (profiles/r1_gemm_raster.md): N-fastest is best while W fits in L2 next to
       // the X panels; 16-block groups once W is large (gate/up/down: 90 MB)

@@ -35,6 +35,20 @@ void clear_error() { g_err.clear(); }
 lobra_status comm_tp_allreduce_bf16(lobra_comm c, void* buf, size_t count, cudaStream_t st);
 lobra_status comm_tp_allreduce_f32(lobra_comm c, float* buf, size_t count, cudaStream_t st);
 void* comm_tp_stage(lobra_comm c, size_t bytes);
+lobra_symm comm_symm(lobra_comm c);
+bool symm_scatter_target(lobra_symm s, long long T, long long N, TpScatter* out);
+lobra_status symm_scatter_finish(lobra_symm s, long long T, long long N, void* dst, cudaStream_t st);
+
+// LOBRA_TP_FUSED=0: row-parallel GEMM writes its partial locally and the own all-reduce
+// follows (A/B of the fused reduce-scatter epilogue)
+bool tp_fused() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_TP_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 lobra_status comm_tp_allreduce_bf16_to(lobra_comm c, const void* src, void* dst, size_t count, cudaStream_t st);
 
 // ------------------------------------------------------------------ tracing
@@ -624,8 +638,19 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
       launch_rowproj(false, mX, mA, in, meta, static_cast<__nv_bfloat16*>(Hs),
                      reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);
     }
-    // row-parallel with a symmetric TP group: the GEMM writes its partial straight into the
-    // peer-visible stage area, the own all-reduce then reduces it into Y (no staging copy)
+    // row-parallel with a symmetric TP group: FUSED GEMM -> reduce-scatter (each output row is
+    // stored into its owner rank's buffer over NVLink from the GEMM epilogue), then the owner
+    // reduces locally and every rank gathers Y; else the GEMM writes its partial into the
+    // peer-visible stage area and the own all-reduce follows (no staging copy either way)
+    TpScatter tps;
+    if (prob->tp_kind == LOBRA_TP_ROW && tp_fused() && gemm_uses_pair() &&
+        symm_scatter_target(comm_symm(prob->tp), P.T, out, &tps)) {
+      { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in,
+                                                     static_cast<__nv_bfloat16*>(Y), 0, meta, ctx->num_sms, st,
+                                                     &tps); }
+      if ((s = check_launch("lobra_lora_fwd")) != LOBRA_OK) return s;
+      return symm_scatter_finish(comm_symm(prob->tp), P.T, out, Y, st);
+    }
     void* stage = prob->tp_kind == LOBRA_TP_ROW ? comm_tp_stage(prob->tp, (size_t)P.T * out * 2) : nullptr;
     { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in,
                                                    static_cast<__nv_bfloat16*>(stage ? stage : Y), 0, meta,

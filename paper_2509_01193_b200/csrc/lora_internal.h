@@ -91,9 +91,18 @@ void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int 
 // true: the 2-CTA (cta_group::2) GEMM is used; its B boxes are 128 rows/columns per CTA
 // (env LOBRA_GEMM_1CTA=1 selects the 1-CTA kernel with 256-wide boxes).
 bool gemm_uses_pair();
+// Fused GEMM -> TP reduce-scatter (symm.cu): output row r is stored into rank
+// (r / chunk_rows)'s symmetric buffer, slot `rank`, row r % chunk_rows (bf16 [chunk_rows, N]
+// per slot) instead of C.  peer == nullptr: plain C.  2-CTA GEMM only, accumulate = 0.
+struct TpScatter {
+  uint8_t* const* peer = nullptr;   // device table of the group's buffer bases
+  long long data_off = 0;           // bytes from a base to its data area
+  int rank = 0, chunk_rows = 1;
+};
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
-                 __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st);
+                 __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st,
+                 const TpScatter* tp = nullptr);
 // partial[u][chunk][q][128] = sum over the unit's slots: Z[tile rows, chunk cols]^T Slot
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
                    const Meta& meta, float* partial, int num_sms, cudaStream_t st);

@@ -19,10 +19,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
 #include "common.h"
+#include "lora_internal.h"
 
 namespace lobra {
 int64_t count_launch(int kind, cudaStream_t st, bool begin);   // lora_host.cu
@@ -131,6 +133,36 @@ __global__ void k_symm_all_gather(uint8_t* const* __restrict__ peer, int world, 
   }
 }
 
+// Fused path, after the GEMM stored row r of its partial into rank (r / chunk)'s slot
+// [this rank]: the owner sums its chunk over the slots in rank order (local memory only) into
+// its own slot, in place.
+__global__ void k_tp_reduce_rows(uint8_t* const* __restrict__ peer, int rank, int world, long long chunk_rows,
+                                 long long rows_here, int nv_row /* uint4 per row */) {
+  uint8_t* base = peer[rank] + kHdr;
+  const long long slot_v = chunk_rows * nv_row;
+  const long long total = rows_here * nv_row;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
+       v += (long long)gridDim.x * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < world; ++p)
+      Vec<__nv_bfloat16>::add(acc, reinterpret_cast<const uint4*>(base)[p * slot_v + v]);
+    reinterpret_cast<uint4*>(base)[rank * slot_v + v] = Vec<__nv_bfloat16>::pack(acc);
+  }
+}
+
+// dst row r <- owner (r / chunk)'s reduced slot
+__global__ void k_tp_gather_rows(uint8_t* const* __restrict__ peer, long long chunk_rows, long long T, int nv_row,
+                                 uint4* __restrict__ dst) {
+  const long long total = T * nv_row;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long row = v / nv_row;
+    const int c = (int)(row / chunk_rows);
+    const long long local = v - c * chunk_rows * nv_row;
+    dst[v] = reinterpret_cast<const uint4*>(peer[c] + kHdr)[c * chunk_rows * nv_row + local];
+  }
+}
+
 int sms() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
@@ -171,6 +203,43 @@ lobra_status symm_allreduce(lobra_symm s, const void* src, void* dst, size_t cou
 }
 template lobra_status symm_allreduce<__nv_bfloat16>(lobra_symm, const void*, void*, size_t, cudaStream_t);
 template lobra_status symm_allreduce<float>(lobra_symm, const void*, void*, size_t, cudaStream_t);
+
+// Target of the fused GEMM -> reduce-scatter for a [T, N] bf16 result (nullptr-peer target
+// when the buffer cannot hold world x ceil(T / world) rows of N).
+bool symm_scatter_target(lobra_symm s, long long T, long long N, TpScatter* out) {
+  if (!s || !s->opened || T <= 0) return false;
+  const long long chunk = (T + s->world - 1) / s->world;
+  if ((size_t)(s->world * chunk * N * 2) > s->bytes) return false;
+  out->peer = s->d_peer;
+  out->data_off = (long long)kHdr;
+  out->rank = s->rank;
+  out->chunk_rows = (int)chunk;
+  return true;
+}
+
+// After the fused GEMM: barrier, owner-local reduction of its row chunk, barrier, gather of
+// every chunk into dst [T, N], barrier.  Same rank-order fp32 sums as symm_allreduce.
+lobra_status symm_scatter_finish(lobra_symm s, long long T, long long N, void* dst, cudaStream_t st) {
+  const long long chunk = (T + s->world - 1) / s->world;
+  const long long r0 = s->rank * chunk, rows_here = std::max(0LL, std::min(T, r0 + chunk) - r0);
+  const int nv_row = (int)(N / 8);
+  const uint64_t e = ++s->epoch;
+  const int grid = 4 * sms();
+  auto counted = [&](auto&& launch) {
+    count_launch(LOBRA_K_COMM, st, true);
+    launch();
+    count_launch(LOBRA_K_COMM, st, false);
+  };
+  counted([&] { k_symm_barrier<<<1, 64, 0, st>>>(s->d_peer, s->rank, s->world, 0, e); });
+  if (rows_here > 0)
+    counted([&] { k_tp_reduce_rows<<<grid, 256, 0, st>>>(s->d_peer, s->rank, s->world, chunk, rows_here, nv_row); });
+  counted([&] { k_symm_barrier<<<1, 64, 0, st>>>(s->d_peer, s->rank, s->world, 1, e); });
+  counted([&] { k_tp_gather_rows<<<grid, 256, 0, st>>>(s->d_peer, chunk, T, nv_row, static_cast<uint4*>(dst)); });
+  counted([&] { k_symm_barrier<<<1, 64, 0, st>>>(s->d_peer, s->rank, s->world, 2, e); });
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(LOBRA_ERR_CUDA, "fused TP reduce-scatter: %s", cudaGetErrorString(err));
+  return LOBRA_OK;
+}
 
 void* symm_data(lobra_symm s) { return s ? s->base + kHdr : nullptr; }
 size_t symm_capacity(lobra_symm s) { return s ? s->bytes : 0; }

@@ -4,9 +4,11 @@ handles travel over a gloo process group).  Checks:
   * bf16 / fp32 all-reduce over 3 epochs, ragged chunks: every rank's result is bitwise the
     rank-order fp32 sum of the partials, rounded once (computed on the host);
   * Megatron TP through the library's own collective (lobra_comm_from_symm, no NCCL): a
-    row-parallel projection's forward Y and a column-parallel projection's backward dX
-    from 2 shards equal the UNSHARDED fp64 oracle (bf16 tolerance) and are bitwise equal on
-    both ranks.
+    row-parallel projection's forward Y (the FUSED GEMM -> reduce-scatter epilogue: output
+    rows stored into their owner rank's buffer, bitwise equal to local GEMM + all-reduce,
+    also for an odd T) and a column-parallel projection's / group's backward dX from 2
+    shards equal the UNSHARDED fp64 oracle (bf16 tolerance) and are bitwise equal on both
+    ranks.
 """
 import os
 import socket
@@ -72,6 +74,29 @@ torch.cuda.synchronize()
 Yg = Y.float().cpu().numpy().astype(np.float64)
 err = O.max_rel_err(Yg, Yo)
 assert err <= 2e-2, ("row fwd", err)
+# the fused GEMM -> reduce-scatter epilogue == local GEMM partial + own all-reduce, bitwise
+Yp, Yr = torch.empty_like(Y), torch.empty_like(Y)
+_lib.lobra_lora_fwd(Xs, Ws, As, Bd, ranks, scales, lens, tasks, Yp, Hs, ws)
+S.allreduce(Yp, Yr)
+torch.cuda.synchronize()
+assert torch.equal(Yr, Y), "fused row-parallel forward differs from GEMM + all-reduce"
+# odd T: unequal row chunks, 128-row tiles straddling the owner boundary
+lens2 = [100, 61, 200]
+wl2 = synth.Workload("tp2", wl.tasks, np.array(lens2, np.int32), np.array(tasks, np.int32), 0)
+t2 = {k: synth.round_bf16(v) for k, v in synth.layer_tensors(wl2, d_in, d_out, seed=6).items()}
+X2 = up(t2["X"][:, i0:i1])
+ws2 = torch.empty(_lib.lobra_lora_workspace_bytes(code, i1 - i0, d_out, lens2, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+Hs2 = torch.empty(_lib.lobra_lora_saved_bytes(code, i1 - i0, d_out, lens2, tasks, ranks, scales), dtype=torch.uint8, device=dev)
+Y2, Y2p, Y2r = (torch.empty(wl2.T, d_out, dtype=torch.bfloat16, device=dev) for _ in range(3))
+W2, A2, B2 = up(t2["W"][:, i0:i1]), up(t2["A"][:, i0:i1]), up(t2["B"])
+_lib.lobra_lora_fwd(X2, W2, A2, B2, ranks, scales, lens2, tasks, Y2, Hs2, ws2, tp_kind=_lib.LOBRA_TP_ROW, comm=comm)
+_lib.lobra_lora_fwd(X2, W2, A2, B2, ranks, scales, lens2, tasks, Y2p, Hs2, ws2)
+S.allreduce(Y2p, Y2r)
+torch.cuda.synchronize()
+assert torch.equal(Y2r, Y2)
+o2 = {k: v.astype(np.float64) for k, v in t2.items()}
+assert O.max_rel_err(Y2.float().cpu().numpy().astype(np.float64),
+                     O.lora_fwd(o2["X"], o2["W"], o2["A"], o2["B"], ranks, scales, lens2, tasks)) <= 2e-2
 # column-parallel (shard `out`): W rows, B rows; backward dX all-reduced
 o0, o1 = rank * d_out // world, (rank + 1) * d_out // world
 Wc, Bc, Ad = up(b["W"][o0:o1]), up(b["B"][o0:o1]), up(b["A"])
