@@ -433,9 +433,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
                            : args.C + (size_t)row * args.N;
           uint4* dst = reinterpret_cast<uint4*>(crow + col0);
           if (args.accumulate) {
+            // accumulate onto the LOCAL partial in C (with the fused reduce-scatter the
+            // accumulated row then goes to its owner)
+            const uint4* src = reinterpret_cast<const uint4*>(args.C + (size_t)row * args.N + col0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              uint4 o = dst[j];
+              uint4 o = src[j];
               const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&o);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {

@@ -758,14 +758,24 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
       launch_rowproj(true, mdY, mBt, out, meta, Gs, reinterpret_cast<float*>(w + L.rpart),
                      reinterpret_cast<int*>(w + L.counters), st);
     }
+    // column-parallel with a symmetric TP group: FUSED GEMM -> reduce-scatter (the epilogue adds
+    // the local partial in dX when accumulating and stores each row into its owner's buffer)
+    TpScatter tps;
+    const bool fused_tp = prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() && gemm_uses_pair() &&
+                          symm_scatter_target(comm_symm(prob->tp), P.T, in, &tps);
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
-                accumulate_dx, meta, ctx->num_sms, st); }
+                accumulate_dx, meta, ctx->num_sms, st, fused_tp ? &tps : nullptr); }
     if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
     { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st); }
     if (!fused_dy && meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
     { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta_b, dB, 0, accumulate_dadb, st); }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
+  if (prob->dtype == LOBRA_BF16 && prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() && gemm_uses_pair()) {
+    TpScatter tps;
+    if (symm_scatter_target(comm_symm(prob->tp), P.T, in, &tps))   // the GEMM already scattered
+      return symm_scatter_finish(comm_symm(prob->tp), P.T, in, dX, st);
+  }
   if (prob->tp_kind == LOBRA_TP_COLUMN) {
     const size_t cnt = (size_t)P.T * in;
     return prob->dtype == LOBRA_BF16 ? comm_tp_allreduce_bf16(prob->tp, dX, cnt, st)
@@ -1051,7 +1061,10 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
   if ((s = make_map(&mHs, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
   // column-parallel with a symmetric TP group: the group's dX GEMMs accumulate straight into
   // the peer-visible stage area, the own all-reduce then reduces it into dX
-  void* stage = g->tp_kind == LOBRA_TP_COLUMN ? comm_tp_stage(g->tp, (size_t)P.T * in * 2) : nullptr;
+  TpScatter tps;
+  const bool fused_tp = g->tp_kind == LOBRA_TP_COLUMN && tp_fused() &&
+                        symm_scatter_target(comm_symm(g->tp), P.T, in, &tps);
+  void* stage = g->tp_kind == LOBRA_TP_COLUMN && !fused_tp ? comm_tp_stage(g->tp, (size_t)P.T * in * 2) : nullptr;
   if (stage && accumulate_dx &&
       cudaMemcpyAsync(stage, dX, (size_t)P.T * in * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return fail(LOBRA_ERR_CUDA, "TP stage copy failed");
@@ -1077,8 +1090,10 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
       launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
                     ctx->num_sms, st);
     }
+    // fused TP: projections 0..np-2 accumulate locally in dX, the last one scatters the rows
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, dXacc,
-                                                   p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st); }
+                                                   p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st,
+                                                   fused_tp && p == np - 1 ? &tps : nullptr); }
     Meta mb = meta;
     mb.use_dy_units = 1;
     { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, mb, dB[p], 0, accumulate_dadb, st); }
@@ -1093,6 +1108,7 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
     launch_finalize(0, partA, in, ma, dA[p], ldA, accumulate_dadb, st);
   }
   if ((s = check_launch("lobra_lora_group_bwd")) != LOBRA_OK) return s;
+  if (fused_tp) return symm_scatter_finish(comm_symm(g->tp), P.T, in, dX, st);
   if (g->tp_kind == LOBRA_TP_COLUMN) return comm_tp_allreduce_bf16_to(g->tp, dXacc, dX, (size_t)P.T * in, st);
   return LOBRA_OK;
 }

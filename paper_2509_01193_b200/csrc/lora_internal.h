@@ -93,7 +93,8 @@ void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int 
 bool gemm_uses_pair();
 // Fused GEMM -> TP reduce-scatter (symm.cu): output row r is stored into rank
 // (r / chunk_rows)'s symmetric buffer, slot `rank`, row r % chunk_rows (bf16 [chunk_rows, N]
-// per slot) instead of C.  peer == nullptr: plain C.  2-CTA GEMM only, accumulate = 0.
+// per slot) instead of C (with accumulate, the row of C is added first: C holds the local
+// partial).  peer == nullptr: plain C.  2-CTA GEMM only.
 struct TpScatter {
   uint8_t* const* peer = nullptr;   // device table of the group's buffer bases
   long long data_off = 0;           // bytes from a base to its data area

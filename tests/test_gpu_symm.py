@@ -113,6 +113,12 @@ torch.cuda.synchronize()
 dXg = dX.float().cpu().numpy().astype(np.float64)
 err = O.max_rel_err(dXg, dXo)
 assert err <= 2e-2, ("column bwd dX", err)
+# fused GEMM -> reduce-scatter in the backward == local partial + own all-reduce, bitwise
+dXp, dXr = torch.empty_like(dX), torch.empty_like(dX)
+_lib.lobra_lora_bwd(Xd, Wc, Ad, Bc, ranks, scales, lens, tasks, Hs, dYc, dXp, dA, dB, ws)
+S.allreduce(dXp, dXr)
+torch.cuda.synchronize()
+assert torch.equal(dXr, dX), "fused column-parallel backward differs from GEMM + all-reduce"
 # both ranks hold bitwise the same all-reduced tensors
 got = [None] * world
 dist.all_gather_object(got, (Y.float().cpu().numpy().tobytes(), dX.float().cpu().numpy().tobytes()))
@@ -156,6 +162,12 @@ assert err <= 2e-2, ("group column bwd dX", err)
 got = [None] * world
 dist.all_gather_object(got, dXg.float().cpu().numpy().tobytes())
 assert all(g == got[0] for g in got)
+# the group's last dX GEMM scatters (fused); == local group partial + own all-reduce, bitwise
+dXgp, dXgr = torch.empty_like(dXg), torch.empty_like(dXg)
+_lib.lobra_lora_group_bwd(Xg, Wg, Ag, Bg, ranks, scales, lens, tasks, Hg, dYg, dXgp, dAs, dBs, wsg)
+S.allreduce(dXgp, dXgr)
+torch.cuda.synchronize()
+assert torch.equal(dXgr, dXg), "fused group backward differs from GEMM + all-reduce"
 comm.destroy()
 S.destroy()
 print("SYMM_OK", rank)
