@@ -1071,6 +1071,7 @@ constexpr int Y_SMEM = Y_STAGES * Y_STAGE_BYTES + 1024 + 256;
 
 struct DyArgs {
   int width, nchunks, nitems, n128, qp;
+  int dbg_dy_only;   // tuning probe (LOBRA_DBG_DY_ONLY=1): stream dY only, skip H / B loads
   float* gpart;    // [nslots][nchunks][128][qp]
   float* bpart;    // [ndyunits][n128][qp][128]   (k_finalize layout)
   Meta meta;
@@ -1122,10 +1123,14 @@ __global__ void __launch_bounds__(256, 1)
           for (int b = 0; b < nb; ++b) {
             const int col = c * 512 + b * 128;
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
+            mbar_expect_tx(&full[stage], args.dbg_dy_only ? Y_Z_BYTES : Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
             uint8_t* st = smem + stage * Y_STAGE_BYTES;
             tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
             tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
+            if (args.dbg_dy_only) {
+              if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+              continue;
+            }
             tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], 0, sl * kTileM);
             // B_t straight from the caller's B (MN-major: q contiguous, rows = o = K)
             tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES, &mapBt, &full[stage], meta.boff[t], col);
@@ -1544,6 +1549,14 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
   a.gpart = gpart;
   a.bpart = bpart;
   a.meta = meta;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("LOBRA_DBG_DY_ONLY");
+      dbg = (e && e[0] == '1') ? 1 : 0;
+    }
+    a.dbg_dy_only = dbg;
+  }
   if (a.nitems > 0) {
     const int grid = a.nitems < num_sms ? a.nitems : num_sms;
     launch_k(k_dypass, dim3(grid), dim3(256), Y_SMEM, st, mapDY, mapH, mapBt, a);
