@@ -264,6 +264,10 @@ def _wl(lens, tasks, ranks, scales):
      [0.5, 1, 2, 4, 0.5, 1, 2, 4, 0.5, 1], 192, 320),                  # 10 tasks in one tile, odd ranks (B padding path)
     ([130, 1, 127, 256, 2], [2, 0, 1, 2, 0], [64, 64, 64], [1.0, 1.0, 1.0], 64, 128),  # rank 64, one K block
     ([300] * 3 + [7] * 20, [0, 1, 2] + [i % 3 for i in range(20)], [16, 32, 48], [2.0, 1.0, 0.5], 256, 256),
+    # 64 tasks, 2-9 tokens each, interleaved (up to ~30 task slots per 128-row tile, every
+    # pair tile's union of tasks in the K-extension), ranks cycling 4..64
+    ([2 + (i * 7) % 8 for i in range(64)], [(i * 37) % 64 for i in range(64)],
+     [4 * (1 + i % 16) for i in range(64)], [0.5 + 0.25 * (i % 4) for i in range(64)], 128, 192),
 ])
 def test_bf16_edge_cases(case):
     lens, tasks, ranks, scales, d_in, d_out = case
