@@ -126,6 +126,24 @@ class LoraLayer:
         self.flat_grad = torch.zeros(off, dtype=torch.float32, device=self.device)
         self.ws = torch.empty(0, dtype=torch.uint8, device=self.device)
 
+    def relayout(self, ranks, scales):
+        """New task set (ranks, scales) on the SAME frozen base: recompute the flat
+        adapter-gradient layout and its offsets; the caller assigns the new A / B tensors
+        ([sum r, in] / [out, sum r] local shards).  Used by the trainer when tasks join or
+        leave (P:680-684)."""
+        self.ranks = np.asarray(ranks, np.int32)
+        self.scales = np.asarray(scales, np.float32)
+        self.rsum = int(self.ranks.sum())
+        off = 0
+        for p in self.projs:
+            p.dA_off = off
+            off += self.rsum * p.d_in
+            p.dB_off = off
+            off += p.d_out * self.rsum
+            p.Hs = None
+        self.group_Hs = {}
+        self.flat_grad = torch.zeros(off, dtype=torch.float32, device=self.device)
+
     def _randn(self, shape, std, g):
         return (torch.randn(shape, generator=g, device=self.device, dtype=torch.float32) * std).to(self.dtype)
 
