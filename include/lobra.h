@@ -260,6 +260,17 @@ LOBRA_API lobra_status lobra_swiglu_fwd(int64_t n, const void* gate, const void*
                                         lobra_stream_t stream);
 LOBRA_API lobra_status lobra_swiglu_bwd(int64_t n, const void* d, const void* gate, const void* up,
                                         void* d_gate, void* d_up, lobra_stream_t stream);
+/* lobra_attn_fwd: causal attention inside every packed sequence (block-diagonal mask over
+ *   the pack; seq_lens host [num_seqs]), tcgen05 kernel.  Q [T, n_heads * 128],
+ *   K, V [T, n_kv_heads * 128] bf16 row-major (n_kv_heads | n_heads: grouped-query heads);
+ *   O [T, n_heads * 128] bf16; lse [n_heads, T] fp32 = natural-log softmax normaliser per
+ *   query (FlashAttention's varlen layout).  scale 1 / sqrt(128).  head_dim must be 128
+ *   (else LOBRA_ERR_UNSUPPORTED).  ws >= lobra_attn_workspace_bytes device bytes. */
+LOBRA_API size_t lobra_attn_workspace_bytes(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads);
+LOBRA_API lobra_status lobra_attn_fwd(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads,
+                                      int32_t n_kv_heads, int32_t head_dim, const void* Q, const void* K,
+                                      const void* V, void* O, float* lse, void* ws, size_t ws_bytes,
+                                      lobra_stream_t stream);
 /* lobra_add: C = A + B elementwise over n bf16 (n % 8 == 0; C may alias A or B): the
  * layer's last residual add. */
 LOBRA_API lobra_status lobra_add(int64_t n, const void* A, const void* B, void* C, lobra_stream_t stream);

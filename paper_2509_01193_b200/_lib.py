@@ -30,6 +30,7 @@ EXPORTED = [
     "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
     "lobra_swiglu_bwd", "lobra_add", "lobra_symm_create", "lobra_symm_open", "lobra_symm_destroy",
     "lobra_symm_data", "lobra_symm_allreduce", "lobra_comm_from_symm", "lobra_comm_attach_symm",
+    "lobra_attn_workspace_bytes", "lobra_attn_fwd",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer", "comm"]
 
@@ -170,6 +171,11 @@ def load() -> C.CDLL:
     lib.lobra_comm_from_symm.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     lib.lobra_comm_attach_symm.restype = C.c_int
     lib.lobra_comm_attach_symm.argtypes = [C.c_void_p, C.c_void_p]
+    lib.lobra_attn_workspace_bytes.restype = C.c_size_t
+    lib.lobra_attn_workspace_bytes.argtypes = [C.c_int32, _i32p, C.c_int32]
+    lib.lobra_attn_fwd.restype = C.c_int
+    lib.lobra_attn_fwd.argtypes = [C.c_int32, _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
     lib.lobra_add.restype = C.c_int
     lib.lobra_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
@@ -593,3 +599,18 @@ def lobra_comm_from_symm(symm: Symm) -> Comm:
 
 def lobra_comm_attach_symm(comm: Comm, symm: Symm | None):
     _check(load().lobra_comm_attach_symm(C.c_void_p(comm.handle), C.c_void_p(symm.ptr if symm else 0)))
+
+
+# ------------------------------------------------------------------ attention (NEXT-3)
+def lobra_attn_workspace_bytes(seq_lens, n_heads) -> int:
+    lens = _i32(seq_lens)
+    return int(load().lobra_attn_workspace_bytes(len(lens), lens.ctypes.data_as(_i32p), int(n_heads)))
+
+
+def lobra_attn_fwd(seq_lens, Q, K, V, O, lse, ws, stream=None):
+    """Causal attention per packed sequence (tcgen05): Q [T, H, 128], K, V [T, Hkv, 128],
+    O [T, H, 128], lse [H, T] (include/lobra.h)."""
+    lens = _i32(seq_lens)
+    H, D, Hkv = int(Q.shape[-2]), int(Q.shape[-1]), int(K.shape[-2])
+    _check(load().lobra_attn_fwd(len(lens), lens.ctypes.data_as(_i32p), H, Hkv, D, _ptr(Q), _ptr(K), _ptr(V),
+                                 _ptr(O), _ptr(lse), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))

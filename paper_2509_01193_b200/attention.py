@@ -8,7 +8,9 @@ causal masks (block-diagonal over the pack):
   * "cudnn": cuDNN 9 frontend SDPA forward / backward on RAGGED tensors (THD layout: the
     sequences of the pack addressed through ragged offsets, no padding copies); graphs
     are built once per (batch bucket, max-length bucket) and cached;
-  * "flash_attn": FlashAttention-2 varlen kernels (mma.sync; measured ~3x slower on B200).
+  * "flash_attn": FlashAttention-2 varlen kernels (mma.sync; measured ~3x slower on B200);
+  * "lobra": our own tcgen05 forward (lobra_attn_fwd, csrc/attn.cu) with FlashAttention-2's
+    varlen backward consuming its O and LSE.
 """
 from __future__ import annotations
 
@@ -149,6 +151,27 @@ class FlashVarlenAttention:
                                             1.0 / math.sqrt(self.D), True, -1, -1, 0.0, None, self.det)
 
 
+class LobraVarlenAttention(FlashVarlenAttention):
+    """Own tcgen05 forward (O, LSE in FlashAttention's varlen layout) + FA2 varlen backward."""
+
+    def __init__(self, n_heads: int, head_dim: int, device, deterministic=False):
+        super().__init__(n_heads, head_dim, device, deterministic)
+        from . import _lib
+        self.lib, self.H = _lib, n_heads
+        self.ws = torch.empty(0, dtype=torch.uint8, device=self.dev)
+
+    def forward(self, q, k, v, seq_lens):
+        cu = torch.from_numpy(np.concatenate([[0], np.cumsum(seq_lens)]).astype(np.int32)).to(self.dev)
+        m = int(max(seq_lens)) if len(seq_lens) else 0
+        need = self.lib.lobra_attn_workspace_bytes(seq_lens, self.H)
+        if self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+        o = torch.empty_like(q)
+        lse = torch.empty(self.H, q.shape[0], dtype=torch.float32, device=self.dev)
+        self.lib.lobra_attn_fwd(seq_lens, q, k, v, o, lse, self.ws)
+        return o, lse, (cu, m)
+
+
 def make_attention(backend: str, n_heads: int, head_dim: int, device, deterministic=False,
                    n_kv_heads: int | None = None):
     """q [T, n_heads, D]; k, v [T, n_kv_heads, D] (grouped-query attention when fewer)."""
@@ -156,4 +179,6 @@ def make_attention(backend: str, n_heads: int, head_dim: int, device, determinis
         return CudnnVarlenAttention(n_heads, head_dim, device, n_kv_heads)
     if backend == "flash_attn":
         return FlashVarlenAttention(n_heads, head_dim, device, deterministic)
+    if backend == "lobra":
+        return LobraVarlenAttention(n_heads, head_dim, device, deterministic)
     raise ValueError(f"unknown attention backend {backend!r}")

@@ -555,6 +555,18 @@ lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobr
 
 using namespace lobra;
 
+namespace lobra {
+// TMA map for other translation units (attn.cu): bf16 2D [outer, inner] row-major, 128-byte
+// swizzle; initialises the driver entry point on first use.
+lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+                                uint32_t box_inner, uint32_t box_outer) {
+  DevCtx* ctx = nullptr;
+  lobra_status s = get_ctx(&ctx);
+  if (s != LOBRA_OK) return s;
+  return make_map(map, ptr, inner, outer, box_inner, box_outer);
+}
+}  // namespace lobra
+
 extern "C" const char* lobra_last_error(void) { return lobra::g_err.c_str(); }
 extern "C" const char* lobra_version(void) { return "lobra-b200 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }
 

@@ -52,7 +52,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--fit", action="store_true")
-    ap.add_argument("--attn", default="cudnn", choices=["cudnn", "flash_attn"])
+    ap.add_argument("--attn", default="cudnn", choices=["cudnn", "flash_attn", "lobra"])
     ap.add_argument("--model", default="7b", choices=["7b", "70b"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_layer_cost.json"))
     args = ap.parse_args()
@@ -82,7 +82,8 @@ def main():
             "unit": "tokens/s", "ms_per_step": ms, "steps": args.steps, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "C2 (T=16384, 4 tasks r=16, lengths <= 4096)", "layer": f"llama2-{args.model}" + (" (GQA 64/8 heads, TP1)" if args.model == "70b" else ""),
                        "attention": {"cudnn": "cuDNN 9 ragged SDPA (library)",
-                                     "flash_attn": "flash_attn 2.8 varlen (library)"}[args.attn]},
+                                     "flash_attn": "flash_attn 2.8 varlen (library)",
+                                     "lobra": "own tcgen05 forward + flash_attn 2.8 varlen backward"}[args.attn]},
             "algorithmic_tflops": fl["total"] / (ms / 1e3) / 1e12,
             "flops_share": {k: fl[k] / fl["total"] for k in ("proj", "lora", "attn")},
             "ms_by_class": cls, "ms_attention_and_glue": ms - ours}
