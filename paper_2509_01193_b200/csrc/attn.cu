@@ -10,7 +10,7 @@
 //   warps 4-7 softmax, one query row per thread: row max of S_j (masked: key <= query and
 //            inside the sequence), p = exp2(s log2e / sqrt(D) - m), P_j to shared memory
 //            in the 128-byte-swizzled K-major layout of the next MMA's A operand, running
-//            sum l, O kept in 128 fp32 registers: o = o * 2^(m_prev - m) + P_j V_j
+//            sum l; O accumulates in TMEM (lazy rescale when the row max grows by > 2^8)
 // Outputs: O (bf16, same layout as Q) and LSE [H, T] fp32 (natural log; FlashAttention's
 // varlen layout, so its backward can consume them).
 #include <cuda.h>
@@ -55,6 +55,12 @@ struct AttnArgs {
   float* lse;                 // [H, T]
 };
 
+__device__ __forceinline__ float ex2(float x) {   // MUFU.EX2; ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint8_t* align1024a(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
@@ -75,7 +81,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* s_empty = bars + 7;     // [2]
   uint64_t* p_full = bars + 9;
   uint64_t* o_full = bars + 10;
-  uint64_t* o_empty = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -92,7 +97,6 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_init(p_full, 128);
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -141,79 +145,93 @@ __global__ void __launch_bounds__(256, 1)
       issue_s(0);
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) issue_s(j + 1);
-        mbar_wait(p_full, j & 1);
-        if (j >= 1) mbar_wait(o_empty, (j - 1) & 1);
+        mbar_wait(p_full, j & 1);   // P_j written (and O rescaled if the softmax had to)
         tc_fence_after();
         const uint32_t v0 = smem_u32(sKV + (j & 1) * 2 * A_TILE_BYTES + A_TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // K = 128 keys: P (K-major) x V (MN-major)
           const uint32_t poff = (kk >> 2) * A_BOX + (kk & 3) * 32;
           mma_bf16(tmem + 256, sdesc_sw128(p0 + poff, 16, 1024), sdesc_sw128(v0 + kk * 2048, A_BOX, 1024), id_o,
-                   kk ? 1u : 0u);
+                   (j | kk) ? 1u : 0u);   // O accumulates in TMEM over the key tiles
         }
         mma_commit(o_full);
         mma_commit(&kv_empty[j & 1]);
       }
     }
   } else if (warp >= 4) {  // ---------------- softmax / epilogue: one query row per thread
+    // O accumulates in TMEM; P is computed against a reference max m that is raised (and O, l
+    // rescaled in place) only when a tile's max exceeds it by more than 8 (log2 units, i.e.
+    // p <= 256): the final O / l is exact either way.
     const int r = (warp - 4) * 32 + lane;
     const int qpos = it.q_tile * A_TILE + r;               // position inside the sequence
     const bool qvalid = qpos < it.len;
     const uint32_t trow = ((warp - 4) * 32u) << 16;
-    float o[128];
-#pragma unroll
-    for (int i = 0; i < 128; ++i) o[i] = 0.0f;
-    float m = -INFINITY, l = 0.0f, alpha_prev = 1.0f;
+    // invalid rows (past the sequence end in its last tile) keep m = 0 and only see -inf
+    float m = qvalid ? -INFINITY : 0.0f, l = 0.0f;
+    // per-element masks only where a tile can hold masked keys: the diagonal tile and the
+    // tiles reaching past the sequence end, plus every tile of a query tile with rows past it
+    const bool tail_rows = (it.q_tile + 1) * A_TILE > it.len;
     for (int j = 0; j < nkv; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
       const int kbase = j * A_TILE;
-      // pass 1: masked row max (scaled, base 2)
-      float mx = -INFINITY;
+      float sv[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float v[32];
         tmem_ld32(tmem + trow + sb * 128 + c * 32, v);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int kpos = kbase + c * 32 + e;
-          if (kpos <= qpos && kpos < it.len) mx = fmaxf(mx, v[e] * args.scale_log2);
+        for (int e = 0; e < 32; ++e) sv[c * 32 + e] = v[e];
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[sb]);                             // S buffer free for S_{j+2}
+      if (j == nkv - 1 || tail_rows || kbase + A_TILE > it.len) {   // warp-uniform
+#pragma unroll
+        for (int e = 0; e < 128; ++e) {
+          const int kpos = kbase + e;
+          if (!(qvalid && kpos <= qpos && kpos < it.len)) sv[e] = -INFINITY;
         }
       }
-      const float m_new = qvalid ? fmaxf(m, mx) : 0.0f;
-      const float alpha = qvalid ? exp2f(m - m_new) : 1.0f;   // m = -inf at j = 0 -> 0
-      // fold the previous tile's P V (its P used the previous max)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 128; ++e) mx = fmaxf(mx, sv[e]);
+      mx *= args.scale_log2;                                  // scale > 0: max commutes
+      // the previous P V is complete (O quiescent, P buffer free) before P_j is written
       if (j >= 1) {
         mbar_wait(o_full, (j - 1) & 1);
         tc_fence_after();
+      }
+      // raise the reference max where needed; the TMEM rescale is warp-collective
+      // (tcgen05.ld / st are .sync.aligned): every lane takes part, alpha = 1 where unchanged
+      const bool raise = qvalid && (j == 0 || mx > m + 8.0f);
+      const float m_new = raise ? fmaxf(m, mx) : m;
+      const float alpha = (raise && j >= 1) ? ex2(m - m_new) : 1.0f;
+      if (j >= 1 && __any_sync(0xffffffffu, raise)) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float v[32];
           tmem_ld32(tmem + trow + 256 + c * 32, v);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + v[e];
+          for (int e = 0; e < 32; ++e) v[e] *= alpha;
+          tmem_st32(tmem + trow + 256 + c * 32, v);
         }
-        tc_fence_before();
-        mbar_arrive(o_empty);
       }
-      // pass 2: p = 2^(s - m_new), row sum, P_j (bf16) into the swizzled A-operand layout
+      l *= alpha;
+      m = m_new;
       float sum = 0.0f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(tmem + trow + sb * 128 + c * 32, v);
         float p[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const int kpos = kbase + c * 32 + e;
-          p[e] = (qvalid && kpos <= qpos && kpos < it.len) ? exp2f(v[e] * args.scale_log2 - m_new) : 0.0f;
+          p[e] = ex2(fmaf(sv[c * 32 + e], args.scale_log2, -m));   // masked: ex2(-inf) = 0
           sum += p[e];
         }
-        uint8_t* atom = sP + (c >> 1) * A_BOX + r * 128;   // 64 keys per 128-byte swizzle atom row
+        uint8_t* atom = sP + (c >> 1) * A_BOX + r * 128;     // 64 keys per 128-byte swizzle atom row
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;                // 16-byte chunk within the 128-byte row
+          const int chunk = (c & 1) * 4 + u;                 // 16-byte chunk within the 128-byte row
           uint4 w;
           w.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
           w.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
@@ -222,38 +240,33 @@ __global__ void __launch_bounds__(256, 1)
           *reinterpret_cast<uint4*>(atom + ((chunk ^ (r & 7)) << 4)) = w;
         }
       }
-      l = l * alpha + sum;
-      m = m_new;
-      alpha_prev = alpha;
+      l += sum;
       tc_fence_before();
-      mbar_arrive(&s_empty[sb]);
       fence_proxy_async_smem();   // P stores visible to the tensor core
       mbar_arrive(p_full);
     }
     mbar_wait(o_full, (nkv - 1) & 1);
     tc_fence_after();
+    const float inv = qvalid ? 1.0f / l : 0.0f;
+    const size_t tok = (size_t)it.q_row0 + r;
+    uint4* dst = reinterpret_cast<uint4*>(args.O + tok * (size_t)(args.H * 128) + it.head * 128);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       float v[32];
-      tmem_ld32(tmem + trow + 256 + c * 32, v);
+      tmem_ld32(tmem + trow + 256 + c * 32, v);            // warp-collective: every lane
+      if (qvalid) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + v[e];
-    }
-    if (qvalid) {
-      const float inv = 1.0f / l;
-      const size_t tok = (size_t)it.q_row0 + r;
-      uint4* dst = reinterpret_cast<uint4*>(args.O + tok * (size_t)(args.H * 128) + it.head * 128);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        uint4 w;
-        w.x = pack_bf16x2(o[u * 8 + 0] * inv, o[u * 8 + 1] * inv);
-        w.y = pack_bf16x2(o[u * 8 + 2] * inv, o[u * 8 + 3] * inv);
-        w.z = pack_bf16x2(o[u * 8 + 4] * inv, o[u * 8 + 5] * inv);
-        w.w = pack_bf16x2(o[u * 8 + 6] * inv, o[u * 8 + 7] * inv);
-        dst[u] = w;
+        for (int u = 0; u < 4; ++u) {
+          uint4 w;
+          w.x = pack_bf16x2(v[u * 8 + 0] * inv, v[u * 8 + 1] * inv);
+          w.y = pack_bf16x2(v[u * 8 + 2] * inv, v[u * 8 + 3] * inv);
+          w.z = pack_bf16x2(v[u * 8 + 4] * inv, v[u * 8 + 5] * inv);
+          w.w = pack_bf16x2(v[u * 8 + 6] * inv, v[u * 8 + 7] * inv);
+          dst[c * 4 + u] = w;
+        }
       }
-      args.lse[(size_t)it.head * args.T + tok] = (m + log2f(l)) * 0.69314718055994531f;
     }
+    if (qvalid) args.lse[(size_t)it.head * args.T + tok] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
