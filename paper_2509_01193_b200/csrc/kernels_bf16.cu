@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <utility>
+#include <vector>
+#include <cstdio>
 
 #include "lora_internal.h"
 #include "ptx.cuh"
@@ -562,7 +564,8 @@ __global__ void __launch_bounds__(256, 1)
           if (kb >= nk) break;
           const int nkb = args.interleave ? 1 : min(R_KB, kb1 - kk);
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + ns * R_V_BYTES));
+          const bool nov = (args.dbg_no_mma & 2) != 0;   // probe: skip the adapter boxes
+          mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + (nov ? 0 : ns) * R_V_BYTES));
           uint8_t* st = smem + stage * R_STAGE_BYTES;
           if (args.prefetch && !args.interleave)   // stream the Z tile into L2 ahead
             for (int j = 0; j < nkb; ++j)
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(256, 1)
                 tma_prefetch_2d(&mapZ, (kb + j + args.prefetch) * 64, m * kTileM);
           for (int j = 0; j < nkb; ++j)
             tma_load_2d(st + j * R_A_BYTES, &mapZ, &full[stage], (kb + j) * 64, m * kTileM);
-          for (int i = 0; i < ns; ++i) {
+          for (int i = 0; i < (nov ? 0 : ns); ++i) {
             const int t = meta.slot_task[s0 + i];
             for (int j = 0; j < nkb; ++j) {
               uint8_t* vd = st + R_KB * R_A_BYTES + (i * R_KB + j) * R_V_BYTES;
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t st0 = smem_u32(smem + stage * R_STAGE_BYTES);
-          if (args.dbg_no_mma) {   // tuning probe: pure TMA streaming, no tensor work
+          if (args.dbg_no_mma & 1) {   // tuning probe: pure TMA streaming, no tensor work
             mbar_arrive(&empty[stage]);
             if (++stage == R_STAGES) stage = 0, phase ^= 1;
             continue;
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(256, 1)
       const int ns = min(R_P, s_end - s0);
       mbar_wait(tfull, p & 1);
       tc_fence_after();
-      for (int i = 0; i < ns; ++i) {
+      for (int i = 0; i < ((args.dbg_no_mma & 4) ? 0 : ns); ++i) {   // bit 2: probe, no output
         const int s = s0 + i;
         const int ts = meta.slot_task[s];
         float v[64];
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       mbar_arrive(tempty);
     }
-    if (args.nsplit > 1) {
+    if (args.nsplit > 1 && !(args.dbg_no_mma & 4)) {
       // deterministic split-K reduction by the last CTA of this tile to finish
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -905,6 +908,196 @@ __global__ void __launch_bounds__(288, 1)
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc<128>(tmem);
+  }
+}
+
+// =====================================================================================
+// Forward shrink, one CTA per 128-row tile and the whole K (no split-K, no partials):
+// slot[s][row][q] = s_t sum_k X[row][k] A(q, k).  Persistent over tiles when there are more
+// tiles than SMs.  A stage is SH_KB adjacent 64-column K blocks of the X tile (2 x 16 KB
+// boxes) plus, per slot of the pass, the matching qv-row boxes of the adapter operand
+// (qv = rows the tile's tasks need: the padded rank, or np*qp for a projection group; rows
+// past a task's rank are masked in the epilogue).  The stage count fills the shared memory
+// (one CTA per SM), so ~200 KB of X is in flight per SM: HBM-bound streaming at the copy
+// roofline needs bytes in flight, not more CTAs (profiles/r1e_shrink.md).
+// Accumulators: two TMEM buffers of SH_P x 64 columns, so the epilogue of one tile overlaps
+// the streaming of the next.
+// =====================================================================================
+constexpr int SH_KB = 2, SH_P = 4;
+struct ShrinkArgs {
+  int K, qv, stages, stage_bytes, P;
+  int per_slot;   // 1: one work item per slot (X tile re-read for every task of a mixed tile;
+                  //    equal work per CTA, used when the slots fit in one wave), 0: per tile
+  __nv_bfloat16* out;
+  unsigned long long* ts;   // probe (LOBRA_DBG_SHRINK_TS): per CTA globaltimer stamps, else null
+  Meta meta;
+};
+// work item w -> tile m and its slot range
+__device__ __forceinline__ void shrink_item(const Meta& meta, int per_slot, int w, int& m, int& s_begin,
+                                            int& s_end) {
+  if (per_slot) {
+    m = meta.slot_tile[w], s_begin = w, s_end = w + 1;
+  } else {
+    m = w, s_begin = meta.tile_slot_off[w], s_end = meta.tile_slot_off[w + 1];
+  }
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(256, 1)
+    k_shrink(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
+             const ShrinkArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int S = args.stages, SB = args.stage_bytes, P = args.P, qv = args.qv;
+  const int vbox = qv * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
+  uint64_t* empty = full + 8;
+  uint64_t* tfull = empty + 8;      // [2]
+  uint64_t* tempty = tfull + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+  const int nk = (args.K + 63) / 64;
+  const int nitems = args.per_slot ? meta.nslots : meta.ntiles;
+
+  if (warp == 0 && lane == 0) tma_prefetch(&mapZ), tma_prefetch(&mapV);
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&tfull[b], 1), mbar_init(&tempty[b], 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (args.ts && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    args.ts[blockIdx.x * 8 + 0] = gtimer();
+    args.ts[blockIdx.x * 8 + 5] = smid;
+    args.ts[blockIdx.x * 8 + 6] = args.per_slot ? 1 : meta.tile_slot_off[blockIdx.x + 1] - meta.tile_slot_off[blockIdx.x];
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        int m, s_begin, s_end;
+        shrink_item(meta, args.per_slot, w, m, s_begin, s_end);
+        for (int s0 = s_begin; s0 < s_end; s0 += P) {
+          const int ns = min(P, s_end - s0);
+          for (int kb = 0; kb < nk; kb += SH_KB) {
+            const int nkb = min(SH_KB, nk - kb);
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + ns * vbox));
+            uint8_t* st = smem + stage * SB;
+            for (int j = 0; j < nkb; ++j)
+              tma_load_2d(st + j * R_A_BYTES, &mapZ, &full[stage], (kb + j) * 64, m * kTileM);
+            // V of K block j: the ns slots' qv-row boxes back to back = ONE K-major operand
+            // of ns*qv rows (8-row groups 1024 B apart), so one MMA covers every slot
+            for (int i = 0; i < ns; ++i) {
+              const int row0 = meta.roff[meta.slot_task[s0 + i]];
+              for (int j = 0; j < nkb; ++j)
+                tma_load_2d(st + SH_KB * R_A_BYTES + (j * P + i) * vbox, &mapV, &full[stage],
+                            (kb + j) * 64, row0);
+            }
+            if (++stage == S) stage = 0, phase ^= 1;
+          }
+        }
+      }
+      if (args.ts) args.ts[blockIdx.x * 8 + 1] = gtimer();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;   // (tile, pass) counter -> accumulator buffer it & 1
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        int m, s_begin, s_end;
+        shrink_item(meta, args.per_slot, w, m, s_begin, s_end);
+        for (int s0 = s_begin; s0 < s_end; s0 += P, ++it) {
+          const int ns = min(P, s_end - s0);
+          const uint32_t id = idesc_bf16(128, ns * qv, false, false);   // slot i: columns [i qv, (i+1) qv)
+          const int b = it & 1;
+          mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t acc = tmem + b * 256;
+          for (int kb = 0; kb < nk; kb += SH_KB) {
+            const int nkb = min(SH_KB, nk - kb);
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t st0 = smem_u32(smem + stage * SB);
+            for (int j = 0; j < nkb; ++j) {
+              const uint32_t a0 = st0 + j * R_A_BYTES;
+              const uint32_t b0 = st0 + SH_KB * R_A_BYTES + j * P * vbox;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(acc, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), id,
+                         (kb != 0 || j != 0 || k != 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == S) stage = 0, phase ^= 1;
+          }
+          mma_commit(&tfull[b]);
+        }
+      }
+      if (args.ts) args.ts[blockIdx.x * 8 + 2] = gtimer();
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;
+    const int lrow = q * 32 + lane;
+    if (blockIdx.x == 0) {   // the all-zero slot (index nslots) used by the 2-CTA GEMM
+      float z[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) z[j] = 0.0f;
+      store_slot_row(args.out, meta.nslots, lrow, z, 0.0f, 0);
+    }
+    int it = 0;
+    bool first = true;
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+      int m, s_begin, s_end;
+      shrink_item(meta, args.per_slot, w, m, s_begin, s_end);
+      const int row = m * kTileM + lrow;
+      const int my_task = row < meta.T ? row_task(meta, row) : -1;
+      for (int s0 = s_begin; s0 < s_end; s0 += P, ++it) {
+        const int ns = min(P, s_end - s0);
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
+        if (args.ts && first && lrow == 0) args.ts[blockIdx.x * 8 + 3] = gtimer();
+        first = false;
+        for (int i = 0; i < ns; ++i) {
+          const int s = s0 + i;
+          const int ts = meta.slot_task[s];
+          float v[64];
+          const uint32_t ta = tmem + ((q * 32u) << 16) + b * 256 + i * qv;
+          tmem_ld32(ta, *reinterpret_cast<float(*)[32]>(v));
+          if (qv > 32) tmem_ld32(ta + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+          else {
+#pragma unroll
+            for (int j = 32; j < 64; ++j) v[j] = 0.0f;
+          }
+          const bool mine = ts == my_task;
+          store_slot_row(args.out, s, lrow, v, mine ? meta.scales[ts] : 0.0f, mine ? meta.ranks[ts] : 0);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+    }
+  }
+  __syncthreads();
+  if (args.ts && threadIdx.x == 0) args.ts[blockIdx.x * 8 + 4] = gtimer();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -1452,6 +1645,8 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   {
     const char* e = getenv("LOBRA_DBG_RP_NOMMA");
     a.dbg_no_mma = (e && e[0] == '1') ? 1 : 0;
+    // LOBRA_DBG_RP: probe bit mask (1 no MMA, 2 no adapter boxes, 4 no output / reduction)
+    if (const char* d = getenv("LOBRA_DBG_RP")) a.dbg_no_mma = atoi(d);
     const char* f = getenv("LOBRA_RP_PREFETCH");
     a.prefetch = f ? atoi(f) : 0;
     const char* g = getenv("LOBRA_RP_INTERLEAVE");
@@ -1480,6 +1675,75 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
     case 9: launch_rp<true, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
     case 10: launch_rp<false, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
     default: launch_rp<true, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
+  }
+}
+
+bool shrink_applies(int ntiles, int num_sms) {
+  // enough tiles to keep >= 3/4 of the SMs streaming; else the split-K k_rowproj
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_SHRINK");   // 0: always k_rowproj (A/B)
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0 && 4 * ntiles >= 3 * num_sms;
+}
+
+void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
+                   __nv_bfloat16* slots, int num_sms, cudaStream_t st) {
+  constexpr int kMaxSmem = 232448;
+  ShrinkArgs a;
+  a.K = K;
+  a.qv = meta.qp;
+  a.per_slot = meta.nslots <= num_sms ? 1 : 0;
+  if (const char* e = getenv("LOBRA_SHRINK_PER_TILE")) a.per_slot = (e[0] == '1') ? 0 : a.per_slot;
+  a.P = a.per_slot ? 1 : std::max(1, std::min(SH_P, meta.max_slots_per_tile));
+  a.stage_bytes = SH_KB * (R_A_BYTES + a.P * a.qv * 128);
+  a.stages = std::min(8, (kMaxSmem - 1024 - 256) / a.stage_bytes);
+  a.out = slots;
+  a.meta = meta;
+  a.ts = nullptr;
+  {
+    static unsigned long long* ts = nullptr;
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("LOBRA_DBG_SHRINK_TS");
+      dbg = (e && e[0] == '1') ? 1 : 0;
+      if (dbg) cudaMalloc(&ts, 8 * 1024 * sizeof(unsigned long long));
+    }
+    a.ts = ts;
+  }
+  const int smem = a.stages * a.stage_bytes + 1024 + 256;
+  static int init = 0;
+  if (init < smem) {
+    cudaFuncSetAttribute(k_shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    init = kMaxSmem;
+  }
+  const int grid = std::max(1, std::min(a.per_slot ? meta.nslots : meta.ntiles, num_sms));
+  launch_k(k_shrink, dim3(grid), dim3(256), smem, st, mapZ, mapV, a);
+  if (a.ts) {   // probe: per-CTA phase times (us from the earliest CTA start)
+    std::vector<unsigned long long> h(8 * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), a.ts, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[8 * c]);
+    double mx[5] = {0}, sm[5] = {0};
+    for (int c = 0; c < grid; ++c)
+      for (int k = 0; k < 5; ++k) {
+        const double v = (h[8 * c + k] - t0) * 1e-3;
+        mx[k] = std::max(mx[k], v);
+        sm[k] += v / grid;
+      }
+    static int dumped = 0;
+    if (dumped++ == 5) {
+      fprintf(stderr, "shrink per-CTA: cta smid done_us\n");
+      for (int c = 0; c < grid; ++c)
+        fprintf(stderr, "CTA %d sm %llu ns %llu start %.1f prod %.1f mma %.1f epi %.1f end %.1f\n", c, h[8 * c + 5],
+                h[8 * c + 6], (h[8 * c] - t0) * 1e-3, (h[8 * c + 1] - t0) * 1e-3, (h[8 * c + 2] - t0) * 1e-3,
+                (h[8 * c + 3] - t0) * 1e-3, (h[8 * c + 4] - t0) * 1e-3);
+    }
+    fprintf(stderr, "shrink ts (us; avg/max over %d CTAs): start %.1f/%.1f producer-done %.1f/%.1f "
+            "mma-done %.1f/%.1f epi-start %.1f/%.1f end %.1f/%.1f\n", grid, sm[0], mx[0], sm[1], mx[1],
+            sm[2], mx[2], sm[3], mx[3], sm[4], mx[4]);
   }
 }
 

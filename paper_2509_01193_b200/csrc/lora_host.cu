@@ -638,7 +638,12 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mW, W, in, out, 64, bn)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mB, Bop, L.ld8, out, 64, bn)) != LOBRA_OK) return s;
-    if (rowproj_uses_ld()) {
+    if (shrink_applies(P.ntiles, ctx->num_sms)) {
+      CUtensorMap mAk;
+      if ((s = make_map(&mAk, ad->A, in, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
+      Prof p_(LOBRA_K_ROWPROJ, st);
+      launch_shrink(mX, mAk, in, meta, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st);
+    } else if (rowproj_uses_ld()) {
       CUtensorMap mAk;
       if ((s = make_map(&mAk, ad->A, in, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
       Prof p_(LOBRA_K_ROWPROJ, st);
@@ -979,8 +984,13 @@ extern "C" lobra_status lobra_lora_group_fwd(const lobra_group_problem* g, const
   if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
   if ((s = make_map(&mAg, Ag, in, (uint64_t)P.ntasks * np * P.qp, 64, 64)) != LOBRA_OK) return s;
   if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
-  {
+  if (shrink_applies(P.ntiles, ctx->num_sms)) {
     // a1: every projection's H_s from ONE pass over X (band p = columns [p qp, (p+1) qp))
+    CUtensorMap mAgk;
+    if ((s = make_map(&mAgk, Ag, in, (uint64_t)P.ntasks * np * P.qp, 64, np * P.qp)) != LOBRA_OK) return s;
+    Prof p_(LOBRA_K_ROWPROJ, st);
+    launch_shrink(mX, mAgk, in, meta_g, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st);
+  } else {
     Prof p_(LOBRA_K_ROWPROJ, st);
     launch_rowproj(false, mX, mAg, in, meta_g, static_cast<__nv_bfloat16*>(Hs),
                    reinterpret_cast<float*>(w + L.rpart), reinterpret_cast<int*>(w + L.counters), st);

@@ -74,6 +74,12 @@ int rowproj_splits(int ntiles, int K);
 void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV, int K,
                     const Meta& meta, __nv_bfloat16* slots, float* partial, int* counters,
                     cudaStream_t st);
+// Forward shrink without split-K (one CTA per tile, persistent, whole K): used when the
+// tiles fill >= 3/4 of the SMs (LOBRA_SHRINK=0 disables).  mapV: the adapter operand
+// (A_cat, or the packed group A) with box {64, meta.qp}.
+bool shrink_applies(int ntiles, int num_sms);
+void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
+                   __nv_bfloat16* slots, int num_sms, cudaStream_t st);
 // LDGSTS-producer variant (default; LOBRA_RP_TMA=1 selects the TMA-producer kernel):
 // Z raw [T, K]; mapVk K-major adapter operand, box {64, qp} (A_cat forward, B^T backward).
 bool rowproj_uses_ld();
