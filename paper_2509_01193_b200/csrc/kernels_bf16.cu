@@ -1306,21 +1306,22 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-        const int u = item / args.nchunks, c = item % args.nchunks;
+      for (int u = meta.dy_cta_off[blockIdx.x]; u < meta.dy_cta_off[blockIdx.x + 1]; ++u) {
+        const int c = meta.dy_unit_chunk[u];
         const int t = meta.dy_unit_task[u];
         const int nb = min(4, args.n128 - c * 4);
+        if (nb <= 0) continue;   // a chunk past this projection's width (group of unequal outs)
         for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k) {
           const int sl = meta.task_slots[k];
           const int tile = meta.slot_tile[sl];
           for (int b = 0; b < nb; ++b) {
             const int col = c * 512 + b * 128;
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], args.dbg_dy_only ? Y_Z_BYTES : Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
+            mbar_expect_tx(&full[stage], (args.dbg_dy_only & 1) ? Y_Z_BYTES : Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
             uint8_t* st = smem + stage * Y_STAGE_BYTES;
             tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
             tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
-            if (args.dbg_dy_only) {
+            if (args.dbg_dy_only & 1) {
               if (++stage == Y_STAGES) stage = 0, phase ^= 1;
               continue;
             }
@@ -1340,9 +1341,10 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int gcount = 0, it = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
-        const int u = item / args.nchunks, c = item % args.nchunks;
+      for (int u = meta.dy_cta_off[blockIdx.x]; u < meta.dy_cta_off[blockIdx.x + 1]; ++u) {
+        const int c = meta.dy_unit_chunk[u];
         const int nb = min(4, args.n128 - c * 4);
+        if (nb <= 0) continue;
         mbar_wait(bempty, (it & 1) ^ 1);
         tc_fence_after();
         bool first_slot = true;
@@ -1357,18 +1359,22 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t z0 = smem_u32(smem + stage * Y_STAGE_BYTES);
             const uint32_t h0 = z0 + Y_Z_BYTES;
             const uint32_t t0 = h0 + Y_H_BYTES;
+            if (!(args.dbg_dy_only & 2)) {   // probe bit 1: skip the dB MMAs
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)   // dB[b] += dY^T H   (K = 128 tokens)
-              mma_bf16(tmem + b * 64, sdesc_sw128(z0 + kk * 2048, 16384, 1024),
-                       sdesc_sw128(h0 + kk * 2048, 8192, 1024), id_b,
-                       (first_slot && kk == 0) ? 0u : 1u);
+              for (int kk = 0; kk < 8; ++kk)   // dB[b] += dY^T H   (K = 128 tokens)
+                mma_bf16(tmem + b * 64, sdesc_sw128(z0 + kk * 2048, 16384, 1024),
+                         sdesc_sw128(h0 + kk * 2048, 8192, 1024), id_b,
+                         (first_slot && kk == 0) ? 0u : 1u);
+            }
+            if (!(args.dbg_dy_only & 4)) {   // probe bit 2: skip the G MMAs
 #pragma unroll
-            for (int j = 0; j < 2; ++j)      // G += dY[:, 64 cols] B^T[qp, 64 cols]^T
+              for (int j = 0; j < 2; ++j)      // G += dY[:, 64 cols] B^T[qp, 64 cols]^T
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_bf16(dg, sdesc_sw128(z0 + j * 16384 + kk * 32, 16, 1024),
-                         sdesc_sw128(t0 + j * bt_box + kk * 2048, 8192, 1024), id_g,
-                         (b == 0 && j == 0 && kk == 0) ? 0u : 1u);
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_bf16(dg, sdesc_sw128(z0 + j * 16384 + kk * 32, 16, 1024),
+                           sdesc_sw128(t0 + j * bt_box + kk * 2048, 8192, 1024), id_g,
+                           (b == 0 && j == 0 && kk == 0) ? 0u : 1u);
+            }
             mma_commit(&empty[stage]);
             if (++stage == Y_STAGES) stage = 0, phase ^= 1;
           }
@@ -1376,15 +1382,17 @@ __global__ void __launch_bounds__(256, 1)
           first_slot = false;
         }
         mma_commit(bfull);
+        ++it;
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
     const uint32_t q = warp - 4;
     const int lr = q * 32 + lane;    // row of the tile (G) / column of the sub-block (dB)
     int gcount = 0, it = 0;
-    for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
-      const int u = item / args.nchunks, c = item % args.nchunks;
+    for (int u = meta.dy_cta_off[blockIdx.x]; u < meta.dy_cta_off[blockIdx.x + 1]; ++u) {
+      const int c = meta.dy_unit_chunk[u];
       const int nb = min(4, args.n128 - c * 4);
+      if (nb <= 0) continue;
       const int t = meta.dy_unit_task[u];
       const int rp = rpad16(meta.ranks[t]);
       for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k, ++gcount) {
@@ -1409,7 +1417,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(bfull, it & 1);
       tc_fence_after();
       for (int b = 0; b < nb; ++b) {
-        float* dst = args.bpart + ((size_t)(u * args.n128 + c * 4 + b) * meta.qp) * 128 + lr;
+        float* dst = args.bpart + ((size_t)(u * 4 + b) * meta.qp) * 128 + lr;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           if (h * 32 >= rp) break;
@@ -1422,6 +1430,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_fence_before();
       mbar_arrive(bempty);
+      ++it;
     }
   }
   __syncthreads();
@@ -1529,15 +1538,59 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
   int t = 0;
   while (meta.roff[t + 1] <= rq) ++t;
   const int q = rq - meta.roff[t];
-  const int* tuo = (mode == 1 && meta.use_dy_units) ? meta.dy_task_unit_off : meta.task_unit_off;
-  const int u0 = tuo[t], u1 = tuo[t + 1];
+  const bool dyseg = mode == 1 && meta.use_dy_units;
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
     const int c = col >> 7, ci = col & 127;
     float s = 0.0f;
-    for (int u = u0; u < u1; ++u)
-      s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + meta.band + q) * 128 + ci);
+    if (dyseg) {   // fused dY pass: segments of (t, 512-column chunk), [seg][4][qp][128]
+      const int tc = t * meta.dy_nch + (col >> 9);
+      for (int u = meta.dy_task_unit_off[tc]; u < meta.dy_task_unit_off[tc + 1]; ++u)
+        s += __ldg(partial + ((size_t)(u * 4 + (c & 3)) * meta.qp + meta.band + q) * 128 + ci);
+    } else {
+      for (int u = meta.task_unit_off[t]; u < meta.task_unit_off[t + 1]; ++u)
+        s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + meta.band + q) * 128 + ci);
+    }
     float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
     *dst = accumulate ? *dst + s : s;
+  }
+}
+
+// Several finalizations in ONE launch (blockIdx.z = job): the dA and dB of a projection, or
+// of every projection of a group.  Same fixed summation order as k_finalize; the unit loads
+// are issued 8 at a time (independent) before the in-order sum.
+__global__ void k_finalize_multi(const FinJobs jobs, const Meta meta) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const FinJob& J = jobs.j[blockIdx.z];
+  const int rq = blockIdx.y;
+  int t = 0;
+  while (meta.roff[t + 1] <= rq) ++t;
+  const int q = rq - meta.roff[t];
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < J.width; col += gridDim.x * blockDim.x) {
+    const int c = col >> 7, ci = col & 127;
+    int u0, u1;
+    size_t base, ustride;
+    if (J.dy) {   // fused dY pass: segments of (t, 512-column chunk), [seg][4][qp][128]
+      const int tc = t * J.dy_nch + (col >> 9);
+      u0 = J.uoff[tc], u1 = J.uoff[tc + 1];
+      base = ((size_t)(c & 3) * J.qp + J.band + q) * 128 + ci;
+      ustride = (size_t)4 * J.qp * 128;
+    } else {
+      u0 = J.uoff[t], u1 = J.uoff[t + 1];
+      base = ((size_t)c * J.qp + J.band + q) * 128 + ci;
+      ustride = (size_t)J.nchunks * J.qp * 128;
+    }
+    float s = 0.0f;
+    for (int u = u0; u < u1; u += 8) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = (u + i < u1) ? __ldg(J.partial + base + (size_t)(u + i) * ustride) : 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (u + i < u1) s += v[i];
+    }
+    float* dst = (J.mode == 0) ? J.out + (long long)rq * J.ld + col : J.out + (long long)col * meta.rsum + rq;
+    *dst = J.accumulate ? *dst + s : s;
   }
 }
 
@@ -1818,13 +1871,12 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
     if (dbg < 0) {
       const char* e = getenv("LOBRA_DBG_DY_ONLY");
       dbg = (e && e[0] == '1') ? 1 : 0;
+      // LOBRA_DBG_DY: probe bit mask (1 dY only, 2 no dB MMAs, 4 no G MMAs)
+      if (const char* f = getenv("LOBRA_DBG_DY")) dbg = atoi(f);
     }
     a.dbg_dy_only = dbg;
   }
-  if (a.nitems > 0) {
-    const int grid = a.nitems < num_sms ? a.nitems : num_sms;
-    launch_k(k_dypass, dim3(grid), dim3(256), Y_SMEM, st, mapDY, mapH, mapBt, a);
-  }
+  if (meta.ndyunits > 0) launch_k(k_dypass, dim3(meta.ndycta), dim3(256), Y_SMEM, st, mapDY, mapH, mapBt, a);
   launch_k(k_gfin, dim3(num_sms * 2), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
 }
 
@@ -1916,6 +1968,15 @@ void launch_finalize(int mode, const float* partial, int width, const Meta& meta
   dim3 grid((width + 255) / 256, meta.rsum);
   launch_k(k_finalize, grid, dim3(256), 0, st, mode, partial, width, (width + 127) / 128, meta, out,
            ld, accumulate);
+}
+
+void launch_finalize_multi(const FinJob* jobs, int n, const Meta& meta, cudaStream_t st) {
+  if (meta.rsum == 0 || n <= 0) return;
+  FinJobs J{};
+  int wmax = 1;
+  for (int i = 0; i < n && i < kMaxFinJobs; ++i) J.j[i] = jobs[i], wmax = std::max(wmax, jobs[i].width);
+  J.n = std::min(n, kMaxFinJobs);
+  launch_k(k_finalize_multi, dim3((wmax + 255) / 256, meta.rsum, J.n), dim3(256), 0, st, J, meta);
 }
 
 void launch_zero_f32(float* p, long long n, cudaStream_t st) {

@@ -231,12 +231,19 @@ struct Plan {
   // offsets (in int32 words) of each array inside buf
   int o_seg_off, o_seg_task, o_tile_slot_off, o_slot_task, o_slot_tile, o_task_slot_off,
       o_task_slots, o_unit_task, o_unit_s0, o_unit_s1, o_task_unit_off, o_ranks, o_roff, o_boff,
-      o_dy_unit_task, o_dy_unit_s0, o_dy_unit_s1, o_dy_task_unit_off,
+      
       o_scales, o_ranks_g, o_roff_g;
   int np = 1;       // projections sharing the slots (projection group)
   int ld8 = 0;      // row stride of the B operand the kernels read (rsum if direct)
   bool bdirect = true;
   int nseg = 0, ntiles = 0, nslots = 0, nunits = 0, max_slots = 0, qp = 16, ndyunits = 0;
+  // fused dY pass schedules, one per distinct output width (a projection group's k/v can be
+  // narrower than q): CTAs of the static schedule, 512-column chunks, segment arrays
+  struct DySet {
+    int width = 0, ncta = 1, nch = 1, nseg = 0;
+    int o_task = 0, o_s0 = 0, o_s1 = 0, o_off = 0, o_chunk = 0, o_cta = 0;
+  };
+  std::vector<DySet> dy;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -275,7 +282,7 @@ lobra_status validate(const lobra_problem* prob, const lobra_batch* b, const lob
 }
 
 void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int dy_width,
-                int num_sms, Plan& P, int np = 1) {
+                int num_sms, Plan& P, int np = 1, const std::vector<int>& dy_widths = {}) {
   const int n = b->num_seqs, G = ad->num_tasks;
   P.ntasks = G;
   P.np = np;
@@ -332,23 +339,67 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     task_unit_off[t + 1] = (int)unit_task.size();
   }
   P.nunits = (int)unit_task.size();
-  // units of the fused dY pass: 512-column items, ~4 equal items per SM
-  std::vector<int> dy_task, dy_s0, dy_s1, dy_off(G + 1, 0);
-  {
-    const int nch = std::max(1, (dy_width + 511) / 512);
-    const double per_dy = std::max(1.0, (double)P.nslots * nch / (4.0 * std::max(num_sms, 1)));
+  // segments of the fused dY pass: the (task, 512-column chunk, slot) entries in that order
+  // are cut into one contiguous range of equal length per CTA (a static balanced schedule:
+  // every entry streams one 128 x 512 dY block), and each range into segments of equal
+  // (task, chunk) -- a segment accumulates its dB chunk over its slots in TMEM and writes one
+  // partial; the segments of one (task, chunk) are consecutive (k_finalize sums them in order).
+  // The schedule depends only on (batch, width), so a projection group reduces in exactly the
+  // order of the single-projection calls.
+  struct DyVecs {
+    std::vector<int> task, s0, s1, chunk, off, cta_off{0};
+    int ncta = 1, nch = 1;
+  };
+  auto build_dy = [&](int width) {
+    DyVecs v;
+    const int nch = std::max(1, (width + 511) / 512);
+    long long W = 0;
+    for (int t = 0; t < G; ++t) W += (long long)(task_slot_off[t + 1] - task_slot_off[t]) * nch;
+    const int ncta = (int)std::max<long long>(1, std::min<long long>(std::max(num_sms, 1), W));
+    v.off.assign((size_t)G * nch + 1, 0);
+    long long e = 0;   // entry index in (task, chunk, slot) order
+    int cta = 0;
+    auto cta_end = [&](int c) { return (long long)W * (c + 1) / ncta; };
     for (int t = 0; t < G; ++t) {
-      const int n_t = task_slot_off[t + 1] - task_slot_off[t];
-      const int nu = n_t ? std::max(1, (int)std::lround(n_t / per_dy)) : 0;
-      for (int u = 0; u < nu; ++u) {
-        dy_task.push_back(t);
-        dy_s0.push_back(task_slot_off[t] + (int)((long long)n_t * u / nu));
-        dy_s1.push_back(task_slot_off[t] + (int)((long long)n_t * (u + 1) / nu));
+      const int k0 = task_slot_off[t], k1 = task_slot_off[t + 1];
+      for (int c = 0; c < nch; ++c) {
+        int k = k0;
+        while (k < k1) {
+          while (cta < ncta - 1 && e >= cta_end(cta)) {
+            v.cta_off.push_back((int)v.task.size());
+            ++cta;
+          }
+          const int take = (int)std::min<long long>(k1 - k, cta_end(cta) - e);
+          v.task.push_back(t), v.chunk.push_back(c);
+          v.s0.push_back(k), v.s1.push_back(k + take);
+          k += take, e += take;
+        }
+        v.off[(size_t)t * nch + c + 1] = (int)v.task.size();
       }
-      dy_off[t + 1] = (int)dy_task.size();
     }
+    while ((int)v.cta_off.size() < ncta + 1) v.cta_off.push_back((int)v.task.size());
+    v.ncta = ncta;
+    v.nch = nch;
+    return v;
+  };
+  std::vector<int> widths = dy_widths;
+  if (widths.empty()) widths.push_back(dy_width);
+  std::vector<DyVecs> dyv;
+  P.dy.clear();
+  P.ndyunits = 0;
+  for (int wdt : widths) {
+    bool seen = false;
+    for (const auto& d : P.dy) seen = seen || d.width == wdt;
+    if (seen) continue;
+    dyv.push_back(build_dy(wdt));
+    Plan::DySet ds;
+    ds.width = wdt;
+    ds.ncta = dyv.back().ncta;
+    ds.nch = dyv.back().nch;
+    ds.nseg = (int)dyv.back().task.size();
+    P.ndyunits = std::max(P.ndyunits, ds.nseg);
+    P.dy.push_back(ds);
   }
-  P.ndyunits = (int)dy_task.size();
   std::vector<int> roff(G + 1, 0);
   for (int t = 0; t < G; ++t) roff[t + 1] = roff[t] + ad->ranks[t];
   P.rsum = roff[G];
@@ -373,10 +424,14 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   P.o_unit_s0 = put(unit_s0);
   P.o_unit_s1 = put(unit_s1);
   P.o_task_unit_off = put(task_unit_off);
-  P.o_dy_unit_task = put(dy_task);
-  P.o_dy_unit_s0 = put(dy_s0);
-  P.o_dy_unit_s1 = put(dy_s1);
-  P.o_dy_task_unit_off = put(dy_off);
+  for (size_t i = 0; i < P.dy.size(); ++i) {
+    P.dy[i].o_task = put(dyv[i].task);
+    P.dy[i].o_s0 = put(dyv[i].s0);
+    P.dy[i].o_s1 = put(dyv[i].s1);
+    P.dy[i].o_off = put(dyv[i].off);
+    P.dy[i].o_chunk = put(dyv[i].chunk);
+    P.dy[i].o_cta = put(dyv[i].cta_off);
+  }
   P.o_ranks = put(std::vector<int>(ad->ranks, ad->ranks + G));
   P.o_roff = put(roff);
   std::vector<int> boff(G + 1, 0);
@@ -393,6 +448,27 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   for (int t = 0; t < G; ++t) rog[t + 1] = rog[t] + np * P.qp;
   P.o_ranks_g = put(rg);
   P.o_roff_g = put(rog);
+}
+
+// point the fused dY pass fields of `m` at the schedule built for output width `width`
+void set_dy(Meta& m, const Plan& P, const void* dev_base, int width) {
+  const int32_t* d = reinterpret_cast<const int32_t*>(dev_base);
+  const Plan::DySet* ds = P.dy.empty() ? nullptr : &P.dy[0];
+  for (const auto& x : P.dy)
+    if (x.width == width) ds = &x;
+  if (!ds) {
+    m.ndycta = 0, m.dy_nch = 1, m.ndyunits = 0;
+    return;
+  }
+  m.ndyunits = ds->nseg;
+  m.ndycta = ds->ncta;
+  m.dy_nch = ds->nch;
+  m.dy_unit_task = d + ds->o_task;
+  m.dy_unit_s0 = d + ds->o_s0;
+  m.dy_unit_s1 = d + ds->o_s1;
+  m.dy_task_unit_off = d + ds->o_off;
+  m.dy_unit_chunk = d + ds->o_chunk;
+  m.dy_cta_off = d + ds->o_cta;
 }
 
 Meta device_meta(const Plan& P, const void* dev_base) {
@@ -420,10 +496,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.task_unit_off = d + P.o_task_unit_off;
   m.ndyunits = P.ndyunits;
   m.use_dy_units = 0;
-  m.dy_unit_task = d + P.o_dy_unit_task;
-  m.dy_unit_s0 = d + P.o_dy_unit_s0;
-  m.dy_unit_s1 = d + P.o_dy_unit_s1;
-  m.dy_task_unit_off = d + P.o_dy_task_unit_off;
+  set_dy(m, P, dev_base, P.dy.empty() ? 0 : P.dy[0].width);
   m.ranks = d + P.o_ranks;
   m.roff = d + P.o_roff;
   m.boff = d + P.o_boff;
@@ -449,6 +522,7 @@ struct Layout {
   size_t meta = 0, bpad = 0, bt = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0,
          gpart = 0, total = 0;
   size_t saved = 0;
+  size_t partB_stride = 0;   // floats between a group's per-projection dB partial regions
   int ld8 = 0;   // row stride (elements) of the B operand the kernels read
 };
 
@@ -476,7 +550,8 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     L.partA = off;
     off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
     L.partB = off;
-    off += align256((size_t)std::max(P.nunits, P.ndyunits) * chB * P.qp * 128 * 4);
+    // unfused: [nunits][chB][qp][128]; fused dY pass: [ndyunits (segments)][4][qp][128]
+    off += align256(std::max((size_t)P.nunits * chB, (size_t)P.ndyunits * 4) * P.qp * 128 * 4);
     L.gpart = off;    // fused dY pass: G partials [nslots][ceil(out/512)][128][qp]
     off += align256((size_t)P.nslots * ((out + 511) / 512) * kTileM * P.qp * 4);
     L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * es;
@@ -783,9 +858,16 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
                 accumulate_dx, meta, ctx->num_sms, st, fused_tp ? &tps : nullptr); }
     if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
-    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(0, partA, in, meta, dA, ldA, accumulate_dadb, st); }
     if (!fused_dy && meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
-    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, meta_b, dB, 0, accumulate_dadb, st); }
+    {
+      // dA and dB in one launch
+      const FinJob jobs[2] = {
+          {partA, dA, ldA, meta.task_unit_off, 0, in, (in + 127) / 128, 0, meta.qp, 0, 1, accumulate_dadb},
+          {partB, dB, 0, fused_dy ? meta_b.dy_task_unit_off : meta.task_unit_off, 1, out, (out + 127) / 128, 0,
+           meta.qp, fused_dy ? 1 : 0, meta_b.dy_nch, accumulate_dadb}};
+      Prof p_(LOBRA_K_FINALIZE, st);
+      launch_finalize_multi(jobs, 2, meta, st);
+    }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
   if (prob->dtype == LOBRA_BF16 && prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() && gemm_uses_pair()) {
@@ -852,6 +934,7 @@ bool group_fused(const lobra_group_problem* g, const lobra_group_adapters* ga) {
 struct GroupLayout {
   size_t meta = 0, bpad = 0, agrp = 0, gslots = 0, rpart = 0, counters = 0, partA = 0, partB = 0,
          gpart = 0, total = 0, saved = 0;
+  size_t partB_stride = 0;   // floats between the per-projection dB partial regions
 };
 
 GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
@@ -874,7 +957,9 @@ GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
   L.partA = off;
   off += align256((size_t)P.nunits * ((in + 127) / 128) * qg * 128 * 4);
   L.partB = off;
-  off += align256((size_t)P.ndyunits * ((omax + 127) / 128) * P.qp * 128 * 4);
+  // per projection [segments][4][qp][128] (the dB finalize of the whole group runs after the loop)
+  L.partB_stride = (size_t)P.ndyunits * 4 * P.qp * 128;
+  off += align256(L.partB_stride * 4 * P.np);
   L.gpart = off;
   off += align256((size_t)P.nslots * ((omax + 511) / 512) * kTileM * P.qp * 4);
   L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * 2;
@@ -885,7 +970,10 @@ GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
 void group_plan(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga,
                 int num_sms, Plan& P) {
   lobra_adapters a0 = single_adapters(ga, 0);
-  build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj);   // units: dA over in
+  std::vector<int> outs;
+  for (int p = 0; p < g->num_proj; ++p) outs.push_back((int)g->out[p]);
+  // units: dA over in; one fused-dY schedule per distinct output width
+  build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj, outs);
 }
 
 // workspace / saved sizes of the fallback (per-projection sequences)
@@ -1091,6 +1179,7 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
       cudaMemcpyAsync(stage, dX, (size_t)P.T * in * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return fail(LOBRA_ERR_CUDA, "TP stage copy failed");
   auto* dXacc = static_cast<__nv_bfloat16*>(stage ? stage : dX);
+  FinJob jobs[kMaxFinJobs];
   for (int p = 0; p < np; ++p) {
     const int out = (int)g->out[p];
     const __nv_bfloat16* Bop = static_cast<const __nv_bfloat16*>(ga->B[p]);
@@ -1106,28 +1195,30 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
     if ((s = make_map(&mAt, ga->A[p], in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
     Meta mp = meta;
     mp.band = p * P.qp;
+    set_dy(mp, P, w + L.meta, out);
     {
       // a3 for projection p: G_s into band p, dB partials against band p of H_s
       Prof p_(LOBRA_K_ROWPROJ, st);
-      launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
-                    ctx->num_sms, st);
+      // dB partials of projection p in their own region (finalized after the loop)
+      launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart),
+                    partB + (size_t)p * L.partB_stride, Gs, ctx->num_sms, st);
     }
     // fused TP: projections 0..np-2 accumulate locally in dX, the last one scatters the rows
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, dXacc,
                                                    p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st,
                                                    fused_tp && p == np - 1 ? &tps : nullptr); }
-    Meta mb = meta;
-    mb.use_dy_units = 1;
-    { Prof p_(LOBRA_K_FINALIZE, st); launch_finalize(1, partB, out, mb, dB[p], 0, accumulate_dadb, st); }
+    jobs[np + p] = {partB + (size_t)p * L.partB_stride, dB[p], 0, mp.dy_task_unit_off, 1, out,
+                    (out + 127) / 128, 0, P.qp, 1, mp.dy_nch, accumulate_dadb};
   }
   // a5 for the whole group: ONE pass over X against all bands of G_s
   if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta_g, partA, ctx->num_sms, st); }
-  for (int p = 0; p < np; ++p) {
-    Meta ma = meta;
-    ma.qp = np * P.qp;
-    ma.band = p * P.qp;
+  for (int p = 0; p < np; ++p)
+    jobs[p] = {partA, dA[p], ldA, meta.task_unit_off, 0, in, (in + 127) / 128, p * P.qp, np * P.qp, 0, 1,
+               accumulate_dadb};
+  {
+    // every projection's dA and dB in one launch
     Prof p_(LOBRA_K_FINALIZE, st);
-    launch_finalize(0, partA, in, ma, dA[p], ldA, accumulate_dadb, st);
+    launch_finalize_multi(jobs, 2 * np, meta, st);
   }
   if ((s = check_launch("lobra_lora_group_bwd")) != LOBRA_OK) return s;
   if (fused_tp) return symm_scatter_finish(comm_symm(g->tp), P.T, in, dX, st);

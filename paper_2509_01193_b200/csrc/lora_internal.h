@@ -37,12 +37,16 @@ struct Meta {
   const int* unit_s0;        // [nunits] range into task_slots
   const int* unit_s1;        // [nunits]
   const int* task_unit_off;  // [ntasks+1]
-  // units of the fused dY pass (512-column items); k_finalize mode 1 uses them when
-  // use_dy_units != 0
-  int ndyunits, use_dy_units;
+  // segments of the fused dY pass (task, 512-column chunk, range [s0, s1) of the task's slot
+  // list); CTA b runs segments [dy_cta_off[b], dy_cta_off[b+1]) (static balanced schedule,
+  // ndycta CTAs); the segments of (task t, chunk c) are [dy_task_unit_off[t*dy_nch + c],
+  // dy_task_unit_off[t*dy_nch + c + 1]).  k_finalize mode 1 uses them when use_dy_units != 0
+  int ndyunits, use_dy_units, ndycta, dy_nch;
   const int* dy_unit_task;
   const int* dy_unit_s0;
   const int* dy_unit_s1;
+  const int* dy_unit_chunk;
+  const int* dy_cta_off;
   const int* dy_task_unit_off;
   const int* ranks;          // [ntasks]
   const int* roff;           // [ntasks+1]
@@ -126,6 +130,22 @@ void launch_finalize(int mode, const float* partial, int width, const Meta& meta
 void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
                    int width, int qp, const Meta& meta, float* gpart, float* bpart,
                    __nv_bfloat16* gslots, int num_sms, cudaStream_t st);
+// One launch for several finalizations (mode 0 dA / mode 1 dB as in launch_finalize).
+// uoff: the task's unit offsets (meta.task_unit_off) or, with dy = 1, the fused dY pass's
+// (task, chunk) segment offsets (meta.dy_task_unit_off, dy_nch chunks per task).
+struct FinJob {
+  const float* partial;
+  float* out;
+  long long ld;
+  const int* uoff;
+  int mode, width, nchunks, band, qp, dy, dy_nch, accumulate;
+};
+constexpr int kMaxFinJobs = 8;
+struct FinJobs {
+  FinJob j[kMaxFinJobs];
+  int n;
+};
+void launch_finalize_multi(const FinJob* jobs, int n, const Meta& meta, cudaStream_t st);
 // Zero (or leave) the dA/dB of every task when the batch has no tokens.
 void launch_zero_f32(float* p, long long n, cudaStream_t st);
 

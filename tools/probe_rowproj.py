@@ -9,7 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(d_in, d_out, reps=30):
+def child(d_in, d_out, reps=30, bwd=False):
     sys.path.insert(0, ROOT)
     import torch
     from paper_2509_01193_b200 import _lib
@@ -28,6 +28,16 @@ def child(d_in, d_out, reps=30):
     ws = torch.empty(_lib.lobra_lora_workspace_bytes(code, d_in, d_out, *args), dtype=torch.uint8, device=dev)
     Hs = torch.empty(_lib.lobra_lora_saved_bytes(code, d_in, d_out, *args), dtype=torch.uint8, device=dev)
     Y = torch.empty(T, d_out, dtype=torch.bfloat16, device=dev)
+    if bwd:
+        dY = torch.randn(T, d_out, generator=g, device=dev).bfloat16()
+        dX = torch.empty(T, d_in, dtype=torch.bfloat16, device=dev)
+        dA = torch.empty(R, d_in, dtype=torch.float32, device=dev)
+        dB = torch.empty(d_out, R, dtype=torch.float32, device=dev)
+        _lib.lobra_lora_fwd(X, W, A, B, wl.ranks, wl.scales, wl.seq_lens, wl.seq_task, Y, Hs, ws)
+        for _ in range(reps):
+            _lib.lobra_lora_bwd(X, W, A, B, wl.ranks, wl.scales, wl.seq_lens, wl.seq_task, Hs, dY, dX, dA, dB, ws)
+        torch.cuda.synchronize()
+        return
     for _ in range(3):
         _lib.lobra_lora_fwd(X, W, A, B, wl.ranks, wl.scales, wl.seq_lens, wl.seq_task, Y, Hs, ws)
     torch.cuda.synchronize()
@@ -42,8 +52,9 @@ def child(d_in, d_out, reps=30):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "child":
-        child(int(sys.argv[2]), int(sys.argv[3]))
+    if len(sys.argv) > 1 and sys.argv[1] in ("child", "childb"):
+        child(int(sys.argv[2]), int(sys.argv[3]), reps=6 if sys.argv[1] == "childb" else 30,
+              bwd=sys.argv[1] == "childb")
         sys.exit(0)
     combos = [{"LOBRA_SHRINK": "0"}, {"LOBRA_SHRINK": "1"}]
     if os.environ.get("PROBE_ALL"):
