@@ -277,6 +277,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no e2e/cpu (for ncu)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3"],
+                    help="c2 (default, BASELINE configs[1]: the metric's workload) or c3 (configs[2]: "
+                         "16 tasks, ranks 8-64, lengths <= 16K, T = 65536; N = 1 only)")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="do not record per-kernel CUDA events inside the timed region")
     args = ap.parse_args()
@@ -308,7 +311,12 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     _lib.load()
 
+    c3 = args.workload == "c3"
+    if c3 and n_gpus > 1:
+        raise SystemExit("--workload c3 is a single-GPU configuration")
     groups = deployment_for(n_gpus) if not gloo_test else [(1, n_gpus, 16384)]
+    if c3:
+        groups = [(1, 1, 65536)]
     reps = replica_ranks(groups)
     my_rep = next(i for i, rr in enumerate(reps) if rank in rr)
     my_group = 0
@@ -358,7 +366,7 @@ def main():
             symm.destroy()
             symm = None
 
-    tasks = synth.c2_tasks()
+    tasks = synth.c3_tasks() if c3 else synth.c2_tasks()
     ranks = [t.rank for t in tasks]
     scales = [t.scale for t in tasks]
     layer = LoraLayer(LLAMA2_7B, ranks, scales, dev, torch.bfloat16, tp_size, tp_rank, comm, seed=1234,
@@ -374,6 +382,8 @@ def main():
 
     def make_batch(step: int):
         """Global batch of the step: N x 16384 tokens of the C2 task mix (seeded)."""
+        if c3:
+            return synth.config_c3(seed=3 + step)
         if n_gpus == 1:
             return synth.config_c2(seed=2 + step)
         return synth.pack_tokens(tasks, T_PER_GPU * n_gpus, 4096, seed=1000 + step, name="C2xN")
@@ -517,7 +527,8 @@ def main():
                 "share_of_step": dom_ms / ms_local if ms_local > 0 else 0.0,
                 "flops_per_launch": dom_fl / max(prof[dom][0], 1),
                 "ms_per_launch": dom_ms / max(prof[dom][0], 1)}
-    flops_step = algorithmic_flops(LLAMA2_7B, int(tokens / args.steps), ranks)["total"]
+    flops_step = algorithmic_flops(LLAMA2_7B, int(tokens / args.steps), ranks,
+                                   tokens_per_task=(nt / args.steps).tolist())["total"]
     step_tflops = flops_step / (ms_step / 1000.0) / 1e12
 
     # ---- end to end through the public API with host buffers (pinned), rank-local
@@ -619,7 +630,8 @@ def main():
     if rank == 0 and n_gpus == 1 and not args.no_cpu and not args.profile_only:
         tps, dt, n, threads = oracle_tokens_per_s(batches[0], LLAMA2_7B, budget_tokens=8192)
         cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-               "sample": f"first {n} tokens of the C2 batch, 7 projections fwd+bwd, fp64 NumPy ({dt:.1f} s)"}
+               "sample": f"first {n} tokens of the {args.workload.upper()} batch, 7 projections fwd+bwd, "
+                         f"fp64 NumPy ({dt:.1f} s)"}
 
     if rank == 0:
         par = "+".join(f"{p}xTP{tp}" for tp, p, _ in groups)
@@ -627,9 +639,11 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded; lengths lognormal-fitted to the paper's dataset table)",
-                "config": {"workload": "C2: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
-                                       "4 tasks r=16 s=2, lengths<=4096 packed",
-                           "global_batch_tokens": int(tokens / args.steps), "seq_len_max": 4096,
+                "config": {"workload": ("C3: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
+                                        "16 tasks ranks 8/16/32/64 s 0.5-4, lengths<=16384 packed") if c3 else
+                                       ("C2: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
+                                        "4 tasks r=16 s=2, lengths<=4096 packed"),
+                           "global_batch_tokens": int(tokens / args.steps), "seq_len_max": 16384 if c3 else 4096,
                            "parallelism": par, "l2": "inputs > L2 (each projection input >= 128 MiB)",
                            "tp_collective": tp_coll},
                 "per_gpu": value / n_gpus,

@@ -1461,18 +1461,29 @@ __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Met
     float sc = 0.0f;
     if (s < meta.nslots) {
       const int t = meta.slot_task[s];
+      // the chunk partials are loaded (4 chunks at a time, independent loads) while the
+      // row's task is looked up; rows of other tasks are masked afterwards
+      const float* src = gpart + ((size_t)s * nchunks * kTileM + lrow) * qp + g * 8;
+      const size_t cstride = (size_t)kTileM * qp;
+      for (int c = 0; c < nchunks; c += 4) {
+        float4 a[4], b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool ok = c + j < nchunks;
+          a[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + (c + j) * cstride)) : make_float4(0, 0, 0, 0);
+          b[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + (c + j) * cstride) + 1) : make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {   // chunk order, as before
+          if (c + j >= nchunks) break;
+          v[0] += a[j].x; v[1] += a[j].y; v[2] += a[j].z; v[3] += a[j].w;
+          v[4] += b[j].x; v[5] += b[j].y; v[6] += b[j].z; v[7] += b[j].w;
+        }
+      }
       const int row = meta.slot_tile[s] * kTileM + lrow;
       if (row < meta.T && row_task(meta, row) == t && g * 8 < meta.ranks[t]) {
         rp = meta.ranks[t] - g * 8;
         sc = meta.scales[t];
-        const float* src = gpart + ((size_t)s * nchunks * kTileM + lrow) * qp + g * 8;
-        const size_t cstride = (size_t)kTileM * qp;
-        for (int c = 0; c < nchunks; ++c) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(src + c * cstride));
-          const float4 b = __ldg(reinterpret_cast<const float4*>(src + c * cstride) + 1);
-          v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
-          v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
-        }
       }
     }
     float w[8];
