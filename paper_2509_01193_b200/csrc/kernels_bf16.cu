@@ -1255,15 +1255,16 @@ __global__ void __launch_bounds__(256, 1)
 // k_gfin then sums the G chunk partials in fixed order, scales by s_t, masks and writes
 // the bf16 G slots; the dB partials go through k_finalize (fixed order) as before.
 // =====================================================================================
-constexpr int Y_STAGES = 3;
+// The H slot and B_t operands are MN-major (q contiguous) boxes only as wide as the rank needs:
+// `hrow` = 32 / 64 / 128 bytes (16 / 32 / 64 q, TMA and UMMA swizzle of that span), MMA N = nq.
+// A stage is [dY 2 x 16 KB][H 128 tokens x hrow][B 2 x 64 o x hrow]: 40 KB for rank 16, so
+// five stages (160 KB of dY) are in flight.
 constexpr int Y_Z_BYTES = 2 * 128 * 64 * 2;   // dY tile: 2 boxes of 64 cols x 128 rows
-constexpr int Y_H_BYTES = 128 * 64 * 2;       // H slot
-constexpr int Y_BT_MAX = 2 * 64 * 128;        // B: 2 MN-major boxes of 64 q x 64 o rows
-constexpr int Y_STAGE_BYTES = Y_Z_BYTES + Y_H_BYTES + Y_BT_MAX;
-constexpr int Y_SMEM = Y_STAGES * Y_STAGE_BYTES + 1024 + 256;
+constexpr int Y_SMEM = 232448;                // stages fill the shared memory (one CTA per SM)
 
 struct DyArgs {
   int width, nchunks, nitems, n128, qp;
+  int hrow, nq, stages, stage_bytes;
   int dbg_dy_only;   // tuning probe (LOBRA_DBG_DY_ONLY=1): stream dY only, skip H / B loads
   float* gpart;    // [nslots][nchunks][128][qp]
   float* bpart;    // [ndyunits][n128][qp][128]   (k_finalize layout)
@@ -1275,20 +1276,22 @@ __global__ void __launch_bounds__(256, 1)
              const __grid_constant__ CUtensorMap mapBt, const DyArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Y_STAGES * Y_STAGE_BYTES);
-  uint64_t* empty = full + Y_STAGES;
-  uint64_t* gfull = empty + Y_STAGES;    // [2]
+  const int NS = args.stages, SB = args.stage_bytes, hrow = args.hrow;
+  const int hbytes = 128 * hrow;          // H region (128 tokens)
+  const int bbox = 64 * hrow;             // one B box (64 o rows)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * SB);
+  uint64_t* empty = full + 8;
+  uint64_t* gfull = empty + 8;           // [2]
   uint64_t* gempty = gfull + 2;          // [2]
   uint64_t* bfull = gempty + 2;          // [1]
   uint64_t* bempty = bfull + 1;          // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
   const uint32_t warp = warp_id(), lane = lane_id();
   const Meta& meta = args.meta;
-  constexpr int bt_box = 64 * 128;       // one MN-major box of B_cat: 64 q x 64 o rows
 
   if (warp == 0 && lane == 0) tma_prefetch(&mapDY), tma_prefetch(&mapH), tma_prefetch(&mapBt);
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < Y_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) mbar_init(&gfull[a], 1), mbar_init(&gempty[a], 128);
     mbar_init(bfull, 1);
     mbar_init(bempty, 128);
@@ -1317,27 +1320,35 @@ __global__ void __launch_bounds__(256, 1)
           for (int b = 0; b < nb; ++b) {
             const int col = c * 512 + b * 128;
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], (args.dbg_dy_only & 1) ? Y_Z_BYTES : Y_Z_BYTES + Y_H_BYTES + 2 * bt_box);
-            uint8_t* st = smem + stage * Y_STAGE_BYTES;
+            mbar_expect_tx(&full[stage], (args.dbg_dy_only & 1) ? Y_Z_BYTES : Y_Z_BYTES + hbytes + 2 * bbox);
+            uint8_t* st = smem + stage * SB;
             tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
             tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
             if (args.dbg_dy_only & 1) {
-              if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+              if (++stage == NS) stage = 0, phase ^= 1;
               continue;
             }
-            tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], 0, sl * kTileM);
+            // H slot columns: this projection's band only (narrow box), or all 64 (hrow 128)
+            tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], hrow == 128 ? 0 : meta.band, sl * kTileM);
             // B_t straight from the caller's B (MN-major: q contiguous, rows = o = K)
-            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES, &mapBt, &full[stage], meta.boff[t], col);
-            tma_load_2d(st + Y_Z_BYTES + Y_H_BYTES + bt_box, &mapBt, &full[stage], meta.boff[t], col + 64);
-            if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+            tma_load_2d(st + Y_Z_BYTES + hbytes, &mapBt, &full[stage], meta.boff[t], col);
+            tma_load_2d(st + Y_Z_BYTES + hbytes + bbox, &mapBt, &full[stage], meta.boff[t], col + 64);
+            if (++stage == NS) stage = 0, phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t id_b = idesc_bf16(128, 64, true, true);          // dB: both MN-major
-      const uint32_t id_g = idesc_bf16(128, 64, false, true);   // G: A K-major, B MN-major
+      const uint32_t id_b = idesc_bf16(128, args.nq, true, true);     // dB: both MN-major
+      const uint32_t id_g = idesc_bf16(128, args.nq, false, true);    // G: A K-major, B MN-major
+      // stage-0 descriptors of the H and B regions; per K step (16 rows) + hstep, per B box
+      // + bstep4 (address field units of 16 bytes)
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t hdesc0 = sdesc_sw(s0 + Y_Z_BYTES, hbytes, 8 * hrow, hrow);
+      const uint64_t tdesc0 = sdesc_sw(s0 + Y_Z_BYTES + hbytes, bbox, 8 * hrow, hrow);
+      const int hstep = hrow;            // 16 rows x hrow bytes >> 4
+      const int bstep4 = bbox >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int gcount = 0, it = 0;
@@ -1356,27 +1367,30 @@ __global__ void __launch_bounds__(256, 1)
           for (int b = 0; b < nb; ++b) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t z0 = smem_u32(smem + stage * Y_STAGE_BYTES);
-            const uint32_t h0 = z0 + Y_Z_BYTES;
-            const uint32_t t0 = h0 + Y_H_BYTES;
+            // descriptors built once per stage; a K step adds its byte offset >> 4 to the
+            // start-address field (the single issuing thread must keep up with the stream)
+            const uint32_t z0 = smem_u32(smem + stage * SB);
+            const uint64_t dz_mn = sdesc_sw128(z0, 16384, 1024);
+            const uint64_t dz_k = sdesc_sw128(z0, 16, 1024);
+            const uint64_t dh = hdesc0 + ((uint64_t)(stage * SB) >> 4);
+            const uint64_t dt = tdesc0 + ((uint64_t)(stage * SB) >> 4);
             if (!(args.dbg_dy_only & 2)) {   // probe bit 1: skip the dB MMAs
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk)   // dB[b] += dY^T H   (K = 128 tokens)
-                mma_bf16(tmem + b * 64, sdesc_sw128(z0 + kk * 2048, 16384, 1024),
-                         sdesc_sw128(h0 + kk * 2048, 8192, 1024), id_b,
-                         (first_slot && kk == 0) ? 0u : 1u);
+                mma_bf16(tmem + b * 64, dz_mn + (uint64_t)(kk * 128), dh + (uint64_t)(kk * hstep),
+                         id_b, (first_slot && kk == 0) ? 0u : 1u);
             }
             if (!(args.dbg_dy_only & 4)) {   // probe bit 2: skip the G MMAs
 #pragma unroll
               for (int j = 0; j < 2; ++j)      // G += dY[:, 64 cols] B^T[qp, 64 cols]^T
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16(dg, sdesc_sw128(z0 + j * 16384 + kk * 32, 16, 1024),
-                           sdesc_sw128(t0 + j * bt_box + kk * 2048, 8192, 1024), id_g,
+                  mma_bf16(dg, dz_k + (uint64_t)(j * 1024 + kk * 2),
+                           dt + (uint64_t)(j * bstep4 + kk * hstep), id_g,
                            (b == 0 && j == 0 && kk == 0) ? 0u : 1u);
             }
             mma_commit(&empty[stage]);
-            if (++stage == Y_STAGES) stage = 0, phase ^= 1;
+            if (++stage == NS) stage = 0, phase ^= 1;
           }
           mma_commit(&gfull[gb]);
           first_slot = false;
@@ -1422,7 +1436,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int h = 0; h < 2; ++h) {
           if (h * 32 >= rp) break;
           float v[32];
-          tmem_ld32(tmem + ((q * 32u) << 16) + b * 64 + meta.band + h * 32, v);   // dB vs H band
+          tmem_ld32(tmem + ((q * 32u) << 16) + b * 64 + (hrow == 128 ? meta.band : 0) + h * 32, v);   // dB vs H band
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (h * 32 + j < rp) dst[(size_t)(h * 32 + j) * 128] = v[j];
@@ -1860,6 +1874,16 @@ void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, 
   }
 }
 
+int dypass_span(int qp) {
+  static int force = -1;   // LOBRA_DY_SPAN=32|64|128 (tuning; never narrower than the rank)
+  if (force < 0) {
+    const char* e = getenv("LOBRA_DY_SPAN");
+    force = e ? atoi(e) : 0;
+  }
+  const int need = qp <= 16 ? 32 : qp <= 32 ? 64 : 128;
+  return force > need ? force : need;
+}
+
 void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
                    int width, int qp, const Meta& meta, float* gpart, float* bpart,
                    __nv_bfloat16* gslots, int num_sms, cudaStream_t st) {
@@ -1869,6 +1893,11 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
     init = true;
   }
   DyArgs a;
+  a.hrow = dypass_span(qp);
+  a.nq = a.hrow / 2;
+  a.stage_bytes = Y_Z_BYTES + 128 * a.hrow + 2 * 64 * a.hrow;
+  a.stages = std::min(8, (Y_SMEM - 1024 - 256) / a.stage_bytes);
+  if (const char* e = getenv("LOBRA_DY_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(e)));
   a.width = width;
   a.n128 = (width + 127) / 128;
   a.nchunks = (width + 511) / 512;

@@ -565,7 +565,7 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
 }
 
 lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-                      uint32_t box_inner, uint32_t box_outer) {
+                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128) {
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
@@ -580,7 +580,9 @@ lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, pr[promo], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                        : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        pr[promo], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(LOBRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=%llu x %llu box=%u x %u",
                 (int)r, (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
@@ -829,8 +831,12 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     if (fused_dy) {
       // G_s and the dB partials in ONE read of dY; B read in place
       // (MN-major operand, box 64 q x 64 o rows: the same map as the two-pass projection)
+      const int sp = dypass_span(P.qp);
+      CUtensorMap mHd, mBd;
+      if ((s = make_map(&mHd, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, sp / 2, 128, sp)) != LOBRA_OK) return s;
+      if ((s = make_map(&mBd, Bop, L.ld8, out, sp / 2, 64, sp)) != LOBRA_OK) return s;
       Prof p_(LOBRA_K_ROWPROJ, st);
-      launch_dypass(mdY, mHs, mBt, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
+      launch_dypass(mdY, mHd, mBd, out, P.qp, meta, reinterpret_cast<float*>(w + L.gpart), partB, Gs,
                     ctx->num_sms, st);
       meta_b.use_dy_units = 1;
     } else if (rowproj_uses_ld()) {   // workspace has L.bt only in this mode
@@ -1196,11 +1202,15 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
     Meta mp = meta;
     mp.band = p * P.qp;
     set_dy(mp, P, w + L.meta, out);
+    const int sp = dypass_span(P.qp);
+    CUtensorMap mHd, mBd;
+    if ((s = make_map(&mHd, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, sp / 2, 128, sp)) != LOBRA_OK) return s;
+    if ((s = make_map(&mBd, Bop, P.ld8, out, sp / 2, 64, sp)) != LOBRA_OK) return s;
     {
       // a3 for projection p: G_s into band p, dB partials against band p of H_s
       Prof p_(LOBRA_K_ROWPROJ, st);
       // dB partials of projection p in their own region (finalized after the loop)
-      launch_dypass(mdY, mHs, mBt, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart),
+      launch_dypass(mdY, mHd, mBd, out, P.qp, mp, reinterpret_cast<float*>(w + L.gpart),
                     partB + (size_t)p * L.partB_stride, Gs, ctx->num_sms, st);
     }
     // fused TP: projections 0..np-2 accumulate locally in dX, the last one scatters the rows

@@ -127,6 +127,9 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
 void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
                      long long ld, int accumulate, cudaStream_t st);
 // Fused dY pass (G slots + dB partials in one dY read) followed by the G finalize.
+// mapH / mapBt: boxes {dypass_span(qp) / 2, 128 tokens} over the H slots and
+// {dypass_span(qp) / 2, 64 o} over B, swizzled with span dypass_span(qp) bytes.
+int dypass_span(int qp);
 void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
                    int width, int qp, const Meta& meta, float* gpart, float* bpart,
                    __nv_bfloat16* gslots, int num_sms, cudaStream_t st);

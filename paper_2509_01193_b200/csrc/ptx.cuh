@@ -260,6 +260,18 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr, uint32_t lbo
   return d;
 }
 
+// Same, for a swizzle span of 32, 64 or 128 bytes (layout type 6, 4, 2): an MN-major operand
+// whose K rows are `span` bytes (16 / 32 / 64 bf16 along MN), 8-row K groups `sbo` bytes apart.
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t smem_addr, uint32_t lbo, uint32_t sbo, int span) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(span == 32 ? 6 : span == 64 ? 4 : 2) << 61;
+  return d;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
