@@ -243,3 +243,20 @@ def test_group_c2_qkv_full_size_equals_single_sequence():
     _same(g, s)
     for y in g["Y"]:
         assert np.isfinite(y).all()
+
+
+def test_group_many_tasks_full_batch():
+    """128 tiles holding 24 interleaved tasks (k_shrink per tile with several passes, many dY
+    segments), unequal widths (q 192 / k,v 64): group == single-projection calls bitwise."""
+    rng = np.random.default_rng(9)
+    lens = []
+    while sum(lens) < 16384:
+        lens.append(int(rng.integers(5, 90)))
+    lens[-1] -= sum(lens) - 16384
+    G = 24
+    ts = [synth.TaskSpec(f"t{i}", 0, 0, 1, 16, 0.5 + 0.5 * (i % 4)) for i in range(G)]
+    wl = synth.Workload("mix24", ts, np.array(lens, np.int32),
+                        np.array([(i * 7) % G for i in range(len(lens))], np.int32), 0)
+    g, X, ts_, _ = _run(wl, 256, [192, 64, 64], seed=3)
+    s, _, _, _ = _run(wl, 256, [192, 64, 64], seed=3, group=False)
+    _same(g, s)

@@ -357,3 +357,33 @@ def test_workspace_too_small_is_rejected():
     with pytest.raises(_lib.LobraError) as e:
         _lib.lobra_lora_fwd(X, W, A, B, [16], [1.0], [300], [0], X, X, ws)
     assert e.value.status == _lib.LOBRA_ERR_INPUT and "workspace" in str(e.value)
+
+
+@pytest.mark.parametrize("T,mixed", [
+    (14080, False),   # 110 tiles: below 3/4 of the SMs -> split-K k_rowproj
+    (14208, False),   # 111 tiles: k_shrink, one CTA per slot (slots fit one wave)
+    (16384, True),    # 128 tiles, 24 interleaved tasks: slots >> SMs -> k_shrink per tile,
+                      # several passes of <= 4 slots per tile, many dY-pass segments
+])
+def test_bf16_shrink_paths_full_batch(T, mixed):
+    """The forward-shrink variants and the balanced dY-pass schedule at bench-sized batches
+    (every row, every task checked against the oracle; narrow widths keep it fast)."""
+    rng = np.random.default_rng(T)
+    if mixed:
+        G = 24
+        ranks = [8, 16, 32, 64] * 6
+        lens = []
+        while sum(lens) < T:
+            lens.append(int(rng.integers(5, 90)))
+        lens[-1] -= sum(lens) - T
+        tasks = [(i * 7) % G for i in range(len(lens))]   # interleaved: many tasks per tile
+    else:
+        G = 4
+        ranks = [16] * 4
+        lens = [T // 8] * 8
+        tasks = [0, 0, 1, 1, 2, 2, 3, 3]
+    scales = [0.5 + 0.5 * (i % 4) for i in range(G)]
+    wl = _wl(lens, tasks, ranks, scales)
+    assert wl.T == T
+    t = synth.layer_tensors(wl, 256, 192, seed=41)
+    check_all(wl, oracle_inputs("bf16", t), run_lib("bf16", wl, t, 256, 192), BF16_TOL, 256, 192)
