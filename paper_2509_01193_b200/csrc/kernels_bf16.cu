@@ -1583,39 +1583,81 @@ __global__ void k_finalize(int mode, const float* __restrict__ partial, int widt
 // Several finalizations in ONE launch (blockIdx.z = job): the dA and dB of a projection, or
 // of every projection of a group.  Same fixed summation order as k_finalize; the unit loads
 // are issued 8 at a time (independent) before the in-order sum.
-__global__ void k_finalize_multi(const FinJobs jobs, const Meta meta) {
+__global__ void __launch_bounds__(256) k_finalize_multi(const FinJobs jobs, const Meta meta) {
+  // block = 8 adapter rows (rq, one per warp) x one 128-column chunk of one job; a lane sums
+  // 4 columns (lane + 32 k: 128-byte coalesced partial loads, 4 independent chains).  dA
+  // (mode 0, row-major [r, width]) is stored directly; dB (mode 1, PEFT [width, rsum]) goes
+  // through a shared-memory transpose so that 8 threads store 8 consecutive rq of one column
+  // (32 B) instead of 8 scattered words.
+  __shared__ float tile[8][129];
   pdl_wait();
   pdl_launch_dependents();
   const FinJob& J = jobs.j[blockIdx.z];
-  const int rq = blockIdx.y;
-  int t = 0;
-  while (meta.roff[t + 1] <= rq) ++t;
-  const int q = rq - meta.roff[t];
-  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < J.width; col += gridDim.x * blockDim.x) {
-    const int c = col >> 7, ci = col & 127;
+  const int col0 = blockIdx.x * 128;
+  if (col0 >= J.width) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rq = blockIdx.y * 8 + w;
+  const int c = blockIdx.x;                       // 128-column chunk
+  float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (rq < meta.rsum) {
+    int lo = 0, hi = meta.ntasks - 1;             // task of row rq: last t with roff[t] <= rq
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (meta.roff[mid] <= rq) lo = mid; else hi = mid - 1;
+    }
+    const int t = lo, q = rq - meta.roff[t];
     int u0, u1;
     size_t base, ustride;
     if (J.dy) {   // fused dY pass: segments of (t, 512-column chunk), [seg][4][qp][128]
-      const int tc = t * J.dy_nch + (col >> 9);
+      const int tc = t * J.dy_nch + (c >> 2);
       u0 = J.uoff[tc], u1 = J.uoff[tc + 1];
-      base = ((size_t)(c & 3) * J.qp + J.band + q) * 128 + ci;
+      base = ((size_t)(c & 3) * J.qp + J.band + q) * 128 + lane;
       ustride = (size_t)4 * J.qp * 128;
     } else {
       u0 = J.uoff[t], u1 = J.uoff[t + 1];
-      base = ((size_t)c * J.qp + J.band + q) * 128 + ci;
+      base = ((size_t)c * J.qp + J.band + q) * 128 + lane;
       ustride = (size_t)J.nchunks * J.qp * 128;
     }
-    float s = 0.0f;
-    for (int u = u0; u < u1; u += 8) {
-      float v[8];
+    for (int u = u0; u < u1; u += 2) {
+      float v[2][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = (u + i < u1) ? __ldg(J.partial + base + (size_t)(u + i) * ustride) : 0.0f;
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (u + i < u1) s += v[i];
+        for (int k = 0; k < 4; ++k)
+          v[a][k] = (u + a < u1 && col0 + lane + 32 * k < J.width)
+                        ? __ldg(J.partial + base + (size_t)(u + a) * ustride + 32 * k) : 0.0f;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+        if (u + a < u1)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) s[k] += v[a][k];
     }
-    float* dst = (J.mode == 0) ? J.out + (long long)rq * J.ld + col : J.out + (long long)col * meta.rsum + rq;
-    *dst = J.accumulate ? *dst + s : s;
+    if (J.mode == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int col = col0 + lane + 32 * k;
+        if (col < J.width) {
+          float* dst = J.out + (long long)rq * J.ld + col;
+          *dst = J.accumulate ? *dst + s[k] : s[k];
+        }
+      }
+    }
+  }
+  if (J.mode == 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tile[w][lane + 32 * k] = s[k];
+    __syncthreads();
+    const int r = threadIdx.x & 7;
+    const int rq2 = blockIdx.y * 8 + r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cc = (threadIdx.x >> 3) + 32 * k, cl = col0 + cc;
+      if (rq2 < meta.rsum && cl < J.width) {
+        float* dst = J.out + (long long)cl * meta.rsum + rq2;
+        const float v = tile[r][cc];
+        *dst = J.accumulate ? *dst + v : v;
+      }
+    }
   }
 }
 
@@ -2016,7 +2058,7 @@ void launch_finalize_multi(const FinJob* jobs, int n, const Meta& meta, cudaStre
   int wmax = 1;
   for (int i = 0; i < n && i < kMaxFinJobs; ++i) J.j[i] = jobs[i], wmax = std::max(wmax, jobs[i].width);
   J.n = std::min(n, kMaxFinJobs);
-  launch_k(k_finalize_multi, dim3((wmax + 255) / 256, meta.rsum, J.n), dim3(256), 0, st, J, meta);
+  launch_k(k_finalize_multi, dim3((wmax + 127) / 128, (meta.rsum + 7) / 8, J.n), dim3(256), 0, st, J, meta);
 }
 
 void launch_zero_f32(float* p, long long n, cudaStream_t st) {
