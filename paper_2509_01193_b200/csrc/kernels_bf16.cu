@@ -1473,7 +1473,7 @@ __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Met
     for (int e = 0; e < 8; ++e) v[e] = 0.0f;
     int rp = 0;
     float sc = 0.0f;
-    if (s < meta.nslots) {
+    if (s < meta.nslots && g * 8 < meta.ranks[meta.slot_task[s]]) {   // columns < r_t only
       const int t = meta.slot_task[s];
       // the chunk partials are loaded (4 chunks at a time, independent loads) while the
       // row's task is looked up; rows of other tasks are masked afterwards
@@ -1495,7 +1495,7 @@ __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Met
         }
       }
       const int row = meta.slot_tile[s] * kTileM + lrow;
-      if (row < meta.T && row_task(meta, row) == t && g * 8 < meta.ranks[t]) {
+      if (row < meta.T && row_task(meta, row) == t) {
         rp = meta.ranks[t] - g * 8;
         sc = meta.scales[t];
       }
