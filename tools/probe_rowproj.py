@@ -9,13 +9,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(d_in, d_out, reps=30, bwd=False):
+def child(d_in, d_out, reps=30, bwd=False, c3=False):
     sys.path.insert(0, ROOT)
     import torch
     from paper_2509_01193_b200 import _lib
     from workloads import synth
     dev = torch.device("cuda:0")
-    wl = synth.config_c2()
+    wl = synth.config_c3() if c3 else synth.config_c2()
     T = wl.T
     g = torch.Generator(device=dev).manual_seed(0)
     X = torch.randn(T, d_in, generator=g, device=dev).bfloat16()
@@ -52,9 +52,9 @@ def child(d_in, d_out, reps=30, bwd=False):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] in ("child", "childb"):
-        child(int(sys.argv[2]), int(sys.argv[3]), reps=6 if sys.argv[1] == "childb" else 30,
-              bwd=sys.argv[1] == "childb")
+    if len(sys.argv) > 1 and sys.argv[1] in ("child", "childb", "childb3"):
+        child(int(sys.argv[2]), int(sys.argv[3]), reps=6 if sys.argv[1] != "child" else 30,
+              bwd=sys.argv[1] != "child", c3=sys.argv[1] == "childb3")
         sys.exit(0)
     combos = [{"LOBRA_SHRINK": "0"}, {"LOBRA_SHRINK": "1"}]
     if os.environ.get("PROBE_ALL"):
