@@ -494,7 +494,7 @@ def main():
     ms_step = ms_total / args.steps
     value = tokens / (ms_total / 1000.0)
     rf = {"pass": "none (--no-kernel-events)"}
-    if not args.no_kernel_events:
+    if not args.no_kernel_events and not args.profile_only:
         barrier()
         _, ms_local_ev, _, _, _, _, prof, clocks_ev = timed(kernel_events=True)
         rf = {"pass": "second pass over the same K steps with per-launch CUDA events on the launching "
