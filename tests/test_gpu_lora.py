@@ -362,6 +362,7 @@ def test_workspace_too_small_is_rejected():
 @pytest.mark.parametrize("T,mixed", [
     (14080, False),   # 110 tiles: below 3/4 of the SMs -> split-K k_rowproj
     (14208, False),   # 111 tiles: k_shrink, one CTA per slot (slots fit one wave)
+    (14300, False),   # 112 tiles, ragged last tile (92 rows)
     (16384, True),    # 128 tiles, 24 interleaved tasks: slots >> SMs -> k_shrink per tile,
                       # several passes of <= 4 slots per tile, many dY-pass segments
 ])
@@ -381,6 +382,7 @@ def test_bf16_shrink_paths_full_batch(T, mixed):
         G = 4
         ranks = [16] * 4
         lens = [T // 8] * 8
+        lens[-1] += T - sum(lens)
         tasks = [0, 0, 1, 1, 2, 2, 3, 3]
     scales = [0.5 + 0.5 * (i % 4) for i in range(G)]
     wl = _wl(lens, tasks, ranks, scales)
