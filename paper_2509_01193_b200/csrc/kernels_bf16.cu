@@ -1166,9 +1166,9 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-        const int u = item / args.nchunks, c = item % args.nchunks;
-        for (int k = meta.unit_s0[u]; k < meta.unit_s1[u]; ++k) {
+      for (int u = meta.sr_cta_off[blockIdx.x]; u < meta.sr_cta_off[blockIdx.x + 1]; ++u) {
+        const int c = meta.sr_chunk[u];
+        for (int k = meta.sr_s0[u]; k < meta.sr_s1[u]; ++k) {
           const int sl = meta.task_slots[k];
           const int tile = meta.slot_tile[sl];
           mbar_wait(&empty[stage], phase ^ 1);
@@ -1187,14 +1187,13 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
-        const int u = item / args.nchunks;
+      for (int u = meta.sr_cta_off[blockIdx.x]; u < meta.sr_cta_off[blockIdx.x + 1]; ++u, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 64;
         bool first = true;
-        for (int k = meta.unit_s0[u]; k < meta.unit_s1[u]; ++k) {
+        for (int k = meta.sr_s0[u]; k < meta.sr_s1[u]; ++k) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * S_STAGE_BYTES);
@@ -1214,13 +1213,12 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
     int it = 0;
-    for (int item = blockIdx.x; item < args.nitems; item += gridDim.x, ++it) {
-      const int u = item / args.nchunks, c = item % args.nchunks;
+    for (int u = meta.sr_cta_off[blockIdx.x]; u < meta.sr_cta_off[blockIdx.x + 1]; ++u, ++it) {
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int rp = rpad16(meta.ranks[meta.unit_task[u]]);
-      float* dst = args.partial + ((size_t)(u * args.nchunks + c) * meta.qp) * 128 + q * 32 + lane;
+      const int rp = rpad16(meta.ranks[meta.sr_task[u]]);
+      float* dst = args.partial + ((size_t)u * meta.qp) * 128 + q * 32 + lane;   // [seg][qp][128]
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         if (h * 32 >= rp) break;
@@ -1608,11 +1606,11 @@ __global__ void __launch_bounds__(256) k_finalize_multi(const FinJobs jobs, cons
     const int t = lo, q = rq - meta.roff[t];
     int u0, u1;
     size_t base, ustride;
-    if (J.dy) {   // fused dY pass: segments of (t, 512-column chunk), [seg][4][qp][128]
-      const int tc = t * J.dy_nch + (c >> 2);
+    if (J.dy) {   // segments of (t, J.sub 128-column blocks): [seg][sub][qp][128]
+      const int tc = t * J.dy_nch + c / J.sub;
       u0 = J.uoff[tc], u1 = J.uoff[tc + 1];
-      base = ((size_t)(c & 3) * J.qp + J.band + q) * 128 + lane;
-      ustride = (size_t)4 * J.qp * 128;
+      base = ((size_t)(c % J.sub) * J.qp + J.band + q) * 128 + lane;
+      ustride = (size_t)J.sub * J.qp * 128;
     } else {
       u0 = J.uoff[t], u1 = J.uoff[t + 1];
       base = ((size_t)c * J.qp + J.band + q) * 128 + lane;
@@ -2036,12 +2034,11 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
   SegArgs a;
   a.width = width;
   a.nchunks = (width + 127) / 128;
-  a.nitems = meta.nunits * a.nchunks;
+  a.nitems = meta.nsrseg;
   a.partial = partial;
   a.meta = meta;
-  if (a.nitems == 0) return;
-  const int grid = a.nitems < num_sms ? a.nitems : num_sms;
-  launch_k(k_segred, dim3(grid), dim3(256), S_SMEM, st, mapZ, mapSlot, a);
+  if (a.nitems == 0 || meta.nsrcta == 0) return;
+  launch_k(k_segred, dim3(meta.nsrcta), dim3(256), S_SMEM, st, mapZ, mapSlot, a);
 }
 
 void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,

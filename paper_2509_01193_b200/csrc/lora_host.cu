@@ -244,6 +244,8 @@ struct Plan {
     int o_task = 0, o_s0 = 0, o_s1 = 0, o_off = 0, o_chunk = 0, o_cta = 0;
   };
   std::vector<DySet> dy;
+  std::vector<DySet> sr;   // k_segred schedules (128-column chunks), per reduction width
+  int nsrseg = 0;          // max segments over sr
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -282,7 +284,8 @@ lobra_status validate(const lobra_problem* prob, const lobra_batch* b, const lob
 }
 
 void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, int dy_width,
-                int num_sms, Plan& P, int np = 1, const std::vector<int>& dy_widths = {}) {
+                int num_sms, Plan& P, int np = 1, const std::vector<int>& dy_widths = {},
+                const std::vector<int>& sr_widths = {}) {
   const int n = b->num_seqs, G = ad->num_tasks;
   P.ntasks = G;
   P.np = np;
@@ -350,9 +353,9 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     std::vector<int> task, s0, s1, chunk, off, cta_off{0};
     int ncta = 1, nch = 1;
   };
-  auto build_dy = [&](int width) {
+  auto build_dy = [&](int width, int chunk_cols) {
     DyVecs v;
-    const int nch = std::max(1, (width + 511) / 512);
+    const int nch = std::max(1, (width + chunk_cols - 1) / chunk_cols);
     long long W = 0;
     for (int t = 0; t < G; ++t) W += (long long)(task_slot_off[t + 1] - task_slot_off[t]) * nch;
     const int ncta = (int)std::max<long long>(1, std::min<long long>(std::max(num_sms, 1), W));
@@ -382,6 +385,24 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     v.nch = nch;
     return v;
   };
+  // the same static balanced schedule for the token reduction k_segred (128-column chunks),
+  // for the dA width and (unfused dY pass) the dB width
+  std::vector<DyVecs> srv;
+  P.sr.clear();
+  P.nsrseg = 0;
+  for (int wdt : sr_widths.empty() ? std::vector<int>{width_hint, dy_width} : sr_widths) {
+    bool seen = false;
+    for (const auto& d : P.sr) seen = seen || d.width == wdt;
+    if (seen || wdt <= 0) continue;
+    srv.push_back(build_dy(wdt, 128));
+    Plan::DySet ds;
+    ds.width = wdt;
+    ds.ncta = srv.back().ncta;
+    ds.nch = srv.back().nch;
+    ds.nseg = (int)srv.back().task.size();
+    P.nsrseg = std::max(P.nsrseg, ds.nseg);
+    P.sr.push_back(ds);
+  }
   std::vector<int> widths = dy_widths;
   if (widths.empty()) widths.push_back(dy_width);
   std::vector<DyVecs> dyv;
@@ -391,7 +412,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     bool seen = false;
     for (const auto& d : P.dy) seen = seen || d.width == wdt;
     if (seen) continue;
-    dyv.push_back(build_dy(wdt));
+    dyv.push_back(build_dy(wdt, 512));
     Plan::DySet ds;
     ds.width = wdt;
     ds.ncta = dyv.back().ncta;
@@ -424,6 +445,14 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   P.o_unit_s0 = put(unit_s0);
   P.o_unit_s1 = put(unit_s1);
   P.o_task_unit_off = put(task_unit_off);
+  for (size_t i = 0; i < P.sr.size(); ++i) {
+    P.sr[i].o_task = put(srv[i].task);
+    P.sr[i].o_s0 = put(srv[i].s0);
+    P.sr[i].o_s1 = put(srv[i].s1);
+    P.sr[i].o_off = put(srv[i].off);
+    P.sr[i].o_chunk = put(srv[i].chunk);
+    P.sr[i].o_cta = put(srv[i].cta_off);
+  }
   for (size_t i = 0; i < P.dy.size(); ++i) {
     P.dy[i].o_task = put(dyv[i].task);
     P.dy[i].o_s0 = put(dyv[i].s0);
@@ -471,6 +500,27 @@ void set_dy(Meta& m, const Plan& P, const void* dev_base, int width) {
   m.dy_cta_off = d + ds->o_cta;
 }
 
+// point the token-reduction (k_segred) schedule fields of `m` at the one built for `width`
+void set_sr(Meta& m, const Plan& P, const void* dev_base, int width) {
+  const int32_t* d = reinterpret_cast<const int32_t*>(dev_base);
+  const Plan::DySet* ds = nullptr;
+  for (const auto& x : P.sr)
+    if (x.width == width) ds = &x;
+  if (!ds) {
+    m.nsrcta = 0, m.sr_nch = 1, m.nsrseg = 0;
+    return;
+  }
+  m.nsrseg = ds->nseg;
+  m.nsrcta = ds->ncta;
+  m.sr_nch = ds->nch;
+  m.sr_task = d + ds->o_task;
+  m.sr_s0 = d + ds->o_s0;
+  m.sr_s1 = d + ds->o_s1;
+  m.sr_tc_off = d + ds->o_off;
+  m.sr_chunk = d + ds->o_chunk;
+  m.sr_cta_off = d + ds->o_cta;
+}
+
 Meta device_meta(const Plan& P, const void* dev_base) {
   const int32_t* d = reinterpret_cast<const int32_t*>(dev_base);
   Meta m;
@@ -497,6 +547,7 @@ Meta device_meta(const Plan& P, const void* dev_base) {
   m.ndyunits = P.ndyunits;
   m.use_dy_units = 0;
   set_dy(m, P, dev_base, P.dy.empty() ? 0 : P.dy[0].width);
+  set_sr(m, P, dev_base, P.sr.empty() ? 0 : P.sr[0].width);
   m.ranks = d + P.o_ranks;
   m.roff = d + P.o_roff;
   m.boff = d + P.o_boff;
@@ -548,10 +599,10 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
     off += align256((size_t)P.ntiles * 4);
     const size_t chA = (in + 127) / 128, chB = (out + 127) / 128;
     L.partA = off;
-    off += align256((size_t)P.nunits * chA * P.qp * 128 * 4);
+    off += align256(std::max((size_t)P.nunits * chA, (size_t)P.nsrseg) * P.qp * 128 * 4);
     L.partB = off;
     // unfused: [nunits][chB][qp][128]; fused dY pass: [ndyunits (segments)][4][qp][128]
-    off += align256(std::max((size_t)P.nunits * chB, (size_t)P.ndyunits * 4) * P.qp * 128 * 4);
+    off += align256(std::max({(size_t)P.nunits * chB, (size_t)P.ndyunits * 4, (size_t)P.nsrseg}) * P.qp * 128 * 4);
     L.gpart = off;    // fused dY pass: G partials [nslots][ceil(out/512)][128][qp]
     off += align256((size_t)P.nslots * ((out + 511) / 512) * kTileM * P.qp * 4);
     L.saved = (size_t)(P.nslots + 1) * kTileM * kSlotW * es;
@@ -622,7 +673,7 @@ lobra_status prepare(const lobra_problem* prob, const lobra_batch* b, const lobr
                      int width_hint, int num_sms, Plan& P, Layout& L) {
   lobra_status st = validate(prob, b, ad);
   if (st != LOBRA_OK) return st;
-  build_plan(b, ad, width_hint, (int)prob->out, num_sms, P);
+  build_plan(b, ad, width_hint, (int)prob->out, num_sms, P, 1, {}, {(int)prob->in, (int)prob->out});
   L = layout(prob, P);
   return LOBRA_OK;
 }
@@ -863,14 +914,18 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
                           symm_scatter_target(comm_symm(prob->tp), P.T, in, &tps);
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
                 accumulate_dx, meta, ctx->num_sms, st, fused_tp ? &tps : nullptr); }
-    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta, partA, ctx->num_sms, st); }
-    if (!fused_dy && meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta, partB, ctx->num_sms, st); }
+    Meta meta_a = meta;
+    set_sr(meta_a, P, w + L.meta, in);
+    if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta_a, partA, ctx->num_sms, st); }
+    Meta meta_s = meta;
+    set_sr(meta_s, P, w + L.meta, out);
+    if (!fused_dy && meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mdY, mHs, out, meta_s, partB, ctx->num_sms, st); }
     {
-      // dA and dB in one launch
+      // dA and dB in one launch (segment partials: k_segred [seg][qp][128], dY pass [seg][4][qp][128])
       const FinJob jobs[2] = {
-          {partA, dA, ldA, meta.task_unit_off, 0, in, (in + 127) / 128, 0, meta.qp, 0, 1, accumulate_dadb},
-          {partB, dB, 0, fused_dy ? meta_b.dy_task_unit_off : meta.task_unit_off, 1, out, (out + 127) / 128, 0,
-           meta.qp, fused_dy ? 1 : 0, meta_b.dy_nch, accumulate_dadb}};
+          {partA, dA, ldA, meta_a.sr_tc_off, 0, in, (in + 127) / 128, 0, meta.qp, 1, meta_a.sr_nch, accumulate_dadb, 1},
+          {partB, dB, 0, fused_dy ? meta_b.dy_task_unit_off : meta_s.sr_tc_off, 1, out, (out + 127) / 128, 0,
+           meta.qp, 1, fused_dy ? meta_b.dy_nch : meta_s.sr_nch, accumulate_dadb, fused_dy ? 4 : 1}};
       Prof p_(LOBRA_K_FINALIZE, st);
       launch_finalize_multi(jobs, 2, meta, st);
     }
@@ -961,7 +1016,7 @@ GroupLayout group_layout(const lobra_group_problem* g, const Plan& P) {
   L.counters = off;
   off += align256((size_t)P.ntiles * 4);
   L.partA = off;
-  off += align256((size_t)P.nunits * ((in + 127) / 128) * qg * 128 * 4);
+  off += align256(std::max((size_t)P.nunits * ((in + 127) / 128), (size_t)P.nsrseg) * qg * 128 * 4);
   L.partB = off;
   // per projection [segments][4][qp][128] (the dB finalize of the whole group runs after the loop)
   L.partB_stride = (size_t)P.ndyunits * 4 * P.qp * 128;
@@ -979,7 +1034,7 @@ void group_plan(const lobra_group_problem* g, const lobra_batch* b, const lobra_
   std::vector<int> outs;
   for (int p = 0; p < g->num_proj; ++p) outs.push_back((int)g->out[p]);
   // units: dA over in; one fused-dY schedule per distinct output width
-  build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj, outs);
+  build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj, outs, {(int)g->in});
 }
 
 // workspace / saved sizes of the fallback (per-projection sequences)
@@ -1218,13 +1273,13 @@ extern "C" lobra_status lobra_lora_group_bwd(const lobra_group_problem* g, const
                                                    p > 0 ? 1 : accumulate_dx, mp, ctx->num_sms, st,
                                                    fused_tp && p == np - 1 ? &tps : nullptr); }
     jobs[np + p] = {partB + (size_t)p * L.partB_stride, dB[p], 0, mp.dy_task_unit_off, 1, out,
-                    (out + 127) / 128, 0, P.qp, 1, mp.dy_nch, accumulate_dadb};
+                    (out + 127) / 128, 0, P.qp, 1, mp.dy_nch, accumulate_dadb, 4};
   }
   // a5 for the whole group: ONE pass over X against all bands of G_s
   if (meta.nunits) { Prof p_(LOBRA_K_SEGRED, st); launch_segred(mX, mG, in, meta_g, partA, ctx->num_sms, st); }
   for (int p = 0; p < np; ++p)
-    jobs[p] = {partA, dA[p], ldA, meta.task_unit_off, 0, in, (in + 127) / 128, p * P.qp, np * P.qp, 0, 1,
-               accumulate_dadb};
+    jobs[p] = {partA, dA[p], ldA, meta_g.sr_tc_off, 0, in, (in + 127) / 128, p * P.qp, np * P.qp, 1,
+               meta_g.sr_nch, accumulate_dadb, 1};
   {
     // every projection's dA and dB in one launch
     Prof p_(LOBRA_K_FINALIZE, st);

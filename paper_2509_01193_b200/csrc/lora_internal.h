@@ -48,6 +48,17 @@ struct Meta {
   const int* dy_unit_chunk;
   const int* dy_cta_off;
   const int* dy_task_unit_off;
+  // token-reduction (k_segred) schedule: the same static balanced cut as the dY pass over
+  // (task, 128-column chunk, slot) entries; CTA b runs segments [sr_cta_off[b], sr_cta_off[b+1])
+  // (nsrcta CTAs), segment partials [seg][qp][128]; the segments of (t, c) are
+  // [sr_tc_off[t*sr_nch + c], sr_tc_off[t*sr_nch + c + 1])
+  int nsrseg, nsrcta, sr_nch;
+  const int* sr_task;
+  const int* sr_s0;
+  const int* sr_s1;
+  const int* sr_chunk;
+  const int* sr_cta_off;
+  const int* sr_tc_off;
   const int* ranks;          // [ntasks]
   const int* roff;           // [ntasks+1]
   const int* boff;           // [ntasks+1] task column offset in the B operand the kernels read
@@ -142,6 +153,7 @@ struct FinJob {
   long long ld;
   const int* uoff;
   int mode, width, nchunks, band, qp, dy, dy_nch, accumulate;
+  int sub = 4;   // with dy = 1: 128-column blocks per segment (4: fused dY pass, 1: k_segred)
 };
 constexpr int kMaxFinJobs = 8;
 struct FinJobs {
