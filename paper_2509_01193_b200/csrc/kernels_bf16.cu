@@ -9,7 +9,7 @@
 //              HBM-bound; CTAs per 128-row tile (split-K when tiles are few) stream Z once.
 // k_segred   : the token reductions dA_t = X^T G_s and dB_t = dY^T H_s on tensor cores,
 //              Z tiles used as MN-major A operands (one HBM read of Z), deterministic
-//              two-pass (partials + k_finalize in fixed order).
+//              two-pass (partials + k_finalize_multi in fixed order).
 // See DESIGN.md "Kernels" for layouts and the roofline of each.
 #include <cuda_bf16.h>
 
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(256, 1)
 // MN-major B for G: no transpose copy).  TMEM: four dB
 // accumulators (4 x 64 cols) kept across the unit's slots + two G accumulators (2 x 64).
 // k_gfin then sums the G chunk partials in fixed order, scales by s_t, masks and writes
-// the bf16 G slots; the dB partials go through k_finalize (fixed order) as before.
+// the bf16 G slots; the dB partials go through k_finalize_multi (fixed order).
 // =====================================================================================
 // The H slot and B_t operands are MN-major (q contiguous) boxes only as wide as the rank needs:
 // `hrow` = 32 / 64 / 128 bytes (16 / 32 / 64 q, TMA and UMMA swizzle of that span), MMA N = nq.
@@ -1265,7 +1265,7 @@ struct DyArgs {
   int hrow, nq, stages, stage_bytes;
   int dbg_dy_only;   // tuning probe (LOBRA_DBG_DY_ONLY=1): stream dY only, skip H / B loads
   float* gpart;    // [nslots][nchunks][128][qp]
-  float* bpart;    // [ndyunits][n128][qp][128]   (k_finalize layout)
+  float* bpart;    // [segments][4][qp][128]
   Meta meta;
 };
 
@@ -1551,33 +1551,7 @@ __global__ void k_pad_cols(const __nv_bfloat16* __restrict__ src, __nv_bfloat16*
   }
 }
 
-// out[(t,q), col] (+)= sum over the task's units (fixed order) of the partials.
-// grid (ceil(width / 256), rsum): one adapter row per blockIdx.y, coalesced over cols.
-__global__ void k_finalize(int mode, const float* __restrict__ partial, int width, int nchunks,
-                           Meta meta, float* __restrict__ out, long long ld, int accumulate) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int rq = blockIdx.y;
-  int t = 0;
-  while (meta.roff[t + 1] <= rq) ++t;
-  const int q = rq - meta.roff[t];
-  const bool dyseg = mode == 1 && meta.use_dy_units;
-  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < width; col += gridDim.x * blockDim.x) {
-    const int c = col >> 7, ci = col & 127;
-    float s = 0.0f;
-    if (dyseg) {   // fused dY pass: segments of (t, 512-column chunk), [seg][4][qp][128]
-      const int tc = t * meta.dy_nch + (col >> 9);
-      for (int u = meta.dy_task_unit_off[tc]; u < meta.dy_task_unit_off[tc + 1]; ++u)
-        s += __ldg(partial + ((size_t)(u * 4 + (c & 3)) * meta.qp + meta.band + q) * 128 + ci);
-    } else {
-      for (int u = meta.task_unit_off[t]; u < meta.task_unit_off[t + 1]; ++u)
-        s += __ldg(partial + ((size_t)(u * nchunks + c) * meta.qp + meta.band + q) * 128 + ci);
-    }
-    float* dst = (mode == 0) ? out + (long long)rq * ld + col : out + (long long)col * meta.rsum + rq;
-    *dst = accumulate ? *dst + s : s;
-  }
-}
-
+// out[(t,q), col] (+)= sum over the task's units / segments (fixed order) of the partials.
 // Several finalizations in ONE launch (blockIdx.z = job): the dA and dB of a projection, or
 // of every projection of a group.  Same fixed summation order as k_finalize; the unit loads
 // are issued 8 at a time (independent) before the in-order sum.
@@ -2039,14 +2013,6 @@ void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int widt
   a.meta = meta;
   if (a.nitems == 0 || meta.nsrcta == 0) return;
   launch_k(k_segred, dim3(meta.nsrcta), dim3(256), S_SMEM, st, mapZ, mapSlot, a);
-}
-
-void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
-                     long long ld, int accumulate, cudaStream_t st) {
-  if (meta.rsum == 0) return;
-  dim3 grid((width + 255) / 256, meta.rsum);
-  launch_k(k_finalize, grid, dim3(256), 0, st, mode, partial, width, (width + 127) / 128, meta, out,
-           ld, accumulate);
 }
 
 void launch_finalize_multi(const FinJob* jobs, int n, const Meta& meta, cudaStream_t st) {

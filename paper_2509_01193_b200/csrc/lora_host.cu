@@ -346,7 +346,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   // are cut into one contiguous range of equal length per CTA (a static balanced schedule:
   // every entry streams one 128 x 512 dY block), and each range into segments of equal
   // (task, chunk) -- a segment accumulates its dB chunk over its slots in TMEM and writes one
-  // partial; the segments of one (task, chunk) are consecutive (k_finalize sums them in order).
+  // partial; the segments of one (task, chunk) are consecutive (k_finalize_multi sums them in order).
   // The schedule depends only on (batch, width), so a projection group reduces in exactly the
   // order of the single-projection calls.
   struct DyVecs {

@@ -40,7 +40,7 @@ struct Meta {
   // segments of the fused dY pass (task, 512-column chunk, range [s0, s1) of the task's slot
   // list); CTA b runs segments [dy_cta_off[b], dy_cta_off[b+1]) (static balanced schedule,
   // ndycta CTAs); the segments of (task t, chunk c) are [dy_task_unit_off[t*dy_nch + c],
-  // dy_task_unit_off[t*dy_nch + c + 1]).  k_finalize mode 1 uses them when use_dy_units != 0
+  // dy_task_unit_off[t*dy_nch + c + 1]) (k_finalize_multi sums them in order)
   int ndyunits, use_dy_units, ndycta, dy_nch;
   const int* dy_unit_task;
   const int* dy_unit_s0;
@@ -130,13 +130,10 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms, cudaStream_t st,
                  const TpScatter* tp = nullptr);
-// partial[u][chunk][q][128] = sum over the unit's slots: Z[tile rows, chunk cols]^T Slot
+// partial[seg][q][128] = sum over the segment's slots: Z[tile rows, chunk cols]^T Slot, for the
+// segments of meta's k_segred schedule (set for this width)
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,
                    const Meta& meta, float* partial, int num_sms, cudaStream_t st);
-// out = (accumulate ? out : 0) + sum_u partial   (fixed order). mode 0: dA [r, width] rows
-// with stride ld; mode 1: dB [width, rsum] (PEFT layout, row stride rsum).
-void launch_finalize(int mode, const float* partial, int width, const Meta& meta, float* out,
-                     long long ld, int accumulate, cudaStream_t st);
 // Fused dY pass (G slots + dB partials in one dY read) followed by the G finalize.
 // mapH / mapBt: boxes {dypass_span(qp) / 2, 128 tokens} over the H slots and
 // {dypass_span(qp) / 2, 64 o} over B, swizzled with span dypass_span(qp) bytes.
@@ -144,9 +141,11 @@ int dypass_span(int qp);
 void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUtensorMap& mapBt,
                    int width, int qp, const Meta& meta, float* gpart, float* bpart,
                    __nv_bfloat16* gslots, int num_sms, cudaStream_t st);
-// One launch for several finalizations (mode 0 dA / mode 1 dB as in launch_finalize).
-// uoff: the task's unit offsets (meta.task_unit_off) or, with dy = 1, the fused dY pass's
-// (task, chunk) segment offsets (meta.dy_task_unit_off, dy_nch chunks per task).
+// One launch for several finalizations: mode 0 dA [r, width] rows with stride ld, mode 1 dB
+// [width, rsum] (PEFT layout); out = (accumulate ? out : 0) + sum of the partials in fixed order.
+// uoff: the task's unit offsets (meta.task_unit_off) or, with dy = 1, (task, chunk) segment
+// offsets (meta.dy_task_unit_off of the dY pass with sub = 4 blocks of 128 columns per segment,
+// or meta.sr_tc_off of k_segred with sub = 1), dy_nch chunks per task.
 struct FinJob {
   const float* partial;
   float* out;
