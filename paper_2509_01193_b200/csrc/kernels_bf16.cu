@@ -926,6 +926,14 @@ __global__ void __launch_bounds__(288, 1)
 constexpr int SH_KB = 2, SH_P = 4;
 struct ShrinkArgs {
   int K, qv, stages, stage_bytes, P;
+  int kb;          // 64-column K blocks per stage (2; 1 when the adapter operand is wide)
+  // planes mode (a projection group whose bands exceed the 64-wide slot, np * qp > 64): the
+  // accumulator's columns [p pq, p pq + pq) go to plane p (out + p * plane_stride), each plane
+  // an ordinary single-projection slot buffer; rk / sc = the tasks' real ranks / scales
+  int nplanes, pq;
+  long long plane_stride;
+  const int* rk;
+  const float* sc;
   int per_slot;   // 1: one work item per slot (X tile re-read for every task of a mixed tile;
                   //    equal work per CTA, used when the slots fit in one wave), 0: per tile
   __nv_bfloat16* out;
@@ -952,7 +960,7 @@ __global__ void __launch_bounds__(256, 1)
              const ShrinkArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = args.stages, SB = args.stage_bytes, P = args.P, qv = args.qv;
+  const int S = args.stages, SB = args.stage_bytes, P = args.P, qv = args.qv, KB = args.kb;
   const int vbox = qv * 128;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
   uint64_t* empty = full + 8;
@@ -994,8 +1002,8 @@ __global__ void __launch_bounds__(256, 1)
         shrink_item(meta, args.per_slot, w, m, s_begin, s_end);
         for (int s0 = s_begin; s0 < s_end; s0 += P) {
           const int ns = min(P, s_end - s0);
-          for (int kb = 0; kb < nk; kb += SH_KB) {
-            const int nkb = min(SH_KB, nk - kb);
+          for (int kb = 0; kb < nk; kb += KB) {
+            const int nkb = min(KB, nk - kb);
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], nkb * (R_A_BYTES + ns * vbox));
             uint8_t* st = smem + stage * SB;
@@ -1006,7 +1014,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int i = 0; i < ns; ++i) {
               const int row0 = meta.roff[meta.slot_task[s0 + i]];
               for (int j = 0; j < nkb; ++j)
-                tma_load_2d(st + SH_KB * R_A_BYTES + (j * P + i) * vbox, &mapV, &full[stage],
+                tma_load_2d(st + KB * R_A_BYTES + (j * P + i) * vbox, &mapV, &full[stage],
                             (kb + j) * 64, row0);
             }
             if (++stage == S) stage = 0, phase ^= 1;
@@ -1030,14 +1038,14 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t acc = tmem + b * 256;
-          for (int kb = 0; kb < nk; kb += SH_KB) {
-            const int nkb = min(SH_KB, nk - kb);
+          for (int kb = 0; kb < nk; kb += KB) {
+            const int nkb = min(KB, nk - kb);
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t st0 = smem_u32(smem + stage * SB);
             for (int j = 0; j < nkb; ++j) {
               const uint32_t a0 = st0 + j * R_A_BYTES;
-              const uint32_t b0 = st0 + SH_KB * R_A_BYTES + j * P * vbox;
+              const uint32_t b0 = st0 + KB * R_A_BYTES + j * P * vbox;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 mma_bf16(acc, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), id,
@@ -1058,7 +1066,8 @@ __global__ void __launch_bounds__(256, 1)
       float z[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) z[j] = 0.0f;
-      store_slot_row(args.out, meta.nslots, lrow, z, 0.0f, 0);
+      for (int pl = 0; pl < args.nplanes; ++pl)
+        store_slot_row(args.out + pl * args.plane_stride, meta.nslots, lrow, z, 0.0f, 0);
     }
     int it = 0;
     bool first = true;
@@ -1078,6 +1087,21 @@ __global__ void __launch_bounds__(256, 1)
           const int s = s0 + i;
           const int ts = meta.slot_task[s];
           float v[64];
+          if (args.nplanes > 1) {   // planes mode (P = 1): plane pl <- columns [pl pq, pl pq + pq)
+            const bool mine = ts == my_task;
+            for (int pl = 0; pl < args.nplanes; ++pl) {
+              const uint32_t ta = tmem + ((q * 32u) << 16) + b * 256 + pl * args.pq;
+              tmem_ld32(ta, *reinterpret_cast<float(*)[32]>(v));
+              if (args.pq > 32) tmem_ld32(ta + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+              else {
+#pragma unroll
+                for (int j = 32; j < 64; ++j) v[j] = 0.0f;
+              }
+              store_slot_row(args.out + pl * args.plane_stride, s, lrow, v, mine ? args.sc[ts] : 0.0f,
+                             mine ? args.rk[ts] : 0);
+            }
+            continue;
+          }
           const uint32_t ta = tmem + ((q * 32u) << 16) + b * 256 + i * qv;
           tmem_ld32(ta, *reinterpret_cast<float(*)[32]>(v));
           if (qv > 32) tmem_ld32(ta + 32, *reinterpret_cast<float(*)[32]>(v + 32));
@@ -1781,15 +1805,21 @@ bool shrink_applies(int ntiles, int num_sms) {
 }
 
 void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
-                   __nv_bfloat16* slots, int num_sms, cudaStream_t st) {
+                   __nv_bfloat16* slots, int num_sms, cudaStream_t st, const ShrinkPlanes* planes) {
   constexpr int kMaxSmem = 232448;
   ShrinkArgs a;
   a.K = K;
   a.qv = meta.qp;
+  a.nplanes = 1, a.pq = 0, a.plane_stride = 0, a.rk = nullptr, a.sc = nullptr;
+  if (planes) {
+    a.nplanes = planes->np, a.pq = planes->pq, a.plane_stride = planes->plane_stride;
+    a.rk = planes->ranks, a.sc = planes->scales;
+  }
   a.per_slot = meta.nslots <= num_sms ? 1 : 0;
   if (const char* e = getenv("LOBRA_SHRINK_PER_TILE")) a.per_slot = (e[0] == '1') ? 0 : a.per_slot;
-  a.P = a.per_slot ? 1 : std::max(1, std::min(SH_P, meta.max_slots_per_tile));
-  a.stage_bytes = SH_KB * (R_A_BYTES + a.P * a.qv * 128);
+  a.P = (a.per_slot || planes) ? 1 : std::max(1, std::min(SH_P, meta.max_slots_per_tile));
+  a.kb = a.qv > 64 ? 1 : SH_KB;   // a wide adapter operand: 1 K block per stage, more stages
+  a.stage_bytes = a.kb * (R_A_BYTES + a.P * a.qv * 128);
   a.stages = std::min(8, (kMaxSmem - 1024 - 256) / a.stage_bytes);
   a.out = slots;
   a.meta = meta;

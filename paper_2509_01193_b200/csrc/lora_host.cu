@@ -719,11 +719,29 @@ extern "C" size_t lobra_lora_saved_bytes(const lobra_problem* prob, const lobra_
   return std::max<size_t>(L.saved, 256);
 }
 
+namespace lobra {
+namespace {
+// skip_shrink: Hs already holds this projection's H_s slots (a wide projection group computed
+// every projection's H_s in one pass over X, lobra_lora_group_fwd)
+lobra_status lora_fwd_impl(const lobra_problem* prob, const lobra_batch* batch,
+                           const lobra_adapters* ad, const void* X, const void* W, void* Y, void* Hs,
+                           void* ws, size_t ws_bytes, lobra_stream_t stream_, bool skip_shrink);
+}  // namespace
+}  // namespace lobra
+
 extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_batch* batch,
                                        const lobra_adapters* ad, const void* X, const void* W,
                                        void* Y, void* Hs, void* ws, size_t ws_bytes,
                                        lobra_stream_t stream_) {
   clear_error();
+  return lora_fwd_impl(prob, batch, ad, X, W, Y, Hs, ws, ws_bytes, stream_, false);
+}
+
+namespace lobra {
+namespace {
+lobra_status lora_fwd_impl(const lobra_problem* prob, const lobra_batch* batch,
+                           const lobra_adapters* ad, const void* X, const void* W, void* Y, void* Hs,
+                           void* ws, size_t ws_bytes, lobra_stream_t stream_, bool skip_shrink) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   DevCtx* ctx = nullptr;
   Plan P;
@@ -766,7 +784,9 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
     if ((s = make_map(&mW, W, in, out, 64, bn)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mB, Bop, L.ld8, out, 64, bn)) != LOBRA_OK) return s;
-    if (shrink_applies(P.ntiles, ctx->num_sms)) {
+    if (skip_shrink) {
+      // H_s computed by the caller (wide projection group)
+    } else if (shrink_applies(P.ntiles, ctx->num_sms)) {
       CUtensorMap mAk;
       if ((s = make_map(&mAk, ad->A, in, (uint64_t)P.rsum, 64, P.qp)) != LOBRA_OK) return s;
       Prof p_(LOBRA_K_ROWPROJ, st);
@@ -809,6 +829,9 @@ extern "C" lobra_status lobra_lora_fwd(const lobra_problem* prob, const lobra_ba
     return comm_tp_allreduce_f32(prob->tp, static_cast<float*>(Y), (size_t)P.T * out, st);
   return LOBRA_OK;
 }
+
+}  // namespace
+}  // namespace lobra
 
 extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_batch* batch,
                                        const lobra_adapters* ad, const void* X, const void* W,
@@ -1037,6 +1060,30 @@ void group_plan(const lobra_group_problem* g, const lobra_batch* b, const lobra_
   build_plan(b, &a0, (int)g->in, (int)max_out(g), num_sms, P, g->num_proj, outs, {(int)g->in});
 }
 
+// Wide group (bands exceed the 64-wide slot, np * qp in (64, 256], e.g. q/k/v at rank 64): the
+// per-projection sequence, except that ONE k_shrink pass over X computes every projection's
+// H_s into its own slot buffer (planes), so X is read once for the shrinks instead of np times.
+bool wide_planes(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOBRA_WIDE_GROUP");   // 0: plain per-projection sequence (A/B)
+    v = e ? atoi(e) : 1;
+  }
+  if (!v || g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld() || !gemm_uses_pair() ||
+      g->tp_kind == LOBRA_TP_ROW || g->num_proj < 2)
+    return false;
+  int qp = 16;
+  for (int t = 0; t < ga->num_tasks; ++t) qp = std::max(qp, (ga->ranks[t] + 15) & ~15);
+  if (g->num_proj * qp <= kSlotW || g->num_proj * qp > 256) return false;
+  long long T = 0;
+  for (int k = 0; k < b->num_seqs; ++k) T += b->seq_lens[k];
+  return shrink_applies((int)((T + kTileM - 1) / kTileM), sms_hint());
+}
+// workspace of the wide-group shrink: group metadata + the packed group A
+size_t planes_ws(const lobra_group_problem* g, const Plan& P) {
+  return align256(P.buf.size() * 4) + align256((size_t)P.ntasks * P.np * P.qp * g->in * 2);
+}
+
 // workspace / saved sizes of the fallback (per-projection sequences)
 size_t fallback_ws(const lobra_group_problem* g, const lobra_batch* b, const lobra_group_adapters* ga) {
   size_t m = 0;
@@ -1044,6 +1091,11 @@ size_t fallback_ws(const lobra_group_problem* g, const lobra_batch* b, const lob
     lobra_problem sp = single_problem(g, p, g->tp_kind);
     lobra_adapters sa = single_adapters(ga, p);
     m = std::max(m, lobra_lora_workspace_bytes(&sp, b, &sa));
+  }
+  if (wide_planes(g, b, ga)) {
+    Plan P;
+    group_plan(g, b, ga, sms_hint(), P);
+    m = std::max(m, planes_ws(g, P));
   }
   return m;
 }
@@ -1091,13 +1143,45 @@ extern "C" lobra_status lobra_lora_group_fwd(const lobra_group_problem* g, const
   if (!W || !Y) return fail(LOBRA_ERR_INPUT, "W[] / Y[] pointer arrays missing");
   const int np = g->num_proj;
   if (!group_fused(g, ga)) {
-    // fallback: np single-projection forwards, each with its own band of Hs
+    // fallback: np single-projection forwards, each with its own band of Hs; a wide group
+    // computes every projection's H_s first in one pass over X
     const size_t each = fallback_saved_each(g, batch, ga);
+    const bool planes = wide_planes(g, batch, ga);
+    if (planes) {
+      cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+      DevCtx* ctx = nullptr;
+      if ((s = get_ctx(&ctx)) != LOBRA_OK) return s;
+      Plan P;
+      group_plan(g, batch, ga, sms_hint(), P);
+      if (!X || !Hs || !ws) return fail(LOBRA_ERR_INPUT, "null device pointer");
+      if (ws_bytes < planes_ws(g, P)) return fail(LOBRA_ERR_INPUT, "workspace too small: %zu < %zu", ws_bytes,
+                                                  planes_ws(g, P));
+      if (P.T > 0) {
+        uint8_t* w = static_cast<uint8_t*>(ws);
+        if ((s = upload_meta(ctx, P.buf, w, st)) != LOBRA_OK) return s;
+        const Meta meta = device_meta(P, w);
+        const Meta meta_g = group_meta(P, w);
+        const int in = (int)g->in;
+        auto* Ag = reinterpret_cast<__nv_bfloat16*>(w + align256(P.buf.size() * 4));
+        {
+          const __nv_bfloat16* As[4];
+          for (int p = 0; p < np; ++p) As[p] = static_cast<const __nv_bfloat16*>(ga->A[p]);
+          Prof p_(LOBRA_K_PAD, st);
+          launch_pack_a_group(As, np, P.qp, in, meta, Ag, st);
+        }
+        CUtensorMap mX, mAgk;
+        if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
+        if ((s = make_map(&mAgk, Ag, in, (uint64_t)P.ntasks * np * P.qp, 64, np * P.qp)) != LOBRA_OK) return s;
+        const ShrinkPlanes pl{np, P.qp, (long long)(each / 2), meta.ranks, meta.scales};
+        Prof p_(LOBRA_K_ROWPROJ, st);
+        launch_shrink(mX, mAgk, in, meta_g, static_cast<__nv_bfloat16*>(Hs), ctx->num_sms, st, &pl);
+      }
+    }
     for (int p = 0; p < np; ++p) {
       lobra_problem sp = single_problem(g, p, g->tp_kind);
       lobra_adapters sa = single_adapters(ga, p);
-      if ((s = lobra_lora_fwd(&sp, batch, &sa, X, W[p], Y[p], static_cast<uint8_t*>(Hs) + p * each, ws,
-                              ws_bytes, stream_)) != LOBRA_OK)
+      if ((s = lora_fwd_impl(&sp, batch, &sa, X, W[p], Y[p], static_cast<uint8_t*>(Hs) + p * each, ws,
+                             ws_bytes, stream_, planes)) != LOBRA_OK)
         return s;
     }
     return LOBRA_OK;

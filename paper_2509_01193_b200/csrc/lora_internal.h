@@ -93,8 +93,18 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
 // tiles fill >= 3/4 of the SMs (LOBRA_SHRINK=0 disables).  mapV: the adapter operand
 // (A_cat, or the packed group A) with box {64, meta.qp}.
 bool shrink_applies(int ntiles, int num_sms);
+// planes: a projection group whose bands do not fit one 64-wide slot (np * pq > 64, <= 256):
+// ONE pass over X (meta.qp = np * pq rows of the packed group A per task), projection p's H_s
+// written to its own single-projection slot buffer `slots + p * plane_stride` (elements).
+struct ShrinkPlanes {
+  int np, pq;
+  long long plane_stride;
+  const int* ranks;     // device: the tasks' ranks / scales (meta of the single projections)
+  const float* scales;
+};
 void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, const Meta& meta,
-                   __nv_bfloat16* slots, int num_sms, cudaStream_t st);
+                   __nv_bfloat16* slots, int num_sms, cudaStream_t st,
+                   const ShrinkPlanes* planes = nullptr);
 // LDGSTS-producer variant (default; LOBRA_RP_TMA=1 selects the TMA-producer kernel):
 // Z raw [T, K]; mapVk K-major adapter operand, box {64, qp} (A_cat forward, B^T backward).
 bool rowproj_uses_ld();

@@ -260,3 +260,21 @@ def test_group_many_tasks_full_batch():
     g, X, ts_, _ = _run(wl, 256, [192, 64, 64], seed=3)
     s, _, _, _ = _run(wl, 256, [192, 64, 64], seed=3, group=False)
     _same(g, s)
+
+
+def test_wide_group_planes_full_batch():
+    """A group whose bands exceed the 64-wide slot (3 x rank 64 = 192 columns, C3's q/k/v):
+    one k_shrink pass over X writes every projection's H_s plane (112 tiles, mixed ranks
+    8-64, ragged last tile); results bitwise those of the single-projection calls."""
+    rng = np.random.default_rng(12)
+    lens = []
+    while sum(lens) < 14300:
+        lens.append(int(rng.integers(20, 400)))
+    lens[-1] -= sum(lens) - 14300
+    ranks = [8, 16, 32, 64] * 2
+    ts = [synth.TaskSpec(f"t{i}", 0, 0, 1, r, 0.5 + 0.5 * (i % 4)) for i, r in enumerate(ranks)]
+    wl = synth.Workload("wide", ts, np.array(lens, np.int32),
+                        np.array(sorted(i % 8 for i in range(len(lens))), np.int32), 0)
+    g, X, ts_, _ = _run(wl, 256, [192, 64, 64], seed=4)
+    s, _, _, _ = _run(wl, 256, [192, 64, 64], seed=4, group=False)
+    _same(g, s)
