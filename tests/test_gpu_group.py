@@ -278,3 +278,55 @@ def test_wide_group_planes_full_batch():
     g, X, ts_, _ = _run(wl, 256, [192, 64, 64], seed=4)
     s, _, _, _ = _run(wl, 256, [192, 64, 64], seed=4, group=False)
     _same(g, s)
+
+
+def test_wide_group_c3_full_size_bitwise():
+    """BASELINE config 3 at full size in the bench launch configuration: q/k/v (4096 -> 4096)
+    over the C3 batch (16 tasks, ranks 8-64: a wide group, planes shrink, 512 tiles), device
+    tensors; group == single-projection calls bit for bit (the single path is checked against
+    the oracle at this size in test_gpu_lora.test_bf16_c3_q_projection_full_size)."""
+    torch = _torch()
+    from paper_2509_01193_b200 import _lib
+    dev = torch.device("cuda:0")
+    wl = synth.config_c3()
+    T, d_in, outs = wl.T, 4096, [4096, 4096, 4096]
+    r, s, L, K = wl.ranks, wl.scales, wl.seq_lens, wl.seq_task
+    Rs = int(r.sum())
+    g = torch.Generator(device=dev).manual_seed(5)
+    rn = lambda *sh, sc=1.0: (torch.randn(*sh, generator=g, device=dev) * sc).to(torch.bfloat16)
+    X = rn(T, d_in)
+    Ws = [rn(o, d_in, sc=d_in ** -0.5) for o in outs]
+    As = [rn(Rs, d_in, sc=d_in ** -0.5) for _ in outs]
+    Bs = [rn(o, Rs, sc=0.125) for o in outs]
+    dYs = [rn(T, o) for o in outs]
+
+    def run(group):
+        Ys = [torch.empty(T, o, device=dev, dtype=torch.bfloat16) for o in outs]
+        dX = torch.empty(T, d_in, device=dev, dtype=torch.bfloat16)
+        dA = [torch.empty(Rs, d_in, device=dev) for _ in outs]
+        dB = [torch.empty(o, Rs, device=dev) for o in outs]
+        if group:
+            ws = torch.empty(_lib.lobra_lora_group_workspace_bytes(_lib.LOBRA_BF16, d_in, outs, L, K, r, s),
+                             device=dev, dtype=torch.uint8)
+            Hs = torch.empty(_lib.lobra_lora_group_saved_bytes(_lib.LOBRA_BF16, d_in, outs, L, K, r, s),
+                             device=dev, dtype=torch.uint8)
+            _lib.lobra_lora_group_fwd(X, Ws, As, Bs, r, s, L, K, Ys, Hs, ws)
+            _lib.lobra_lora_group_bwd(X, Ws, As, Bs, r, s, L, K, Hs, dYs, dX, dA, dB, ws)
+        else:
+            for p, o in enumerate(outs):
+                ws = torch.empty(_lib.lobra_lora_workspace_bytes(_lib.LOBRA_BF16, d_in, o, L, K, r, s),
+                                 device=dev, dtype=torch.uint8)
+                Hs = torch.empty(_lib.lobra_lora_saved_bytes(_lib.LOBRA_BF16, d_in, o, L, K, r, s),
+                                 device=dev, dtype=torch.uint8)
+                _lib.lobra_lora_fwd(X, Ws[p], As[p], Bs[p], r, s, L, K, Ys[p], Hs, ws)
+                _lib.lobra_lora_bwd(X, Ws[p], As[p], Bs[p], r, s, L, K, Hs, dYs[p], dX, dA[p], dB[p], ws,
+                                    accumulate_dx=p > 0)
+        torch.cuda.synchronize()
+        return Ys, dX, dA, dB
+
+    a, b = run(True), run(False)
+    for p in range(3):
+        assert torch.equal(a[0][p], b[0][p]), f"Y[{p}]"
+        assert torch.equal(a[2][p], b[2][p]), f"dA[{p}]"
+        assert torch.equal(a[3][p], b[3][p]), f"dB[{p}]"
+    assert torch.equal(a[1], b[1]), "dX"
