@@ -178,7 +178,10 @@ LOBRA_API lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_bat
  * X is read ONCE for all the shrinks H_s,p and ONCE for all the dA_p reductions: the
  * H_s / G_s slots hold one qp-column band per projection (qp = max rank padded to 16;
  * bands used when num_proj * qp <= 64 and dtype is bf16).  Otherwise the call runs the
- * num_proj single-projection sequences internally (same results, no X sharing).
+ * num_proj single-projection sequences internally (same results); for bf16 with
+ * 64 < num_proj * qp <= 256 and a batch that fills >= 3/4 of the SMs with 128-token tiles,
+ * the forward still reads X once: one shrink pass writes every projection's H_s into its
+ * own single-projection slot buffer inside Hs (the dA reductions stay per projection).
  * TP: all projections of a group have tp_kind; a COLUMN group all-reduces dX once at the
  * end of the backward; a ROW group all-reduces every Y_p in the forward.
  * Hs: one buffer of lobra_lora_group_saved_bytes bytes, written by the forward, read by
