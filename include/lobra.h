@@ -401,6 +401,21 @@ LOBRA_API lobra_status lobra_propose_configs(const lobra_thruput_table* table, i
                                              int32_t* keep);
 
 /* ------------------------------------------------------------------------------
+ * Replica time cost model, App. D, with 1F1B pipeline parallel.
+ * Bucket j holds d[j] >= 0 sequences of (padded) length s[j], 1 <= s[j] <= max_tokens (M,
+ * the configuration's maximum supportable length); full micro-batches hold
+ * b_j = floor(M / s_j) sequences: d_j = m_j b_j + r_j.  With the fitted per-chunk time
+ * t(b, s) = c0 + c1 b s + c2 b s^2 (b >= 1; t(0, s) = 0; reading Q28):
+ *   *out = sum_j (m_j t(b_j, s_j) + t(r_j, s_j)) + (pp_stages - 1) x (longest existing chunk)
+ * (Eq. appendix_cost_model_pp_varlen; pp_stages = 1 is the no-PP equation; reading Q29: the
+ * max ranges over the chunks that exist).  Host only, no device work.
+ * Errors: LOBRA_ERR_INPUT for num_buckets < 1, pp_stages < 1, max_tokens < 1, a null pointer,
+ * d[j] < 0 or s[j] outside [1, max_tokens]. */
+LOBRA_API lobra_status lobra_replica_time(int32_t num_buckets, const int32_t* d, const int32_t* s,
+                                          int64_t max_tokens, int32_t pp_stages, double c0,
+                                          double c1, double c2, double* out);
+
+/* ------------------------------------------------------------------------------
  * Communication (NCCL over NVLink/NVSwitch).  One process per GPU.
  * ------------------------------------------------------------------------------ */
 /* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (e.g. with

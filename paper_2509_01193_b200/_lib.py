@@ -30,7 +30,7 @@ EXPORTED = [
     "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
     "lobra_swiglu_bwd", "lobra_add", "lobra_symm_create", "lobra_symm_open", "lobra_symm_destroy",
     "lobra_symm_data", "lobra_symm_allreduce", "lobra_comm_from_symm", "lobra_comm_attach_symm",
-    "lobra_attn_workspace_bytes", "lobra_attn_fwd",
+    "lobra_attn_workspace_bytes", "lobra_attn_fwd", "lobra_replica_time",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer", "comm"]
 
@@ -198,6 +198,9 @@ def load() -> C.CDLL:
     lib.lobra_profile_read.restype = C.c_int
     lib.lobra_profile_read.argtypes = [C.POINTER(Profile), C.c_int]
     lib.lobra_launch_count.restype = C.c_int64
+    lib.lobra_replica_time.restype = C.c_int
+    lib.lobra_replica_time.argtypes = [C.c_int32, _i32p, _i32p, C.c_int64, C.c_int32, C.c_double,
+                                       C.c_double, C.c_double, C.POINTER(C.c_double)]
     lib.lobra_propose_configs.restype = C.c_int
     lib.lobra_propose_configs.argtypes = [C.POINTER(ThruputTable), _i32p, _i32p]
     lib.lobra_plan_deployment.restype = C.c_int
@@ -507,6 +510,18 @@ def lobra_plan_deployment(tp, max_tokens, cost, n_gpus, lens, batch_size=0, grid
     return {"status": st, "replicas": reps, "boundaries": bnd[:nb], "demands": dem[:nb],
             "plans_total": o.plans_total, "plans_solved": o.plans_solved, "gpus_used": o.gpus_used,
             "t_hat": int(o.t_hat)}
+
+
+def lobra_replica_time(d, s, max_tokens, pp_stages, c0, c1, c2) -> float:
+    """App. D replica time with 1F1B bubble (include/lobra.h): buckets (d[j] sequences of
+    length s[j]), micro-batch token limit max_tokens, t(b, s) = c0 + c1 b s + c2 b s^2."""
+    d, s = _i32(d), _i32(s)
+    out = C.c_double(0.0)
+    st = load().lobra_replica_time(len(d), d.ctypes.data_as(_i32p), s.ctypes.data_as(_i32p), int(max_tokens),
+                                   int(pp_stages), float(c0), float(c1), float(c2), C.byref(out))
+    if st != LOBRA_OK:
+        raise LobraError(st, load().lobra_last_error().decode())
+    return out.value
 
 
 def lobra_propose_configs(tp, pp, seq_lens, thruput, gpu_counts):

@@ -780,3 +780,28 @@ extern "C" lobra_status lobra_propose_configs(const lobra_thruput_table* tb, int
   }
   return LOBRA_OK;
 }
+
+// ------------------------------------------------------------------ App. D replica time
+// T = sum_j (m_j t(b_j, s_j) + t(r_j, s_j)) + (p - 1) max over existing chunks
+extern "C" lobra_status lobra_replica_time(int32_t R, const int32_t* d, const int32_t* s, int64_t M,
+                                          int32_t pp, double c0, double c1, double c2, double* out) {
+  using namespace lobra;
+  clear_error();
+  if (R < 1 || pp < 1 || M < 1 || !d || !s || !out)
+    return fail(LOBRA_ERR_INPUT, "replica_time: need num_buckets >= 1, pp_stages >= 1, max_tokens >= 1");
+  auto t = [&](int64_t b, int64_t len) {
+    return b <= 0 ? 0.0 : c0 + c1 * (double)b * (double)len + c2 * (double)b * (double)len * (double)len;
+  };
+  double compute = 0.0, longest = 0.0;
+  for (int j = 0; j < R; ++j) {
+    if (d[j] < 0 || s[j] < 1 || s[j] > M)
+      return fail(LOBRA_ERR_INPUT, "replica_time: bucket %d: d = %d, s = %d (need d >= 0, 1 <= s <= M)", j,
+                  d[j], s[j]);
+    const int64_t b = M / s[j], m = d[j] / b, r = d[j] % b;
+    const double full = m > 0 ? t(b, s[j]) : 0.0, rem = r > 0 ? t(r, s[j]) : 0.0;
+    compute += (double)m * full + rem;
+    longest = std::max(longest, std::max(full, rem));
+  }
+  *out = compute + (double)(pp - 1) * longest;
+  return LOBRA_OK;
+}
