@@ -5,11 +5,15 @@
 //              tile's adapter slots ("K-extension"): "the computation of the base
 //              model can be fused into a batched operation whilst ... multiple LoRA
 //              adapters ... customized operations".
-// k_rowproj  : the rank-r shrink H_s = s_t X A_t^T (and the backward G_s = s_t dY B_t),
-//              HBM-bound; CTAs per 128-row tile (split-K when tiles are few) stream Z once.
-// k_segred   : the token reductions dA_t = X^T G_s and dB_t = dY^T H_s on tensor cores,
-//              Z tiles used as MN-major A operands (one HBM read of Z), deterministic
-//              two-pass (partials + k_finalize_multi in fixed order).
+// k_shrink   : the forward rank-r shrink H_s = s_t X A_t^T, HBM-bound: one CTA per slot (or
+//              per tile) over the whole K, deep TMA ring, the slots of a tile as one MMA;
+//              planes mode for wide projection groups.
+// k_rowproj  : the same with split-K over CTAs (small batches; the unfused backward G_s).
+// k_dypass   : the fused backward dY pass: G_s = s_t dY B_t partials and dB_t partials from
+//              ONE read of dY (static balanced schedule); k_gfin writes the G slots.
+// k_segred   : the token reductions dA_t = X^T G_s (and unfused dB_t = dY^T H_s) on tensor
+//              cores, Z tiles used as MN-major A operands (one HBM read of Z), static balanced
+//              schedule, deterministic two-pass (segment partials + k_finalize_multi).
 // See DESIGN.md "Kernels" for layouts and the roofline of each.
 #include <cuda_bf16.h>
 
