@@ -320,9 +320,15 @@ typedef struct {
  * sequences); 1 = packed micro-batches ("can also be applied when
  * packing is employed"; reading Q6b): the replica's sequences in (bucket desc, index)
  * order filled next-fit into chunks of at most M_i REAL tokens.
- * node_cap: max branch-and-bound nodes (<= 0: default 2e7); on hitting it the best
- * incumbent is returned with LOBRA_ERR_BUDGET.  Errors: LOBRA_ERR_INPUT,
- * LOBRA_ERR_INFEASIBLE.  Host only; thread-safe (no global state). */
+ * Eq. 3 (mode 0) is solved exactly: 1 group trivially, 2 groups by a pseudo-polynomial DP,
+ * >= 3 groups by branch-and-bound over the replica rounds q_ij = ceil(d_ij / p_i) (LP and
+ * per-bucket integer-covering Lagrangian bounds) followed by the lexicographic
+ * canonicalisation of reading Q12 (csrc/eq3_bb.cpp).
+ * node_cap: branch-and-bound node budget for >= 3 groups (<= 0: default 1e6 nodes, ~5-10 s);
+ * when it is exhausted the call returns LOBRA_ERR_BUDGET with the LENGTH-BASED d (mode 1's)
+ * in `out` -- never a silent substitute: the status says the Eq. 3 optimum was not reached.
+ * Errors: LOBRA_ERR_INPUT, LOBRA_ERR_INFEASIBLE, LOBRA_ERR_BUDGET.  Host only; thread-safe
+ * (no global state). */
 LOBRA_API lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
                             int32_t grid_step, int32_t grid_max, int32_t R, int32_t mode,
                             int32_t chunking, int64_t node_cap, lobra_dispatch_out* out);
@@ -359,7 +365,7 @@ typedef struct {
   int64_t* demands;            /* [R] out: B_j                                            */
   int32_t num_buckets;         /* out                                                     */
   int32_t plans_total;         /* out: maximal covering plans                             */
-  int32_t plans_solved;        /* out: plans kept by the lower-bound filter               */
+  int32_t plans_solved;        /* out: plans kept by the Theorem-1 filter (each decided exactly: solved, or proven worse than the best by its Eq. 3 lower bound) */
   int32_t gpus_used;           /* out                                                     */
   int64_t t_hat;               /* out: Eq. 3 objective of the chosen plan                 */
 } lobra_plan_out;
@@ -471,13 +477,17 @@ LOBRA_API lobra_status lobra_adapter_allreduce(lobra_comm comm, float* flat_grad
  *     p = p - lr * ( (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps) + wd * p )
  * over a flat fp32 master-parameter buffer with per-group hyper-parameters (multi-tenant:
  * one group per task).  params/m/v are updated in place; grads are read.  group: device
- * uint8 [count] group id per element, or NULL (every element in group 0).  hp: host
- * array [num_groups], 1 <= num_groups <= 64.  params_bf16: optional device bf16 [count]
- * copy of the updated parameters (what the LoRA kernels read), or NULL.  All device
- * pointers 16-byte aligned.  Errors: LOBRA_ERR_INPUT, LOBRA_ERR_CUDA.
+ * uint8 [count] group id per element, or NULL (every element in group 0); elements whose
+ * id is >= num_groups are left untouched.  hp: host array [num_groups], 1 <= num_groups
+ * <= 64.  hp[k].step is group k's own step count t >= 1 in the bias corrections (a task
+ * that joined later has taken fewer steps than the others); 0 = use `step`.
+ * params_bf16: optional device bf16 [count] copy of the updated parameters (what the LoRA
+ * kernels read), or NULL.  All device pointers 16-byte aligned.  Errors: LOBRA_ERR_INPUT,
+ * LOBRA_ERR_CUDA.
  * ------------------------------------------------------------------------------ */
 typedef struct {
   float lr, beta1, beta2, eps, weight_decay;
+  int64_t step;
 } lobra_adamw_hparams;
 LOBRA_API lobra_status lobra_adamw_step(float* params, void* params_bf16, const float* grads,
                                         float* m, float* v, const uint8_t* group, size_t count,

@@ -2,7 +2,8 @@
 
 PAPER.md P:709: "We use the Adam optimizer [adam, adamw] for all experiments."  AdamW
 (decoupled weight decay), written out per element, one hyper-parameter set per group
-(task):
+(task), t = the group's own step count (hparams[k]["step"] when given, else `step`: a task
+that joined the joint run later has taken fewer steps):
     g = s * grad
     m_t = b1 m_{t-1} + (1 - b1) g
     v_t = b2 v_{t-1} + (1 - b2) g^2
@@ -22,9 +23,10 @@ def adamw_step(p, g, m, v, group, hparams, step, grad_scale=1.0):
     for k, h in enumerate(hparams):
         sel = group == k
         b1, b2 = h["beta1"], h["beta2"]
+        t = h.get("step") or step
         m[sel] = b1 * m[sel] + (1 - b1) * g[sel]
         v[sel] = b2 * v[sel] + (1 - b2) * g[sel] ** 2
-        mh = m[sel] / (1 - b1 ** step)
-        vh = v[sel] / (1 - b2 ** step)
+        mh = m[sel] / (1 - b1 ** t)
+        vh = v[sel] / (1 - b2 ** t)
         p[sel] = p[sel] - h["lr"] * (mh / (np.sqrt(vh) + h["eps"]) + h["weight_decay"] * p[sel])
     return p, m, v

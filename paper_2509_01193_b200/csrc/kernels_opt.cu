@@ -26,6 +26,7 @@ struct AdamArgs {
 
 __device__ __forceinline__ float adam_one(float p, float g, float& m, float& v, int k,
                                           const AdamArgs& a) {
+  if (k >= a.num_groups) return p;   // not an adapter element of any group: untouched
   g *= a.grad_scale;
   m = a.b1[k] * m + (1.0f - a.b1[k]) * g;
   v = a.b2[k] * v + (1.0f - a.b2[k]) * g * g;
@@ -99,8 +100,10 @@ extern "C" lobra_status lobra_adamw_step(float* params, void* params_bf16, const
     if (!(h.beta1 >= 0 && h.beta1 < 1 && h.beta2 >= 0 && h.beta2 < 1 && h.eps > 0))
       return fail(LOBRA_ERR_INPUT, "group %d: need 0 <= beta < 1 and eps > 0", k);
     a.lr[k] = h.lr, a.b1[k] = h.beta1, a.b2[k] = h.beta2, a.eps[k] = h.eps, a.wd[k] = h.weight_decay;
-    a.c1[k] = (float)(1.0 / (1.0 - std::pow((double)h.beta1, (double)step)));
-    a.c2[k] = (float)(1.0 / (1.0 - std::pow((double)h.beta2, (double)step)));
+    const int64_t t = h.step > 0 ? h.step : step;
+    if (h.step < 0) return fail(LOBRA_ERR_INPUT, "group %d: step must be >= 0", k);
+    a.c1[k] = (float)(1.0 / (1.0 - std::pow((double)h.beta1, (double)t)));
+    a.c2[k] = (float)(1.0 / (1.0 - std::pow((double)h.beta2, (double)t)));
   }
   a.grad_scale = grad_scale;
   a.num_groups = num_groups;

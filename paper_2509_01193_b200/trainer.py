@@ -54,6 +54,7 @@ class MultiTaskLoRATrainer:
         self.layer = LoraLayer(self.shapes, [t.rank for t in self.tasks], [t.scale for t in self.tasks],
                                self.dev, torch.bfloat16, comm=comm, seed=seed)
         self.step_count = 0
+        self.task_steps = {t.name: 0 for t in self.tasks}   # optimizer steps taken per task
         self._new_micro_batch = True
         n = self.layer.flat_grad.numel()
         self.params = torch.empty(n, dtype=torch.float32, device=self.dev)
@@ -88,7 +89,10 @@ class MultiTaskLoRATrainer:
             self._block(self.group, p, "B").copy_(tid_of_r[None, :].expand(p.d_out, -1).to(torch.uint8))
 
     def hparams(self):
-        return [{"lr": t.lr, "beta1": t.beta1, "beta2": t.beta2, "eps": t.eps, "weight_decay": t.weight_decay}
+        """Per-task AdamW hyper-parameters with each task's own step count (the step the
+        coming update is for): a task added mid-run starts its bias correction at 1."""
+        return [{"lr": t.lr, "beta1": t.beta1, "beta2": t.beta2, "eps": t.eps, "weight_decay": t.weight_decay,
+                 "step": self.task_steps[t.name] + 1}
                 for t in self.tasks]
 
     # ------------------------------------------------------------------ the step
@@ -107,15 +111,19 @@ class MultiTaskLoRATrainer:
         if self._new_micro_batch:
             raise RuntimeError("optimizer_step without a backward in this step")
         self.layer.sync_adapter_grads(stream=stream)
+        hp = self.hparams()
         self.step_count += 1
-        _lib.lobra_adamw_step(self.params, self.layer.flat_grad, self.m, self.v, self.hparams(), self.step_count,
+        _lib.lobra_adamw_step(self.params, self.layer.flat_grad, self.m, self.v, hp, self.step_count,
                               group=self.group, params_bf16=self.params_bf16, grad_scale=grad_scale, stream=stream)
+        for t in self.tasks:
+            self.task_steps[t.name] += 1
         self._new_micro_batch = True
 
     # ------------------------------------------------------------------ checkpoints
     def state_dict(self):
         return {"format": "lobra-lora-adapters-v1", "shapes": self.shapes,
                 "tasks": [dataclasses.asdict(t) for t in self.tasks], "step": self.step_count,
+                "task_steps": dict(self.task_steps),
                 "params": self.params.cpu(), "m": self.m.cpu(), "v": self.v.cpu()}
 
     def load_state_dict(self, sd):
@@ -133,6 +141,8 @@ class MultiTaskLoRATrainer:
         self.m = sd["m"].to(self.dev).clone()
         self.v = sd["v"].to(self.dev).clone()
         self.step_count = int(sd["step"])
+        # checkpoints without per-task counts predate task changes: every task took them all
+        self.task_steps = {t.name: int(sd.get("task_steps", {}).get(t.name, self.step_count)) for t in tasks}
         self._new_micro_batch = True
         self._bind()
 
@@ -175,6 +185,7 @@ class MultiTaskLoRATrainer:
                     self._block(new[0], p, "A")[r0:r1].copy_(
                         torch.randn(r1 - r0, p.d_in, generator=g, device=self.dev) / math.sqrt(p.d_in))
         self.params, self.m, self.v = new
+        self.task_steps = {t.name: self.task_steps.get(t.name, 0) for t in self.tasks}
         self._bind()
 
     def add_task(self, task: TaskConfig, init_seed=0):

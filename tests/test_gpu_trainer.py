@@ -70,9 +70,10 @@ def test_optimizer_step_matches_oracle():
     p0, m0, v0 = (x.double().cpu().numpy() for x in (tr.params, tr.m, tr.v))
     g = tr.layer.flat_grad.double().cpu().numpy()
     grp = tr.group.cpu().numpy()
+    hp = tr.hparams()                    # per-task step counts of the coming update
     tr.optimizer_step()
     torch.cuda.synchronize()
-    pr, mr, vr = OPT.adamw_step(p0, g, m0, v0, grp, tr.hparams(), tr.step_count)
+    pr, mr, vr = OPT.adamw_step(p0, g, m0, v0, grp, hp, tr.step_count)
     scale = lambda a: np.max(np.abs(a)) + 1e-30
     assert np.max(np.abs(tr.params.double().cpu().numpy() - pr)) / scale(pr) <= 1e-5
     assert np.max(np.abs(tr.m.double().cpu().numpy() - mr)) / scale(mr) <= 1e-5
@@ -123,6 +124,37 @@ def test_add_and_remove_task_keep_other_tasks_exactly():
         for pname, (A, B) in tr.task_params(n).items():
             assert torch.equal(A, kept[n][pname][0]) and torch.equal(B, kept[n][pname][1])
     _run_steps(tr, 1, start=20)
+
+
+def test_added_task_first_update_uses_its_own_step():
+    """A task added after k steps takes its first AdamW update with bias correction t = 1
+    (oracle with step = 1 for it, k + 1 for the others), not t = k + 1."""
+    torch = _torch()
+    from paper_2509_01193_b200.trainer import MultiTaskLoRATrainer, TaskConfig
+    tr = MultiTaskLoRATrainer(SMALL, _tasks(), seed=8)
+    _run_steps(tr, 3)
+    tr.add_task(TaskConfig("c", 8, 1.0, lr=2e-3), init_seed=4)
+    hp = tr.hparams()
+    assert [h["step"] for h in hp] == [4, 4, 1]
+    lens, tids = np.array([30, 50, 40], np.int32), np.array([0, 1, 2], np.int32)
+    T = int(lens.sum())
+    io = _io(tr, T, seed=13)
+    tr.forward(lens, tids, io, T)
+    tr.backward(lens, tids, io, T)
+    torch.cuda.synchronize()
+    p0, m0, v0 = (x.double().cpu().numpy() for x in (tr.params, tr.m, tr.v))
+    g = tr.layer.flat_grad.double().cpu().numpy()
+    grp = tr.group.cpu().numpy()
+    tr.optimizer_step()
+    torch.cuda.synchronize()
+    pr, _, _ = OPT.adamw_step(p0, g, m0, v0, grp, hp, tr.step_count)
+    got = tr.params.double().cpu().numpy()
+    assert np.max(np.abs(got - pr)) / (np.max(np.abs(pr)) + 1e-30) <= 1e-5
+    # Adam's first step moves an element by ~lr (|g| >> eps): the new task's B columns
+    sel = (grp == 2) & (np.abs(g) > 1e-4)
+    step_c = np.abs(got[sel] - p0[sel])
+    assert sel.sum() > 0 and np.all(step_c <= 2e-3 * 1.01) and np.median(step_c) > 2e-3 * 0.9
+    assert tr.task_steps == {"a": 4, "b": 4, "c": 1}
 
 
 def test_teacher_student_regression_converges():

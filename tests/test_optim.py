@@ -30,6 +30,37 @@ def test_oracle_matches_torch_adamw():
             assert np.allclose(p[group == k], params[k].detach().numpy(), rtol=1e-12, atol=1e-14)
 
 
+def test_oracle_per_group_step_matches_torch_for_a_late_group():
+    """A group that joins after 3 steps (its own torch param group created then) is the
+    oracle with hparams[k]["step"] = its own count."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5)
+    n = 64
+    p0 = rng.standard_normal(n)
+    group = (np.arange(n) % 2).astype(np.int64)
+    p, m, v = p0.copy(), np.zeros(n), np.zeros(n)
+    t0 = torch.tensor(p0[group == 0], dtype=torch.float64, requires_grad=True)
+    t1 = torch.tensor(p0[group == 1], dtype=torch.float64, requires_grad=True)
+    opt0 = torch.optim.AdamW([t0], lr=1e-3, weight_decay=0.01)
+    opt1 = torch.optim.AdamW([t1], lr=1e-3, weight_decay=0.01)
+    hp = [dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01) for _ in range(2)]
+    for step in range(1, 7):
+        g = rng.standard_normal(n)
+        if step <= 3:                       # group 1 not trained yet: zero gradient, no step
+            g[group == 1] = 0.0
+            p, m, v = O.adamw_step(p, g, m, v, group, hp[:1], step)   # group 1 not in hparams
+        else:
+            hp[1]["step"] = step - 3
+            hp[0]["step"] = step
+            p, m, v = O.adamw_step(p, g, m, v, group, hp, step)
+            t1.grad = torch.tensor(g[group == 1], dtype=torch.float64)
+            opt1.step()
+        t0.grad = torch.tensor(g[group == 0], dtype=torch.float64)
+        opt0.step()
+        assert np.allclose(p[group == 0], t0.detach().numpy(), rtol=1e-12, atol=1e-14)
+        assert np.allclose(p[group == 1], t1.detach().numpy(), rtol=1e-12, atol=1e-14)
+
+
 @pytest.mark.gpu
 def test_gpu_adamw_matches_oracle():
     torch = pytest.importorskip("torch")
