@@ -2,6 +2,7 @@
 """Benchmark of the LobRA multi-LoRA hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lobra|reference]
+    python bench.py --plan-only            # CPU: the N = 1/2/4/8 deployments and dispatches
 
 One STEP = one pass of the whole hot path over one batch:
 per-step dispatch on the host (a7: bucketing DP + exact Eq. 3 + chunking), then for
@@ -9,14 +10,19 @@ every micro-batch of this rank's replica the forward and backward of all seven
 Llama-2-7B projections with every task's adapters (a0-a5, TP collectives a6), then the
 adapter-gradient all-reduce across replicas (a8).
 
-N = 1: BASELINE config 2 (7B shapes, 4 tasks r=16 s=2, skewed lengths <= 4K, T = 16384
-packed, bf16) on 1 x TP1.  N > 1 (launched by torchrun, one rank per GPU): weak scaling,
-N x 16384 tokens of the same task mix per step, dispatched over heterogeneous replicas
-(2: 2xTP1; 4: 2xTP1 + 1xTP2; 8: 4xTP1 + 2xTP2; SURVEY.md §8(d) sweep).
+N = 1 (default workload): BASELINE configs[2] = C3, the largest single-GPU configuration
+(7B shapes, 16 tasks ranks 8-64, long-tail lengths <= 16K, T = 65536 packed, bf16, 1 x TP1);
+a short C2 run (configs[1]) is reported beside it (`c2`).  N > 1 (torchrun, one rank per GPU):
+C5 = weak scaling, N x 65536 tokens of the same 16-task mix per step, dispatched by Eq. 3 over
+the heterogeneous deployment the stage-1 planner (lobra_plan_deployment) picks from TP1 /
+TP2 / TP4 candidates with max tokens per chunk 8192 / 16384 / 32768 (Q25) and a
+cost table built from measured per-TP layer timings (profiles/r2_tp_costs_7b.json, App. D
+"offline profiling" P:1485; `--plan-only` prints the plans).
 
-value = real tokens processed by all ranks / max-over-ranks device time.  Inputs are
-resident in HBM when the timed region starts; every projection input exceeds L2
-(>= 128 MiB per step-input vs 126 MB L2), so no explicit L2 flush is used.
+value = real tokens processed by all ranks / max-over-ranks device time (the whole-job
+aggregate, as the bench contract asks; `per_gpu` = value / N).  Inputs are resident in HBM
+when the timed region starts; every projection input exceeds L2 (>= 128 MiB per step-input
+vs 126 MB L2), so no explicit L2 flush is used.
 """
 from __future__ import annotations
 
@@ -35,8 +41,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "multi-LoRA fwd+bwd tokens/s/GPU at 1/2/4/8 B200; % of bf16 tensor peak"
+WORKLOAD_NAMES = {
+    "c2": "C2 (BASELINE configs[1]): Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
+          "4 tasks r=16 s=2, lengths<=4096 packed, T=16384",
+    "c3": "C3 (BASELINE configs[2]): Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
+          "16 tasks ranks 8/16/32/64 s 0.5-4, lengths<=16384 packed, T=65536",
+    "c5": "C5 (BASELINE configs[4]): Llama-2-7B layer, 7 LoRA projections, C3's 16 tasks, N x 65536 tokens "
+          "per step dispatched by Eq. 3 over the planner's heterogeneous TP1/TP2/TP4 replicas",
+}
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-T_PER_GPU = 16384
 
 
 def load_peaks():
@@ -148,48 +161,88 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ plans
-CANDIDATES = [(1, 16384), (2, 32768)]   # (TP degree, max tokens per chunk), Q25
+C5_CANDIDATES = [(1, 8192), (2, 16384), (4, 32768)]   # (TP degree, max tokens per chunk), Q25
+C5_TOKENS_PER_GPU = 65536
+GRID_MAX = 16384             # longest sequence of C3 / C5 (grid 256)
+COST_UNIT_US = 10.0          # integer cost unit of the dispatch tables (reading Q15)
+ALLREDUCE_GBS = 700.0        # assumed NVLink 5 all-reduce bus bandwidth
 
 
-def deployment_for(n_gpus: int, tasks=None):
-    """(tp, replicas, max_tokens) per deployed group, ordered by (tp, M), chosen by the
-    paper's stage-1 planner (lobra_plan_deployment: §4.2 Eq. 2 + App. A) on a sample of
-    100 x B lengths of the step's task mix with the bench cost model."""
-    if n_gpus == 1:
-        return [(1, 1, 16384)]
-    from paper_2509_01193_b200 import _lib
-    from workloads import synth
-    tasks = tasks or synth.c2_tasks()
-    per_step = synth.pack_tokens(tasks, T_PER_GPU * n_gpus, 4096, seed=7).seq_lens
-    sample = synth.sample_batch(tasks, seed=8, l_max=4096,
-                                per_task=[max(1, 100 * len(per_step) * t.batch_size //
-                                              sum(x.batch_size for x in tasks)) for t in tasks])
-    grid_max = max(m for _, m in CANDIDATES)
-    cands = [(tp, 0, m) for tp, m in CANDIDATES]
-    try:
-        res = _lib.lobra_plan_deployment([c[0] for c in cands], [c[2] for c in cands],
-                                         cost_table(cands, 256, grid_max), n_gpus, sample.seq_lens,
-                                         len(per_step), 256, grid_max, 16)
-        groups = [(tp, int(p), m) for (tp, m), p in zip(CANDIDATES, res["replicas"]) if p > 0]
-        used = sum(tp * p for tp, p, _ in groups)
-        if used == n_gpus:
-            return groups
-    except Exception:
-        pass
-    return [(1, n_gpus, 16384)]
+def tp_costs():
+    """Per-token device time (us) of one Llama-2-7B layer's seven LoRA projections fwd+bwd on
+    a TP-k replica: the measured per-rank shard compute (tools/bench_tp_shapes.py --model 7b
+    --workload c3, profiles/r2_tp_costs_7b.json) plus the four T x h bf16 TP all-reduces per
+    layer at ALLREDUCE_GBS (2 (k-1)/k of the message per rank, ring/two-shot volume)."""
+    p = os.path.join(ROOT, "profiles", "r2_tp_costs_7b.json")
+    comp = {1: 0.70, 2: 0.37, 4: 0.20, 8: 0.11}            # fallback: round-1 C3 scaling
+    src = "fallback (round-1 C3 per-token time / TP)"
+    if os.path.exists(p):
+        d = json.load(open(p))
+        comp = {int(k): float(v) for k, v in d["us_per_token"].items()}
+        src = "measured (profiles/r2_tp_costs_7b.json)"
+    out = {}
+    for tp, us in comp.items():
+        comm = 0.0 if tp == 1 else 4 * 4096 * 2 * 2 * (tp - 1) / tp / (ALLREDUCE_GBS * 1e3)
+        out[tp] = us + comm
+    return out, src
 
 
 def cost_table(groups, grid_step=256, grid_max=32768):
-    """Integer per-sequence cost c_i(u) on the grid (reading Q15): projections are
-    linear in tokens (App. D with a2 = 0 for projection-only layers); TP2 costs half
-    per token plus a communication penalty.  Units ~ 64 tokens."""
+    """Integer per-sequence cost c_i(u) on the grid (reading Q15): the projections are linear
+    in tokens (App. D with a2 = 0 for projection-only layers), c = u * t_tp / unit."""
+    per_tok, _ = tp_costs()
     U = grid_max // grid_step
-    eff = {1: 1.0, 2: 0.89, 4: 0.75, 8: 0.6}
-    out = []
-    for tp, _, _ in groups:
-        out.append([max(1, int(round((k + 1) * grid_step / 64 / (tp * eff.get(tp, 0.5)))))
-                    for k in range(U)])
-    return out
+    return [[max(1, int(round((k + 1) * grid_step * per_tok.get(tp, per_tok[1] / tp) / COST_UNIT_US)))
+             for k in range(U)] for tp, _, _ in groups]
+
+
+def c5_batch(n_gpus: int, step: int):
+    from workloads import synth
+    return synth.pack_tokens(synth.c3_tasks(), C5_TOKENS_PER_GPU * n_gpus, 16384, seed=1000 + step, name="C5")
+
+
+def deployment_for(n_gpus: int):
+    """(tp, replicas, max_tokens) per deployed group, ordered by (tp, M), chosen by the
+    paper's stage-1 planner (lobra_plan_deployment: §4.2 Eq. 2 + App. A) on a sample of
+    100 x B lengths of the step's task mix with the bench cost model.  N = 1 is
+    C3's single TP1 replica (one chunk of the whole 65536-token batch)."""
+    if n_gpus == 1:
+        return [(1, 1, C5_TOKENS_PER_GPU)]
+    from paper_2509_01193_b200 import _lib
+    from workloads import synth
+    tasks = synth.c3_tasks()
+    per_step = c5_batch(n_gpus, 0).seq_lens
+    sample = synth.sample_batch(tasks, seed=8, l_max=16384,
+                                per_task=[max(1, 100 * len(per_step) * t.batch_size //
+                                              sum(x.batch_size for x in tasks)) for t in tasks])
+    cands = [(tp, 0, m) for tp, m in C5_CANDIDATES]
+    res = _lib.lobra_plan_deployment([c[0] for c in cands], [c[2] for c in cands],
+                                     cost_table(cands, 256, GRID_MAX), n_gpus, sample.seq_lens,
+                                     len(per_step), 256, GRID_MAX, 16)
+    groups = [(tp, int(p), m) for (tp, m), p in zip(C5_CANDIDATES, res["replicas"]) if p > 0]
+    if sum(tp * p for tp, p, _ in groups) != n_gpus:
+        raise SystemExit(f"planner deployment {groups} does not use all {n_gpus} GPUs")
+    return groups
+
+
+def plan_only():
+    """CPU: print the deployment and the step-0 dispatch status / solve time per N."""
+    from paper_2509_01193_b200 import _lib
+    per_tok, src = tp_costs()
+    for n in (1, 2, 4, 8):
+        groups = deployment_for(n)
+        wl = c5_batch(n, 0) if n > 1 else None
+        line = {"n_gpus": n, "deployment": "+".join(f"{p}xTP{tp}(M={m})" for tp, p, m in groups),
+                "us_per_token": per_tok, "cost_source": src}
+        if wl is not None:
+            t0 = time.perf_counter()
+            d = _lib.lobra_dispatch([g[0] for g in groups], [g[1] for g in groups], [g[2] for g in groups],
+                                    cost_table(groups, 256, GRID_MAX), wl.seq_lens, wl.seq_task, 256, GRID_MAX,
+                                    16, 0, chunking=1)
+            line.update({"status": d["status"], "t_hat": d["t_hat"], "solve_ms": 1000 * (time.perf_counter() - t0),
+                         "num_seqs": int(len(wl.seq_lens)), "tokens": int(wl.seq_lens.sum()),
+                         "nodes": d["nodes"]})
+        print(json.dumps(line), flush=True)
 
 
 def replica_ranks(groups):
@@ -239,13 +292,15 @@ def oracle_tokens_per_s(wl, shapes, budget_tokens=2048, seed=7):
 
 def run_reference(args):
     """--impl reference: the oracle (as it stands) on the host cores, bounded samples of
-    the same workload; rank 0 only."""
+    the same workload as the lobra arm (C3 at N = 1, C5 at N > 1); rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2509_01193_b200.layer import LLAMA2_7B
     from workloads import synth
-    wl = synth.config_c2()
+    workload = args.workload or ("c3" if args.gpus == 1 else "c5")
+    wl = {"c2": lambda: synth.config_c2(), "c3": lambda: synth.config_c3(),
+          "c5": lambda: c5_batch(args.gpus, 0)}[workload]()
     budget = 2048
     times, toks = [], 0
     for i in range(args.warmup + args.steps):
@@ -259,12 +314,26 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * tot / len(times), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: Llama-2-7B 7 projections, 4 tasks r=16 s=2, lengths<=4K",
-                       "global_batch_tokens": toks, "parallelism": "host"},
+            "config": {"workload": WORKLOAD_NAMES[workload], "global_batch_tokens": toks, "parallelism": "host"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-                             "sample": f"first {toks} tokens of the C2 batch, 7 projections fwd+bwd, fp64 NumPy"},
+                             "sample": f"first {toks} tokens of the {workload.upper()} batch, 7 projections "
+                                       "fwd+bwd, fp64 NumPy"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def c2_side(args):
+    """N = 1: the C2 configuration (BASELINE configs[1]) measured beside the C3 headline, in
+    a fresh process (same timing rules, no e2e / oracle legs)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c2", "--steps", str(args.steps),
+           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu", "--no-c2"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        return {k: d[k] for k in ("value", "unit", "ms_per_step", "algorithmic_tflops", "frac_of_bf16_peak",
+                                  "roofline", "clocks", "gpu_launches")} | {"workload": d["config"]["workload"]}
+    except Exception as e:   # reported, never fatal for the headline line
+        return {"error": str(e)[:200]}
 
 
 # ------------------------------------------------------------------------------ main leg
@@ -277,12 +346,20 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no e2e/cpu (for ncu)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3"],
-                    help="c2 (default, BASELINE configs[1]: the metric's workload) or c3 (configs[2]: "
-                         "16 tasks, ranks 8-64, lengths <= 16K, T = 65536; N = 1 only)")
+    ap.add_argument("--workload", default="", choices=["", "c2", "c3", "c5"],
+                    help="default: c3 at N = 1 (BASELINE configs[2], the largest single-GPU config), c5 at "
+                         "N > 1 (weak scaling over heterogeneous replicas); c2 = configs[1] (N = 1)")
+    ap.add_argument("--no-c2", action="store_true", help="N = 1: skip the C2 side measurement")
+    ap.add_argument("--plan-only", action="store_true", help="CPU: print the N = 1/2/4/8 plans and exit")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="do not record per-kernel CUDA events inside the timed region")
     args = ap.parse_args()
+    lobra_env = {k: v for k, v in sorted(os.environ.items()) if k.startswith("LOBRA_")}
+    dbg = [k for k in lobra_env if k.startswith("LOBRA_DBG_") or k == "LOBRA_META_CACHE"]
+    if dbg:   # work-skipping probes (compiled only with -DLOBRA_PROBES): never a bench number
+        raise SystemExit(f"bench.py refuses to run with probe variables set: {', '.join(dbg)}")
+    if args.plan_only:
+        return plan_only()
     if args.impl == "reference":
         return run_reference(args)
 
@@ -311,12 +388,15 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     _lib.load()
 
-    c3 = args.workload == "c3"
-    if c3 and n_gpus > 1:
-        raise SystemExit("--workload c3 is a single-GPU configuration")
-    groups = deployment_for(n_gpus) if not gloo_test else [(1, n_gpus, 16384)]
-    if c3:
-        groups = [(1, 1, 65536)]
+    workload = args.workload or ("c3" if n_gpus == 1 else "c5")
+    if workload in ("c2", "c3") and n_gpus > 1:
+        raise SystemExit(f"--workload {workload} is a single-GPU configuration (use c5 for N > 1)")
+    if workload == "c5" and gloo_test:
+        groups = [(1, n_gpus, C5_TOKENS_PER_GPU)]
+    elif workload == "c5":
+        groups = deployment_for(n_gpus)
+    else:
+        groups = [(1, 1, C5_TOKENS_PER_GPU if workload == "c3" else 16384)]
     reps = replica_ranks(groups)
     my_rep = next(i for i, rr in enumerate(reps) if rank in rr)
     my_group = 0
@@ -366,7 +446,7 @@ def main():
             symm.destroy()
             symm = None
 
-    tasks = synth.c3_tasks() if c3 else synth.c2_tasks()
+    tasks = synth.c2_tasks() if workload == "c2" else synth.c3_tasks()
     ranks = [t.rank for t in tasks]
     scales = [t.scale for t in tasks]
     layer = LoraLayer(LLAMA2_7B, ranks, scales, dev, torch.bfloat16, tp_size, tp_rank, comm, seed=1234,
@@ -377,23 +457,26 @@ def main():
     tp_list = [g[0] for g in groups]
     rep_list = [g[1] for g in groups]
     m_list = [g[2] for g in groups]
-    grid_step, grid_max = 256, max(m_list)
+    grid_step, grid_max = 256, GRID_MAX if workload != "c2" else 4096
     costs = cost_table(groups, grid_step, grid_max)
 
     def make_batch(step: int):
-        """Global batch of the step: N x 16384 tokens of the C2 task mix (seeded)."""
-        if c3:
+        """Global batch of the step (seeded): C3 / C2 at N = 1, N x 65536 tokens of the C3
+        task mix at N > 1 (C5)."""
+        if workload == "c3":
             return synth.config_c3(seed=3 + step)
-        if n_gpus == 1:
+        if workload == "c2":
             return synth.config_c2(seed=2 + step)
-        return synth.pack_tokens(tasks, T_PER_GPU * n_gpus, 4096, seed=1000 + step, name="C2xN")
+        return c5_batch(n_gpus, step)
 
     n_batches = 4
     batches = [make_batch(i) for i in range(n_batches)]
 
     def plan(wl):
+        # raises on LOBRA_ERR_BUDGET: a bench step never runs a non-Eq.-3 dispatch
         d = _lib.lobra_dispatch(tp_list, rep_list, m_list, costs, wl.seq_lens, wl.seq_task,
                                 grid_step, grid_max, 16, 0, chunking=1)
+        assert d["status"] == 0
         mine = np.nonzero(d["seq_replica"] == my_rep)[0]
         chunks = []
         for c in sorted(set(d["seq_chunk"][mine].tolist())):
@@ -418,6 +501,8 @@ def main():
 
     plans = [plan(b) for b in batches]
     stream = torch.cuda.current_stream()
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -444,12 +529,19 @@ def main():
         disp_ms = []
         barrier()
         e0.record(stream)
-        for i in range(args.steps):
-            # a7: the dispatch of this step runs on the host while the GPU works on the
-            # previously enqueued step ("fully overlapped")
+        # a7: every step's dispatch is computed on the host one step ahead, in a worker thread
+        # (the C++ call releases the GIL), while the GPU works on the enqueued step (P:586
+        # "fast and can be fully overlapped by the training of previous step(s)")
+        def timed_plan(b):
             t0 = time.perf_counter()
-            chunks, tok, _ = plan(batches[(args.warmup + i) % n_batches])
-            disp_ms.append(1000 * (time.perf_counter() - t0))
+            r = plan(b)
+            return r, 1000 * (time.perf_counter() - t0)
+        fut = pool.submit(timed_plan, batches[args.warmup % n_batches])
+        for i in range(args.steps):
+            (chunks, tok, _), dms = fut.result()
+            disp_ms.append(dms)
+            if i + 1 < args.steps:
+                fut = pool.submit(timed_plan, batches[(args.warmup + i + 1) % n_batches])
             run_step(chunks)
             tokens += tok
             tokens_local += sum(int(c[0].sum()) for c in chunks)
@@ -649,7 +741,7 @@ def main():
     if rank == 0 and n_gpus == 1 and not args.no_cpu and not args.profile_only:
         tps, dt, n, threads = oracle_tokens_per_s(batches[0], LLAMA2_7B, budget_tokens=8192)
         cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-               "sample": f"first {n} tokens of the {args.workload.upper()} batch, 7 projections fwd+bwd, "
+               "sample": f"first {n} tokens of the {workload.upper()} batch, 7 projections fwd+bwd, "
                          f"fp64 NumPy ({dt:.1f} s)"}
 
     if rank == 0:
@@ -658,12 +750,11 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded; lengths lognormal-fitted to the paper's dataset table)",
-                "config": {"workload": ("C3: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
-                                        "16 tasks ranks 8/16/32/64 s 0.5-4, lengths<=16384 packed") if c3 else
-                                       ("C2: Llama-2-7B layer, 7 LoRA projections (q,k,v,o,gate,up,down), "
-                                        "4 tasks r=16 s=2, lengths<=4096 packed"),
-                           "global_batch_tokens": int(tokens / args.steps), "seq_len_max": 16384 if c3 else 4096,
+                "config": {"workload": WORKLOAD_NAMES[workload],
+                           "global_batch_tokens": int(tokens / args.steps), "seq_len_max": grid_max,
                            "parallelism": par, "l2": "inputs > L2 (each projection input >= 128 MiB)",
+                           "dispatch": "Eq. 3 exact (lobra_dispatch mode 0), packed chunks <= M_i tokens",
+                           "cost_table": tp_costs()[1],
                            "tp_collective": tp_coll},
                 "per_gpu": value / n_gpus,
                 "algorithmic_tflops": step_tflops,
@@ -672,7 +763,9 @@ def main():
                 "nominal_2250": step_tflops / 2250.0},
                 "clocks": clocks, **({"remeasured_after": remeasured} if remeasured else {}), "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
                 "kernels": kern, "dispatch_ms_median": statistics.median(disp_ms) if disp_ms else None,
-                "cpu_baseline": cpu}
+                "cpu_baseline": cpu, "lobra_env": lobra_env}
+        if workload == "c3" and n_gpus == 1 and not args.no_c2 and not args.profile_only:
+            line["c2"] = c2_side(args)
         print(json.dumps(line), flush=True)
     if comm is not None:
         torch.cuda.synchronize()

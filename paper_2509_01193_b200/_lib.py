@@ -93,7 +93,7 @@ class PlanOut(C.Structure):
 
 class AdamHP(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("weight_decay", C.c_float)]
+                ("weight_decay", C.c_float), ("step", C.c_int64)]
 
 
 class Profile(C.Structure):
@@ -387,9 +387,11 @@ def lobra_lora_bwd(X, W, A, B, ranks, scales, seq_lens, seq_task, Hs, dY, dX, dA
 
 
 def lobra_dispatch(tp, replicas, max_tokens, cost, seq_lens, seq_task, grid_step=256,
-                   grid_max=16384, R=16, mode=0, node_cap=0, chunking=0):
+                   grid_max=16384, R=16, mode=0, node_cap=0, chunking=0, allow_budget=False):
     """Per-step dispatch (host).  Returns a dict of numpy arrays; raises LobraError on
-    input / infeasibility errors.  status LOBRA_ERR_BUDGET is returned in the dict."""
+    input / infeasibility errors and, unless ``allow_budget``, when the exact Eq. 3 solver
+    exhausted its node budget (LOBRA_ERR_BUDGET: the returned d would be the length-based
+    one, not the Eq. 3 optimum)."""
     tp, replicas, max_tokens = _i32(tp), _i32(replicas), _i32(max_tokens)
     cost = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
     G = len(tp)
@@ -408,7 +410,7 @@ def lobra_dispatch(tp, replicas, max_tokens, cost, seq_lens, seq_task, grid_step
                     out["replica_cost"].ctypes.data_as(_i64p), 0, 0)
     st = load().lobra_dispatch(C.byref(dep), C.byref(batch), grid_step, grid_max, R, mode,
                                chunking, node_cap, C.byref(o))
-    if st not in (LOBRA_OK, LOBRA_ERR_BUDGET):
+    if st != LOBRA_OK and not (st == LOBRA_ERR_BUDGET and allow_budget):
         raise LobraError(st, load().lobra_last_error().decode())
     nb = o.num_buckets
     out["status"] = st
@@ -478,9 +480,10 @@ def lobra_launch_count() -> int:
 def lobra_adamw_step(params, grads, m, v, hparams, step, group=None, params_bf16=None,
                      grad_scale=1.0, stream=None):
     """One multi-tenant AdamW step (include/lobra.h).  hparams: list of dicts with keys
-    lr, beta1, beta2, eps, weight_decay (one per group); group: uint8 tensor or None."""
+    lr, beta1, beta2, eps, weight_decay and optionally step (the group's own step count,
+    else `step`), one per group; group: uint8 tensor or None."""
     hp = (AdamHP * len(hparams))(*[AdamHP(h["lr"], h["beta1"], h["beta2"], h["eps"],
-                                          h["weight_decay"]) for h in hparams])
+                                          h["weight_decay"], int(h.get("step", 0))) for h in hparams])
     _check(load().lobra_adamw_step(_ptr(params), _ptr(params_bf16), _ptr(grads), _ptr(m), _ptr(v),
                                    _ptr(group), int(params.numel()), hp, len(hparams), int(step),
                                    float(grad_scale), _stream(stream)))
@@ -488,9 +491,10 @@ def lobra_adamw_step(params, grads, m, v, hparams, step, group=None, params_bf16
 
 # ---------------------------------------------------------------------------- planner
 def lobra_plan_deployment(tp, max_tokens, cost, n_gpus, lens, batch_size=0, grid_step=256,
-                          grid_max=16384, R=16, threshold=0.15, node_cap=0):
+                          grid_max=16384, R=16, threshold=0.15, node_cap=0, allow_budget=False):
     """Stage-1 deployment planning (include/lobra.h).  Returns a dict; raises LobraError
-    on input/infeasible errors (status LOBRA_ERR_BUDGET is reported in the dict)."""
+    on input/infeasible errors and, unless ``allow_budget``, when a per-plan Eq. 3 solve
+    exhausted its node budget (LOBRA_ERR_BUDGET)."""
     tp, max_tokens, lens = _i32(tp), _i32(max_tokens), _i32(lens)
     cost = np.ascontiguousarray(np.asarray(cost, dtype=np.int64))
     S = len(tp)
@@ -504,7 +508,7 @@ def lobra_plan_deployment(tp, max_tokens, cost, n_gpus, lens, batch_size=0, grid
     st = load().lobra_plan_deployment(C.byref(cand), n_gpus, lens.ctypes.data_as(_i32p), len(lens),
                                       batch_size, grid_step, grid_max, R, threshold, node_cap,
                                       C.byref(o))
-    if st not in (LOBRA_OK, LOBRA_ERR_BUDGET):
+    if st != LOBRA_OK and not (st == LOBRA_ERR_BUDGET and allow_budget):
         raise LobraError(st, load().lobra_last_error().decode())
     nb = o.num_buckets
     return {"status": st, "replicas": reps, "boundaries": bnd[:nb], "demands": dem[:nb],

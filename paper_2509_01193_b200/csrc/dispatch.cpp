@@ -22,6 +22,7 @@
 // force / MILP; tests check the two agree bit for bit.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -30,6 +31,7 @@
 #include <vector>
 
 #include "common.h"
+#include "eq3_bb.h"
 
 namespace {
 
@@ -222,86 +224,188 @@ std::vector<std::vector<i64>> by_length(const Inst& I, const std::vector<i64>& t
   return d;
 }
 
-// DFS over the leading groups (all but the last two) in lexicographic order.
-struct Multi {
+// Eq. 3 with G >= 3 deployed groups (reading Q12: the lexicographically smallest optimal
+// d in (group, bucket) order).
+//  1. t* = the smallest t for which the covering program of eq3_bb.cpp (q_ij rounds, loads
+//     <= t) is feasible, scanning up from the LP / Lagrangian lower bound;
+//  2. groups 0..G-3, bucket by bucket: the smallest d_ij that still admits a completion with
+//     max load <= t*.  "d_ij <= u feasible" is monotone in u, so each variable costs one
+//     proof that d_ij <= (incumbent value - 1) is infeasible, plus one search per improved
+//     incumbent.  d_ij <= u splits into q_ij <= floor(u / p_i) and (when p_i does not
+//     divide u) q_ij = ceil(u / p_i) covering exactly u;
+//  3. the last two groups: the exact 2-group DP's lexicographic reconstruction.
+// Every decision is exact (lobra::eq3::feasible either returns an integer certificate or proves
+// infeasibility); only an exhausted node budget leaves a decision open (LOBRA_ERR_BUDGET).
+struct MultiLex {
   const Inst& I;
-  Budget& bud;
-  i64 UB;
-  i64 best = BIG;
-  std::vector<std::vector<i64>> cur, sol;
-  bool want_lex = false;
-  i64 target = BIG;
-  bool done = false;
-  std::unique_ptr<Two> leaf;
-  Multi(const Inst& in, Budget& b, i64 ub) : I(in), bud(b), UB(ub) {
-    cur.assign(I.G, std::vector<i64>(I.R, 0));
+  lobra::eq3::Stats& st;
+  bool budget_hit = false;
+  MultiLex(const Inst& in, lobra::eq3::Stats& s) : I(in), st(s) {}
+
+  lobra::eq3::Cover cover(const std::vector<i64>& tau, const std::vector<i64>& D,
+                   const std::vector<std::vector<char>>& fixed) const {
+    lobra::eq3::Cover cv;
+    cv.G = I.G;
+    cv.R = I.R;
+    cv.p = I.p;
+    cv.c = I.c;
+    cv.tau = tau;
+    cv.D = D;
+    cv.qhi.assign(I.G, std::vector<i64>(I.R, 0));
+    for (int i = 0; i < I.G; ++i)
+      for (int j = 0; j < I.R; ++j)
+        if (I.sup(i, j) && !fixed[i][j] && D[j] > 0) cv.qhi[i][j] = cdiv(D[j], I.p[i]);
+    return cv;
   }
-  // Phase 1 (want_lex=false): minimise; phase 2: first lexicographic d meeting target.
-  void rec(int i, int j, std::vector<i64>& rem, std::vector<i64>& load) {
-    if (done || bud.hit) return;
-    const int G = I.G;
-    if (i == G - 2) {
-      // the leading groups never load groups G-2, G-1: La = Lb = 0; one cached 2-group DP
-      // over budgets 0..UB, updated incrementally from leaf to leaf
-      if (!leaf) {
-        leaf.reset(new Two(I, G - 2, G - 1, rem, 0, 0, UB, bud));
-      } else if (!leaf->update(rem, bud)) {
-        return;
-      }
-      if (!leaf->ok) return;
-      Two& two = *leaf;
-      if (!want_lex) {
-        const i64 t = std::max(two.best(), *std::max_element(load.begin(), load.end() - 2));
-        if (t < best) {
-          best = t;
+  // d from a covering certificate q of the residual (D, fixed): in every bucket the later
+  // groups take as much as their rounds allow, the earlier ones the rest (smallest
+  // incumbent values for the lexicographic scan).
+  void to_d(const lobra::eq3::Cover& cv, const std::vector<std::vector<i64>>& q,
+            std::vector<std::vector<i64>>& d) const {
+    for (int j = 0; j < I.R; ++j) {
+      i64 rem = cv.D[j];
+      for (int i = 0; i < I.G; ++i) {
+        if (cv.qhi[i][j] <= 0) {
+          if (!fixed_[i][j]) d[i][j] = 0;   // not fixed, no rounds allowed: takes nothing
+          continue;
         }
-      } else {
-        std::vector<i64> da;
-        const i64 lead = *std::max_element(load.begin(), load.end() - 2);
-        if (lead <= target && two.lexmin(target, da)) {
-          sol = cur;
-          for (int jj = 0; jj < I.R; ++jj) {
-            sol[G - 2][jj] = da[jj];
-            sol[G - 1][jj] = rem[jj] - da[jj];
+        i64 later = 0;
+        for (int k = i + 1; k < I.G; ++k)
+          if (cv.qhi[k][j] > 0) later += I.p[k] * q[k][j];
+        const i64 v = std::max<i64>(0, rem - later);
+        d[i][j] = v;
+        rem -= v;
+      }
+    }
+  }
+  std::vector<std::vector<char>> fixed_;   // variables of the lexicographic prefix
+  int feas(const lobra::eq3::Cover& cv, std::vector<std::vector<i64>>& q) {
+#ifdef EQ3_TRACE
+    const i64 n0 = st.nodes;
+#endif
+    const int r = lobra::eq3::feasible(cv, q, st);
+#ifdef EQ3_TRACE
+    i64 sd = 0;
+    for (auto v : cv.D) sd += v;
+    fprintf(stderr, "feas r=%d nodes=%lld sumD=%lld tau0=%lld\n", r, (long long)(st.nodes - n0), (long long)sd, (long long)cv.tau[0]);
+#endif
+    if (r < 0) budget_hit = true;
+    return r;
+  }
+
+  // t_only: stop after step 1 (dl = a certificate attaining t*, not the canonical d)
+  bool run(std::vector<std::vector<i64>>& dl, i64 UB, bool t_only = false) {
+    const int G = I.G, R = I.R;
+    fixed_.assign(G, std::vector<char>(R, 0));
+    std::vector<std::vector<char>>& fixed = fixed_;
+    std::vector<i64> tau(G, 0), D = I.Bj;
+    // 1. t*
+    i64 t;
+    {
+      lobra::eq3::Cover cv = cover(tau, D, fixed);
+      const double lb = lobra::eq3::lower_bound(cv, st);
+      t = (i64)std::ceil(lb - 1e-6);
+      if (!(lb > -1e300)) t = 0;
+    }
+    std::vector<std::vector<i64>> q, inc(G, std::vector<i64>(R, 0));
+    for (;; ++t) {
+      if (t >= UB) {   // the length-based dispatch attains UB
+        t = UB;
+        inc = dl;
+        break;
+      }
+      std::fill(tau.begin(), tau.end(), t);
+      lobra::eq3::Cover cv = cover(tau, D, fixed);
+      const int r = feas(cv, q);
+      if (r < 0) return false;
+      if (r == 1) {
+        to_d(cv, q, inc);
+        break;
+      }
+    }
+    std::fill(tau.begin(), tau.end(), t);
+    if (t_only) {
+      dl = inc;
+      return true;
+    }
+    // 2. groups 0..G-3
+    std::vector<std::vector<i64>> d(G, std::vector<i64>(R, 0));
+    for (int i = 0; i + 2 < G; ++i)
+      for (int j = 0; j < R; ++j) {
+        if (!I.sup(i, j) || D[j] == 0) {
+          fixed[i][j] = 1;
+          continue;
+        }
+        while (inc[i][j] > 0) {
+          const i64 u = inc[i][j] - 1;
+          bool improved = false;
+          // (A) q_ij <= floor(u / p_i)
+          {
+            lobra::eq3::Cover cv = cover(tau, D, fixed);
+            cv.qhi[i][j] = std::min(cv.qhi[i][j], u / I.p[i]);
+            const int r = feas(cv, q);
+            if (r < 0) return false;
+            if (r == 1) {
+              std::vector<std::vector<i64>> nd = inc;
+              to_d(cv, q, nd);
+              for (int jj = j; jj < R; ++jj) inc[i][jj] = nd[i][jj];
+              for (int ii = i + 1; ii < G; ++ii) inc[ii] = nd[ii];
+              improved = true;
+            }
           }
-          done = true;
+          // (B) q_ij = ceil(u / p_i) covering exactly u
+          if (!improved && u % I.p[i] != 0) {
+            std::vector<i64> tau2 = tau, D2 = D;
+            tau2[i] -= I.c[i][j] * cdiv(u, I.p[i]);
+            D2[j] -= u;
+            std::vector<std::vector<char>> fx = fixed;
+            fx[i][j] = 1;
+            lobra::eq3::Cover cv = cover(tau2, D2, fx);
+            const int r = feas(cv, q);
+            if (r < 0) return false;
+            if (r == 1) {
+              std::vector<std::vector<i64>> nd = inc;
+              to_d(cv, q, nd);
+              nd[i][j] = u;
+              for (int jj = j; jj < R; ++jj) inc[i][jj] = nd[i][jj];
+              for (int ii = i + 1; ii < G; ++ii) inc[ii] = nd[ii];
+              improved = true;
+            }
+          }
+          if (!improved) break;
+          if (inc[i][j] > u) {   // a certificate of d_ij <= u must lower the incumbent
+            lobra::set_error("internal: Eq. 3 incumbent did not improve");
+            return false;
+          }
         }
+        const i64 v = inc[i][j];
+        d[i][j] = v;
+        tau[i] -= I.cost(i, j, v);
+        D[j] -= v;
+        fixed[i][j] = 1;
       }
-      return;
+    // 3. the last two groups
+    Budget bud{(i64)4000000000LL};
+    Two two(I, G - 2, G - 1, D, 0, 0, t, bud);
+    std::vector<i64> da;
+    if (!two.ok || !two.lexmin(t, da)) {
+      // cannot happen: the incumbent restricted to the last two groups is a witness
+      lobra::set_error("internal: Eq. 3 lexicographic completion failed");
+      return false;
     }
-    if (j == I.R) {
-      rec(i + 1, 0, rem, load);
-      return;
+    for (int j = 0; j < R; ++j) {
+      d[G - 2][j] = da[j];
+      d[G - 1][j] = D[j] - da[j];
     }
-    const i64 lim = want_lex ? target : best - 1;
-    const i64 hi = I.sup(i, j) ? rem[j] : 0;
-    for (i64 d = 0; d <= hi; ++d) {
-      if (!bud.take(1)) return;
-      const i64 ci = I.cost(i, j, d);
-      if (load[i] + ci > lim) break;
-      // remaining must still be coverable by some later group
-      load[i] += ci;
-      rem[j] -= d;
-      cur[i][j] = d;
-      bool coverable = true;
-      if (rem[j] > 0) {
-        coverable = false;
-        for (int k = i + 1; k < G; ++k) coverable |= I.sup(k, j);
-      }
-      if (coverable) rec(i, j + 1, rem, load);
-      cur[i][j] = 0;
-      rem[j] += d;
-      load[i] -= ci;
-      if (done || bud.hit) return;
-    }
+    dl = d;
+    return true;
   }
 };
 
 // Exact Eq. 3 over the deployed groups of L: the lexicographically smallest optimal d
-// (reading Q12).  false = node budget hit (dl then holds the best incumbent found, or
-// the length-based solution).
-bool eq3_exact(const Inst& L, const std::vector<i64>& tp, Budget& bud,
-               std::vector<std::vector<i64>>& dl) {
+// (reading Q12).  false = solver budget exhausted (dl then holds the length-based d).
+bool eq3_exact(const Inst& L, const std::vector<i64>& tp, Budget& bud, i64 node_cap, i64& nodes,
+               std::vector<std::vector<i64>>& dl, bool t_only = false) {
   dl = by_length(L, tp);
   if (L.G == 1) {
     dl[0] = L.Bj;
@@ -316,19 +420,18 @@ bool eq3_exact(const Inst& L, const std::vector<i64>& tp, Budget& bud,
       if (two.lexmin(t, da))
         for (int j = 0; j < L.R; ++j) dl[0][j] = da[j], dl[1][j] = L.Bj[j] - da[j];
     }
-  } else {
-    Multi m(L, bud, UB);
-    std::vector<i64> rem = L.Bj, load(L.G, 0);
-    m.best = UB + 1;
-    m.rec(0, 0, rem, load);
-    if (!bud.hit && m.best <= UB) {
-      m.want_lex = true;
-      m.target = m.best;
-      m.rec(0, 0, rem, load);
-      if (m.done) dl = m.sol;
-    }
+    nodes = bud.used;
+    return !bud.hit;
   }
-  return !bud.hit;
+  lobra::eq3::Stats st;
+  st.cap = node_cap > 0 ? node_cap : (i64)1000000;
+  MultiLex ml(L, st);
+  std::vector<std::vector<i64>> d = dl;
+  const bool ok = ml.run(d, UB, t_only);
+  nodes = st.nodes;
+  if (ok) dl = d;
+  else dl = by_length(L, tp);
+  return ok;
 }
 
 }  // namespace
@@ -425,7 +528,8 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   L.Bj = Bj;
   std::vector<i64> ltp;
   for (int i : live) L.p.push_back(p[i]), L.r.push_back(I.r[i]), L.c.push_back(I.c[i]), ltp.push_back(tp[i]);
-  Budget bud{node_cap > 0 ? node_cap : (i64)400000000};
+  Budget bud{(i64)4000000000LL};   // 2-group DP cells
+  i64 nodes = 0;
   std::vector<std::vector<i64>> dl = by_length(L, ltp);
   lobra_status st = LOBRA_OK;
   if (mode == 2 && L.G != 1)
@@ -433,7 +537,7 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   if (mode == 2) {
     for (int j = 0; j < Rb; ++j) dl[0][j] = Bj[j];
   }
-  if (mode == 0 && !eq3_exact(L, ltp, bud, dl)) st = LOBRA_ERR_BUDGET;
+  if (mode == 0 && !eq3_exact(L, ltp, bud, node_cap, nodes, dl)) st = LOBRA_ERR_BUDGET;
   // write d (all groups; undeployed rows are 0)
   std::vector<std::vector<i64>> d(G, std::vector<i64>(Rb, 0));
   for (size_t k = 0; k < live.size(); ++k) d[live[k]] = dl[k];
@@ -562,7 +666,7 @@ extern "C" lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_
   }
   for (i64 q = 0; q < total_rep; ++q) out->replica_cost[q] = running[q];
   out->t_hat = t_hat;
-  out->nodes = bud.used;
+  out->nodes = nodes;
   if (st == LOBRA_ERR_BUDGET) lobra::set_error("Eq. 3 solver node cap hit; incumbent returned");
   return st;
 }
@@ -699,7 +803,6 @@ extern "C" lobra_status lobra_plan_deployment(const lobra_candidates* cand, int3
   double min_lb = lbs[0].lb;
   for (auto& e : lbs) min_lb = std::min(min_lb, e.lb);
   // 6. exact Eq. 3 per kept plan
-  Budget bud{node_cap > 0 ? node_cap : (i64)400000000};
   bool hit = false;
   int solved = 0;
   i64 best_t = BIG;
@@ -715,13 +818,47 @@ extern "C" lobra_status lobra_plan_deployment(const lobra_candidates* cand, int3
     if (a != b) return a < b;
     return plans[k] < plans[best];
   };
+  // kept plans in ascending Theorem-1 bound (good incumbents first); a plan whose exact Eq. 3
+  // lower bound (LP / Lagrangian, eq3_bb.cpp) already exceeds the best t found is skipped:
+  // it can be neither the best nor tied with it, so the selection stays exact
+  // (plans with <= 2 groups first: their exact solve is a cheap DP)
+  auto ngroups = [&](int k) {
+    int g = 0;
+    for (int i = 0; i < S; ++i) g += plans[k][i] > 0;
+    return g;
+  };
+  std::stable_sort(lbs.begin(), lbs.end(), [&](const Cand& a, const Cand& b) {
+    const bool ha = ngroups(a.idx) >= 3, hb = ngroups(b.idx) >= 3;
+    return ha != hb ? hb : a.lb < b.lb;
+  });
   for (auto& e : lbs) {
     if (threshold >= 0 && e.lb > (1.0 + threshold) * min_lb + 1e-9) continue;
     std::vector<i64> tpl;
     Inst L = make_inst(plans[e.idx], tpl);
+    if (best >= 0 && L.G >= 3) {
+      lobra::eq3::Cover cv;
+      cv.G = L.G;
+      cv.R = L.R;
+      cv.p = L.p;
+      cv.c = L.c;
+      cv.tau.assign(L.G, 0);
+      cv.D = L.Bj;
+      cv.qhi.assign(L.G, std::vector<i64>(L.R, 0));
+      for (int g = 0; g < L.G; ++g)
+        for (int j = 0; j < L.R; ++j)
+          if (L.sup(g, j) && L.Bj[j] > 0) cv.qhi[g][j] = cdiv(L.Bj[j], L.p[g]);
+      lobra::eq3::Stats s0;
+      s0.cap = INT64_MAX;
+      const double lbz = lobra::eq3::lower_bound(cv, s0);
+      if (lbz > -1e300 && (i64)std::ceil(lbz - 1e-6) > best_t) {
+        ++solved;   // decided exactly: proven worse than the incumbent plan
+        continue;
+      }
+    }
     std::vector<std::vector<i64>> d;
-    Budget b1{bud.cap};
-    if (!eq3_exact(L, tpl, b1, d)) hit = true;
+    Budget b1{(i64)4000000000LL};
+    i64 nodes = 0;
+    if (!eq3_exact(L, tpl, b1, node_cap, nodes, d, /*t_only=*/true)) hit = true;
     ++solved;
     const i64 t = objective(L, d);
     if (better(t, e.idx)) best_t = t, best = e.idx;

@@ -1763,10 +1763,13 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   RowArgs a;
   a.K = K;
   {
+    a.dbg_no_mma = 0;
+#ifdef LOBRA_PROBES   // work-skipping probes: never compiled into the product library
     const char* e = getenv("LOBRA_DBG_RP_NOMMA");
     a.dbg_no_mma = (e && e[0] == '1') ? 1 : 0;
     // LOBRA_DBG_RP: probe bit mask (1 no MMA, 2 no adapter boxes, 4 no output / reduction)
     if (const char* d = getenv("LOBRA_DBG_RP")) a.dbg_no_mma = atoi(d);
+#endif
     const char* f = getenv("LOBRA_RP_PREFETCH");
     a.prefetch = f ? atoi(f) : 0;
     const char* g = getenv("LOBRA_RP_INTERLEAVE");
@@ -1832,9 +1835,12 @@ void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, cons
     static unsigned long long* ts = nullptr;
     static int dbg = -1;
     if (dbg < 0) {
+      dbg = 0;
+#ifdef LOBRA_PROBES
       const char* e = getenv("LOBRA_DBG_SHRINK_TS");
       dbg = (e && e[0] == '1') ? 1 : 0;
       if (dbg) cudaMalloc(&ts, 8 * 1024 * sizeof(unsigned long long));
+#endif
     }
     a.ts = ts;
   }
@@ -1957,10 +1963,13 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
   {
     static int dbg = -1;
     if (dbg < 0) {
+      dbg = 0;
+#ifdef LOBRA_PROBES
       const char* e = getenv("LOBRA_DBG_DY_ONLY");
       dbg = (e && e[0] == '1') ? 1 : 0;
       // LOBRA_DBG_DY: probe bit mask (1 dY only, 2 no dB MMAs, 4 no G MMAs)
       if (const char* f = getenv("LOBRA_DBG_DY")) dbg = atoi(f);
+#endif
     }
     a.dbg_dy_only = dbg;
   }

@@ -194,15 +194,20 @@ lobra_status upload(DevCtx* c, const void* src, size_t bytes, void* dst, cudaStr
   return LOBRA_OK;
 }
 
-// Metadata upload with an optional cache (LOBRA_META_CACHE=1, experiment): skip the H2D
-// copy when this device address already holds byte-identical metadata.
+// Metadata upload with an optional cache (LOBRA_META_CACHE=1, probe builds only): skip the
+// H2D copy when this device address already holds byte-identical metadata.  Not in the
+// product library: the cache keys on the address, so a reused workspace could go stale.
 bool meta_cache_on() {
+#ifdef LOBRA_PROBES
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("LOBRA_META_CACHE");
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
+#else
+  return false;
+#endif
 }
 std::mutex g_meta_mu;
 std::vector<std::pair<const void*, uint64_t>> g_meta_cache;

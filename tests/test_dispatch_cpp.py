@@ -129,6 +129,83 @@ def test_c5_scale_runs_fast():
     assert (got["seq_replica"][long] >= 4).all()
 
 
+# --------------------------------------------------------------------------- C5 scale, G = 2..4
+_C5 = os.path.join(os.path.dirname(__file__), "golden", "dispatch_c5.json")
+C5 = json.load(open(_C5)) if os.path.exists(_C5) else {"cases": []}
+
+
+def _c5_cost(groups, unit):
+    out = []
+    for g in groups:
+        eff = g.tp * (0.85 ** np.log2(g.tp))
+        out.append([max(1, int(round(((k + 1) * 256 + ((k + 1) * 256) ** 2 / 16384) / eff / unit)))
+                    for k in range(64)])
+    return out
+
+
+def _digest(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(np.asarray(a, dtype=np.int64)).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("case", C5["cases"], ids=lambda c: f"{c['name']}-s{c['seed']}")
+def test_c5_scale_exact_vs_oracle_fixture(case):
+    """C5-scale steps (B ~ 1952 sequences of C3's 16 tasks, R = 16) on 2-4 deployed groups
+    (TP1/TP2/TP4/TP8): the C++ Eq. 3 solver returns exactly the oracle's optimum and
+    canonical (lexicographically smallest) d, and the same per-sequence outputs
+    (tests/golden/dispatch_c5.json, written by tools/gen_dispatch_golden.py from the
+    oracle alone)."""
+    import time
+    from paper_2509_01193_b200 import _lib
+    groups = [D.Group(*g) for g in case["deployment"]]
+    cost = _c5_cost(groups, C5["cost_unit"])
+    tasks = synth.c3_tasks()
+    wl = synth.sample_batch(tasks, seed=case["seed"], l_max=16384,
+                            per_task=[t.batch_size for t in tasks[:12]] + [64] * 4)
+    assert len(wl.seq_lens) == case["num_seqs"]
+    t0 = time.perf_counter()
+    got = _lib.lobra_dispatch([g.tp for g in groups], [g.replicas for g in groups],
+                              [g.max_tokens for g in groups], cost, wl.seq_lens, wl.seq_task,
+                              C5["grid_step"], C5["grid_max"], C5["R"], 0, chunking=C5["chunking"])
+    dt = time.perf_counter() - t0
+    assert got["status"] == 0
+    assert got["boundaries"].tolist() == case["boundaries"]
+    assert got["t_hat"] == case["t_hat"]
+    assert got["d"].tolist() == case["d"]
+    assert _digest(got["seq_bucket"], got["seq_replica"], got["seq_chunk"], got["pack_order"],
+                   got["replica_cost"]) == case["sha256"]
+    assert dt < 10.0, dt   # measured solve times: profiles/r2_dispatch_solve_times.md
+
+
+def test_c5_scale_live_oracle_g3():
+    """One C5-scale 3-group step against the live oracle (not the fixture)."""
+    tasks = synth.c3_tasks()
+    wl = synth.sample_batch(tasks, seed=107, l_max=16384,
+                            per_task=[t.batch_size for t in tasks[:12]] + [64] * 4)
+    groups = [D.Group(1, 2, 8192), D.Group(2, 1, 16384), D.Group(4, 1, 16384)]
+    _run_both(groups, _c5_cost(groups, 32), wl.seq_lens, wl.seq_task, 256, 16384, 16, chunking=1)
+
+
+def test_budget_exhaustion_is_loud():
+    """A node budget too small for Eq. 3 raises (LOBRA_ERR_BUDGET) instead of silently
+    returning the length-based d; allow_budget=True returns it with the status."""
+    from paper_2509_01193_b200 import _lib
+    tasks = synth.c3_tasks()
+    wl = synth.sample_batch(tasks, seed=100, l_max=16384,
+                            per_task=[t.batch_size for t in tasks[:12]] + [64] * 4)
+    groups = [D.Group(1, 2, 8192), D.Group(2, 1, 16384), D.Group(4, 1, 16384)]
+    args = ([1, 2, 4], [2, 1, 1], [8192, 16384, 16384], _c5_cost(groups, 32), wl.seq_lens, wl.seq_task,
+            256, 16384, 16, 0)
+    with pytest.raises(_lib.LobraError) as e:
+        _lib.lobra_dispatch(*args, node_cap=5)
+    assert e.value.status == _lib.LOBRA_ERR_BUDGET
+    got = _lib.lobra_dispatch(*args, node_cap=5, allow_budget=True)
+    assert got["status"] == _lib.LOBRA_ERR_BUDGET
+
+
 def test_uniform_mode_cpp():
     rng = np.random.default_rng(9)
     lens = rng.integers(1, 4096, size=37)

@@ -177,3 +177,82 @@ def test_packed_chunking_respects_token_budget():
         for c in set(res.seq_chunk[res.seq_replica == rep].tolist()):
             m = (res.seq_replica == rep) & (res.seq_chunk == c)
             assert lens[m].sum() <= 2048
+
+
+# --------------------------------------------------------------------------- mode 1 pin
+T3 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_thruputs.json")))
+
+
+def _table3_pp1_deployment():
+    """The four PP = 1 configurations of Table tb:parallel_config_thruputs,
+    one replica each, M = the longest length the table gives a throughput for, and the
+    per-sequence cost = time of one sequence on one replica = s / (thruput * n) (tokens /
+    (tokens per GPU per second * GPUs)), in integer units of 1e-6 s / 1e3."""
+    rows = {tuple(c): T3["thruput"][k] for k, c in enumerate(T3["configs"])}
+    lens = T3["seq_lens"]
+    groups, cost = [], []
+    for tp in (1, 2, 4, 8):
+        th = rows[(tp, 1)]
+        m = max(s for s, v in zip(lens, th) if v > 0)
+        groups.append(D.Group(tp, 1, m))
+        row = []
+        for k in range(8):                      # grid 2048 .. 16384
+            s = 2048 * (k + 1)
+            v = dict(zip(lens, th)).get(s, 0) or min(x for x in th if x > 0)
+            row.append(int(round(1e6 * s / (v * tp))))
+        cost.append(row)
+    return groups, cost
+
+
+def test_length_based_mode_sends_each_bucket_to_the_most_efficient_config():
+    """Fig. 4(c): length-based dispatch sends every bucket to 'the most
+    suitable replica(s)' so that 'from the perspective of each sequence, it can be processed
+    by the most efficient configuration' -- the highest tokens per GPU per second of Table
+    tb:parallel_config_thruputs.  Hand-read from the table: 2K -> TP1 (5.11 > 4.30 > 3.63 >
+    2.79), 4K -> TP2 (4.12 > 3.50 > 2.71), 8K -> TP4 (3.25 > 2.56), 16K -> TP8 (2.33, the only
+    one).  A rule that minimised the per-replica time c_ij alone (ignoring the n_i GPUs it
+    occupies) would send every bucket to TP8 instead."""
+    groups, cost = _table3_pp1_deployment()
+    lens = [2048] * 5 + [4096] * 3 + [8192] * 2 + [16384]
+    res = D.dispatch(groups, cost, lens, [0] * len(lens), 2048, 16384, 4, mode=1)
+    assert res.boundaries == [2048, 4096, 8192, 16384]
+    assert res.d.tolist() == [[5, 0, 0, 0], [0, 3, 0, 0], [0, 0, 2, 0], [0, 0, 0, 1]]
+    # the per-replica-time rule differs on this instance (the pin has teeth)
+    by_c = [min(range(4), key=lambda i: (cost[i][b // 2048 - 1] if b <= groups[i].max_tokens else 1e18, i))
+            for b in res.boundaries]
+    assert by_c == [3, 3, 3, 3]
+
+
+def test_length_based_mode_cpp_matches_hand_reading():
+    from paper_2509_01193_b200 import _lib
+    groups, cost = _table3_pp1_deployment()
+    lens = [2048] * 5 + [4096] * 3 + [8192] * 2 + [16384]
+    got = _lib.lobra_dispatch([g.tp for g in groups], [1] * 4, [g.max_tokens for g in groups], cost, lens,
+                              [0] * len(lens), 2048, 16384, 4, mode=1)
+    assert got["d"].tolist() == [[5, 0, 0, 0], [0, 3, 0, 0], [0, 0, 2, 0], [0, 0, 0, 1]]
+
+
+# --------------------------------------------------------------------------- steps 9-10 pins
+def test_chunks_and_packing_order_hand_worked():
+    """Steps 9-10 of the oracle by hand, one replica (M = 1024, grid 256, R = 2).
+    Lengths (index: len, task): 0:200 t2, 1:900 t0, 2:250 t1, 3:100 t0, 4:700 t1, 5:60 t2.
+    Grid values 256 (0, 2, 3, 5) and 1024 (1, 4) -> buckets [256, 1024].
+    chunking = 0 (App. D, b_j = floor(M / s_j)): bucket 1024 -> b = 1 -> chunks {1}, {4};
+      bucket 256 -> b = 4 -> chunk {0, 2, 3, 5}; descending cost c_j * count with cost 1 per
+      256 tokens: {0,2,3,5} costs 4, {1} and {4} cost 4 each -> ties by bucket index: the
+      256-bucket chunk first, then {1}, {4}.  Inside a chunk: (task, index) -> 3, 2, 0, 5.
+    chunking = 1 (packed next-fit over (bucket desc, index asc) = 1, 4, 0, 2, 3, 5 with at
+      most M real tokens): {1} (900; +700 overflows), {4, 0} (900; +250 overflows),
+      {2, 3, 5} (410).  Chunks in creation order; packing inside by (task, index): {1};
+      {4 (t1), 0 (t2)}; {3 (t0), 2 (t1), 5 (t2)}."""
+    groups = [D.Group(1, 1, 1024)]
+    lens = [200, 900, 250, 100, 700, 60]
+    tasks = [2, 0, 1, 0, 1, 2]
+    cost = [[1, 2, 3, 4]]
+    r0 = D.dispatch(groups, cost, lens, tasks, 256, 1024, 2, chunking=0)
+    assert r0.boundaries == [256, 1024]
+    assert r0.seq_chunk.tolist() == [0, 1, 0, 0, 2, 0]
+    assert r0.pack_order.tolist() == [2, 0, 1, 0, 0, 3]
+    r1 = D.dispatch(groups, cost, lens, tasks, 256, 1024, 2, chunking=1)
+    assert r1.seq_chunk.tolist() == [1, 0, 2, 2, 1, 2]
+    assert r1.pack_order.tolist() == [1, 0, 1, 0, 0, 2]
