@@ -19,6 +19,13 @@
    for B-D chosen by enumerating all TP{1,2,4} mixes of 8 GPUs (a small stage-1 search).
 GPU-seconds per step = N x max over replicas of the sum of its chunk times.
 
+--padding: the paper's own setting ("we assume padding"): micro-batches of App. D
+(chunking = 0: b_j = floor(M_i / s_j) sequences of bucket j, every sequence padded to s_j),
+each chunk executed and charged at its PADDED tokens, and Eq. 3's per-sequence cost made
+consistent with that execution: c_ij = t_i(s_j) + a0 / b_j (the per-chunk constant
+amortised over a full micro-batch, App. D t(b, s) = a0 + b t(s)).  --r-sweep adds the
+R-sensitivity study of P:1155-1161 (R = 4..32: padding tokens and step time of D).
+
 --layer-cost profiles/r1_layer_cost.json (tools/bench_layer.py --fit) replaces step 1 by the
 full decoder layer's measured App. D cost t = c0 + c1 sum(s) + c2 sum(s^2) per chunk
 (attention's s^2 term real); TP-k replicas divide the token-dependent part
@@ -75,6 +82,7 @@ def measure_layer(Ts=(1024, 2048, 4096, 8192, 16384), reps=5):
 
 
 QUAD = {"c2": 0.0}   # s^2 coefficient (seconds per token x length) when --layer-cost is given
+PAD = {"on": False}  # --padding
 
 
 def t_rep(k, T, a0, a1, S2=0.0):
@@ -85,8 +93,17 @@ def t_rep(k, T, a0, a1, S2=0.0):
 
 def cost_table(groups, a0, a1, grid_step, grid_max, unit=1e-5):
     U = grid_max // grid_step
-    return [[max(1, int(round(t_rep(tp, (u + 1) * grid_step, 0.0, a1, float((u + 1) * grid_step) ** 2) / unit)))
-             for u in range(U)] for tp, _, _ in groups]
+    out = []
+    for tp, _, M in groups:
+        row = []
+        for u in range(U):
+            sj = (u + 1) * grid_step
+            c = t_rep(tp, sj, 0.0, a1, float(sj) ** 2)
+            if PAD["on"]:
+                c += a0 / max(1, M // sj)      # per-chunk constant over a full micro-batch
+            row.append(max(1, int(round(c / unit))))
+        out.append(row)
+    return out
 
 
 def step_time(groups, wl, mode, grid_step, R, a0, a1):
@@ -95,18 +112,23 @@ def step_time(groups, wl, mode, grid_step, R, a0, a1):
     M = [g[2] for g in groups]
     gmax = 16384
     d = _lib.lobra_dispatch(tp, reps, M, cost_table(groups, a0, a1, grid_step, gmax), wl.seq_lens,
-                            wl.seq_task, grid_step, gmax, R, mode, chunking=1)
+                            wl.seq_task, grid_step, gmax, R, mode, chunking=0 if PAD["on"] else 1)
     rbase = np.concatenate([[0], np.cumsum(reps)])
+    bnd = np.asarray(d["boundaries"], np.float64)
     times = []
     for rep in range(int(rbase[-1])):
         gi = int(np.searchsorted(rbase, rep, side="right") - 1)
         mine = d["seq_replica"] == rep
         t = 0.0
         for c in set(d["seq_chunk"][mine].tolist()):
-            ls = wl.seq_lens[mine & (d["seq_chunk"] == c)].astype(np.float64)
+            sel = mine & (d["seq_chunk"] == c)
+            ls = wl.seq_lens[sel].astype(np.float64)
+            if PAD["on"]:   # every sequence of an App. D micro-batch padded to its bucket length
+                ls = bnd[d["seq_bucket"][sel]]
             t += t_rep(tp[gi], float(ls.sum()), a0, a1, float((ls ** 2).sum()))
         times.append(t)
-    return max(times), float(np.mean(times))
+    pad_tokens = float((bnd[d["seq_bucket"]] - wl.seq_lens).sum())
+    return max(times), float(np.mean(times)), pad_tokens
 
 
 def deployments(n=8, tps=(1, 2, 4)):
@@ -125,7 +147,11 @@ def main():
     ap.add_argument("--a0", type=float, default=None, help="skip the GPU measurement (seconds)")
     ap.add_argument("--a1", type=float, default=None)
     ap.add_argument("--layer-cost", default=None, help="App. D fit of the full layer (tools/bench_layer.py)")
+    ap.add_argument("--padding", action="store_true", help="the paper's padded micro-batches (P:272)")
+    ap.add_argument("--r-sweep", action="store_true", help="R-sensitivity of D (P:1155-1161)")
+    ap.add_argument("--calibration", default=None, help="reuse the calibration of a previous ablation JSON")
     args = ap.parse_args()
+    PAD["on"] = args.padding
     if args.layer_cost:
         lc = json.load(open(args.layer_cost))
         cal = {"source": args.layer_cost, "model": lc["model"], "a0_s": lc["c0_ms"] / 1e3,
@@ -133,6 +159,8 @@ def main():
         QUAD["c2"] = cal["c2_s_per_token_len"]
         if args.out.endswith("r1_ablation.json"):
             args.out = args.out.replace("r1_ablation.json", "r1_ablation_layer.json")
+    elif args.calibration:
+        cal = json.load(open(args.calibration))["calibration"]
     elif args.a0 is None:
         cal = measure_layer()
     else:
@@ -143,14 +171,17 @@ def main():
     batches = [synth.sample_batch(tasks, seed=100 + i, l_max=16384, per_task=per_task)
                for i in range(args.steps)]
     n = 8
-    res = {"calibration": cal, "n_gpus": n, "steps": args.steps, "strategies": {}}
+    res = {"calibration": cal, "n_gpus": n, "steps": args.steps, "padding": PAD["on"], "strategies": {}}
     # A: Task-Fused, homogeneous TP able to hold the longest sequence of every batch
     longest = max(int(b.seq_lens.max()) for b in batches)
     tpA = min(t for t in (1, 2, 4) if M_LIMIT[t] >= longest)
     depA = [(tpA, n // tpA, M_LIMIT[tpA])]
     t0 = time.time()
-    sA = [step_time(depA, b, 2, 256, 16, a0, a1) for b in batches]
-    res["strategies"]["A_task_fused"] = {"deployment": depA, "step_s": float(np.mean([x[0] for x in sA]))}
+    # the naive design fuses the batches with the same fixed 1K buckets as B and C (its padding
+    # is what dynamic bucketing, D, removes)
+    sA = [step_time(depA, b, 2, 1024, 16, a0, a1) for b in batches]
+    res["strategies"]["A_task_fused"] = {"deployment": depA, "step_s": float(np.mean([x[0] for x in sA])),
+                                         "pad_tokens": float(np.mean([x[2] for x in sA]))}
     # B-D on the best heterogeneous deployment for D (covering the longest sequence)
     best = None
     for dep in deployments(n):
@@ -165,11 +196,19 @@ def main():
                              ("D_lobra_balanced_dynamic", 0, 256)):
         st = [step_time(dep, b, mode, grid, 16, a0, a1) for b in batches]
         res["strategies"][name] = {"deployment": dep, "step_s": float(np.mean([x[0] for x in st])),
-                                   "mean_replica_s": float(np.mean([x[1] for x in st]))}
+                                   "mean_replica_s": float(np.mean([x[1] for x in st])),
+                                   "pad_tokens": float(np.mean([x[2] for x in st]))}
     base = res["strategies"]["A_task_fused"]["step_s"]
     for k, v in res["strategies"].items():
         v["gpu_seconds"] = n * v["step_s"]
         v["reduction_vs_task_fused"] = 1.0 - v["step_s"] / base
+    if args.r_sweep:
+        res["r_sweep"] = {}
+        for R in (4, 8, 12, 16, 24, 32):
+            st = [step_time(dep, b, 0, 256, R, a0, a1) for b in batches]
+            res["r_sweep"][R] = {"step_s": float(np.mean([x[0] for x in st])),
+                                 "pad_tokens": float(np.mean([x[2] for x in st])),
+                                 "reduction_vs_task_fused": 1.0 - float(np.mean([x[0] for x in st])) / base}
     res["planning_wall_s"] = time.time() - t0
     res["tokens_per_step"] = float(np.mean([b.T for b in batches]))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
