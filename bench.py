@@ -629,9 +629,14 @@ def main():
     achieved = dom_fl / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("k_gemm_" + dom.split("_")[1])
+    if os.path.exists(tf):   # ncu DRAM bytes per launch of this workload's dominant class
+        traffic = json.load(open(tf)).get(workload, {}).get("k_gemm_" + dom.split("_")[1])
+    # algorithmic DRAM bytes per launch of the class: each operand once (activations, the
+    # weight, the bf16 output), averaged over the projections' launches
+    Tl = T_step_local
+    alg_b = float(np.mean([2.0 * (Tl * p.in_l + p.in_l * p.out_l + Tl * p.out_l) for p in layer.projs]))
     roofline = {"bound": "tensor", "kernel": f"k_gemm ({dom})", "achieved": achieved, "peak": peak_t,
+                "algorithmic_bytes_per_launch": alg_b,
                 "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": traffic,
                 "peak_source": f"{peak_src} {peak_kind} (burst)" + ("; sw_power_cap was active in the timed region" if capped else ""),
                 "frac_vs_sustained": achieved / peak_sus,

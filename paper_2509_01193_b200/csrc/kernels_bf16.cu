@@ -278,7 +278,17 @@ __device__ __forceinline__ void for_union(const Meta& m, int tA, int tB, uint32_
 
 // Pair-tile order: groups of `group_m` pair-M blocks, N-major inside a group, so that the
 // concurrently running clusters share a few X panels AND a few W panels (both stay in L2).
+// group_m < 0: the transpose -- groups of -group_m N blocks, M-major inside a group.
 __device__ __forceinline__ void pair_tile(int pt, int ntm2, int ntn, int group_m, int& mp, int& n) {
+  if (group_m < -1) {
+    const int gn_ = -group_m;
+    const int per_group = gn_ * ntm2;
+    const int g = pt / per_group, r = pt % per_group;
+    const int gn = min(gn_, ntn - g * gn_);
+    n = g * gn_ + r % gn;
+    mp = r / gn;
+    return;
+  }
   if (group_m <= 1) {
     mp = pt / ntn, n = pt % ntn;
     return;
@@ -1698,6 +1708,7 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cfg.attrs = attr;
   cfg.numAttrs = use_pdl() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  note_launch();
 }
 }  // namespace
 void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int ld8,
@@ -1977,6 +1988,17 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
   launch_k(k_gfin, dim3(num_sms * 2), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
 }
 
+// Tile order of the 2-CTA GEMM per shape class (pair_tile).  Measured defaults
+// (profiles/r1_gemm_raster.md, r2_gemm_raster.md); tuning overrides, read per launch:
+// LOBRA_GEMM_GM_SMALL (weight <= 48 MB), LOBRA_GEMM_GM_NBIG (large weight, N >= K),
+// LOBRA_GEMM_GM_KBIG (large weight, K > N).
+int gemm_group_m(int N, int K) {
+  const bool big = (double)N * K * 2 > 48e6;
+  const char* key = !big ? "LOBRA_GEMM_GM_SMALL" : (K > N ? "LOBRA_GEMM_GM_KBIG" : "LOBRA_GEMM_GM_NBIG");
+  if (const char* e = getenv(key)) return atoi(e);
+  return !big ? 1 : 16;
+}
+
 bool gemm_uses_pair() {
   const char* e = getenv("LOBRA_GEMM_1CTA");
   return !(e && e[0] == '1');
@@ -2005,16 +2027,7 @@ void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
     a.C = C;
     a.meta = meta;
     a.tp = tp ? *tp : TpScatter{};
-    {
-      // measured (profiles/r1_gemm_raster.md): N-fastest is best while W fits in L2 next to
-      // the X panels; 16-block groups once W is large (gate/up/down: 90 MB)
-      static int gm = -2;
-      if (gm == -2) {
-        const char* e = getenv("LOBRA_GEMM_GROUP_M");
-        gm = e ? atoi(e) : -1;
-      }
-      a.group_m = gm >= 0 ? gm : ((double)N * K * 2 > 48e6 ? 16 : 1);
-    }
+    a.group_m = gemm_group_m(N, K);
     const int tiles = a.ntm2 * a.ntn;
     int clusters = num_sms / 2;
     if (tiles < clusters) clusters = tiles;

@@ -99,7 +99,7 @@ __global__ void k32_segred(int dir, const float* __restrict__ Z, const float* __
 
 void launch_f32_rowproj(int dir, const float* Z, const float* A, const float* B, int in, int out,
                         const Meta& meta, float* H, cudaStream_t st) {
-  if (meta.T > 0) k32_rowproj<<<meta.T, kSlotW, 0, st>>>(dir, Z, A, B, in, out, meta, H);
+  if (meta.T > 0) { k32_rowproj<<<meta.T, kSlotW, 0, st>>>(dir, Z, A, B, in, out, meta, H); note_launch(); }
 }
 
 void launch_f32_gemm(int dir, const float* Z, const float* W, const float* A, const float* B,
@@ -107,12 +107,13 @@ void launch_f32_gemm(int dir, const float* Z, const float* W, const float* A, co
                      cudaStream_t st) {
   const int N = dir == 0 ? out : in;
   dim3 grid((N + 15) / 16, (meta.T + 15) / 16);
-  if (meta.T > 0) k32_gemm<<<grid, dim3(16, 16), 0, st>>>(dir, Z, W, A, B, H, in, out, meta, C, accumulate);
+  if (meta.T > 0) { k32_gemm<<<grid, dim3(16, 16), 0, st>>>(dir, Z, W, A, B, H, in, out, meta, C, accumulate); note_launch(); }
 }
 
 void launch_f32_segred(int dir, const float* Z, const float* H, int width, const Meta& meta,
                        float* out, long long ld, int accumulate, cudaStream_t st) {
   k32_segred<<<592, 256, 0, st>>>(dir, Z, H, width, meta, out, ld, accumulate);
+  note_launch();
 }
 
 }  // namespace lobra

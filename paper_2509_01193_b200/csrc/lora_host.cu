@@ -83,7 +83,8 @@ struct Prof {
   cudaStream_t st;
   cudaEvent_t e0 = nullptr;
   Prof(int k, cudaStream_t s) : kind(k), st(s) {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    // launches are counted where they happen (note_launch: launch_k and the fp32 launchers),
+    // so a launcher that enqueues two kernels (dY pass + G finalize) counts two
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (g_prof_on) {
       e0 = prof_event();
@@ -99,6 +100,9 @@ struct Prof {
   }
 };
 }  // namespace
+
+// One kernel launch of the library (called by every launcher right after it enqueues).
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // Launch accounting for kernels outside this file (begin/end bracket one launch).
 int64_t count_launch(int kind, cudaStream_t st, bool begin) {

@@ -79,6 +79,9 @@ __device__ __forceinline__ int row_task(const Meta& m, int row) {
 // B_cat [out, rsum] -> Bp [out, ld8] with task t's columns at boff[t] (8-aligned, zero
 // padded): only when some rank is not a multiple of 8 (TMA needs 16-byte aligned inner
 // coordinates and strides).
+// one library kernel launch (lora_host.cu): every launcher calls it after enqueueing
+void note_launch();
+
 void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int ld8,
                      const Meta& meta, cudaStream_t st);
 // Split factor of the rank-r projection for `ntiles` tiles and reduction length K.

@@ -31,5 +31,5 @@ def test_bench_two_ranks_one_gpu():
     assert r.returncode == 0 and len(lines) == 1, r.stdout[-3000:] + r.stderr[-3000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
-    assert d["config"]["global_batch_tokens"] == 2 * 16384
+    assert d["config"]["global_batch_tokens"] == 2 * 65536
     assert d["config"]["parallelism"] == "2xTP1"

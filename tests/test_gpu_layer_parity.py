@@ -161,3 +161,30 @@ def test_c3_qkv_gate_up_vs_oracle():
     shapes = [s for s in LLAMA2_7B if s[0] in ("q", "k", "v", "gate", "up")]
     layer, runs = _run(shapes, ranks, scales, [synth.config_c3(seed=3)], seed=33)
     _check(layer, runs, ranks, scales, sub_rows=8192)
+
+
+def test_launch_counter_matches_cupti():
+    """lobra_launch_count (the bench's `gpu_launches`) counts every kernel the library
+    enqueues -- the dY pass's G finalize included -- as CUPTI sees them."""
+    torch = _torch()
+    from torch.profiler import ProfilerActivity, profile
+    from paper_2509_01193_b200 import _lib
+    from paper_2509_01193_b200.layer import LLAMA2_7B, LoraLayer
+    tasks = synth.c2_tasks()
+    ranks, scales = [t.rank for t in tasks], [t.scale for t in tasks]
+    shapes = [(n, i // 4, o // 4, k, g) for n, i, o, k, g in LLAMA2_7B]
+    layer = LoraLayer(shapes, ranks, scales, torch.device("cuda:0"), torch.bfloat16, seed=3)
+    wl = synth.config_c2(seed=9, t_max=4096)
+    io = layer.alloc_io(wl.T, seed=4)
+    lens, tsk = wl.seq_lens.astype(np.int32), wl.seq_task.astype(np.int32)
+    layer.forward(lens, tsk, io, wl.T)            # warm (workspace allocation, attributes)
+    layer.backward(lens, tsk, io, wl.T, accumulate_dadb=False)
+    torch.cuda.synchronize()
+    n0 = _lib.lobra_launch_count()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        layer.forward(lens, tsk, io, wl.T)
+        layer.backward(lens, tsk, io, wl.T, accumulate_dadb=False)
+        torch.cuda.synchronize()
+    n = _lib.lobra_launch_count() - n0
+    kern = [e for e in prof.events() if e.device_type.name == "CUDA" and not e.name.startswith(("Memcpy", "Memset"))]
+    assert n == len(kern) > 0, (n, sorted({e.name.split("(")[0] for e in kern}))
