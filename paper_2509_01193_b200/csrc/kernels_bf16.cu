@@ -1,6 +1,7 @@
 // bf16 kernels of the multi-LoRA hot path for sm_100a (tcgen05 + TMEM + TMA).
 //
-// k_gemm     : C = Z W^T (fwd) or Z W (bwd, W as an MN-major operand) with the LoRA
+// k_gemm2    : 2-CTA (cta_group::2, 256 x 256 per CTA pair) persistent GEMM:
+//              C = Z W^T (fwd) or Z W (bwd, W as an MN-major operand) with the LoRA
 //              expand fused into the SAME TMEM accumulator as extra K steps over the
 //              tile's adapter slots ("K-extension"): "the computation of the base
 //              model can be fused into a batched operation whilst ... multiple LoRA
@@ -36,202 +37,14 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 }
 __device__ __forceinline__ int rpad16(int r) { return (r + 15) & ~15; }
 
-// =====================================================================================
-// GEMM with fused K-extension
-// =====================================================================================
-constexpr int G_BM = 128, G_BN = 256, G_BK = 64, G_STAGES = 4;
-constexpr int G_A_BYTES = G_BM * G_BK * 2;   // 16 KB
-constexpr int G_B_BYTES = G_BN * G_BK * 2;   // 32 KB
-constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;
-constexpr int G_SMEM = G_STAGES * G_STAGE_BYTES + 1024 + 256;
 constexpr int G_THREADS = 256;
-
-struct GemmArgs {
-  int T, N, K, ntm, ntn, accumulate;
-  __nv_bfloat16* C;
-  Meta meta;
-};
-
-template <bool kBMN>
-__global__ void __launch_bounds__(G_THREADS, 1)
-    k_gemm(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW,
-           const __grid_constant__ CUtensorMap mapSlot, const __grid_constant__ CUtensorMap mapV,
-           const GemmArgs args) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + G_STAGES * G_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + G_STAGES * G_B_BYTES);
-  uint64_t* empty = full + G_STAGES;
-  uint64_t* tfull = empty + G_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mapZ);
-    tma_prefetch(&mapW);
-    tma_prefetch(&mapSlot);
-    tma_prefetch(&mapV);
-  }
-  if (warp == 1 && lane == 0) {
-    for (int s = 0; s < G_STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
-    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 128);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();
-  pdl_launch_dependents();
-
-  const int ntiles = args.ntm * args.ntn;
-  const int nk = (args.K + G_BK - 1) / G_BK;
-  const Meta& meta = args.meta;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m = tile / args.ntn, n = tile % args.ntn;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], G_STAGE_BYTES);
-          tma_load_2d(sA + stage * G_A_BYTES, &mapZ, &full[stage], kb * G_BK, m * G_BM);
-          if (!kBMN) {
-            tma_load_2d(sB + stage * G_B_BYTES, &mapW, &full[stage], kb * G_BK, n * G_BN);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              tma_load_2d(sB + stage * G_B_BYTES + c * 8192, &mapW, &full[stage],
-                          n * G_BN + c * 64, kb * G_BK);
-          }
-          if (++stage == G_STAGES) stage = 0, phase ^= 1;
-        }
-        for (int s = meta.tile_slot_off[m]; s < meta.tile_slot_off[m + 1]; ++s) {
-          const int t = meta.slot_task[s];
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], G_STAGE_BYTES);
-          tma_load_2d(sA + stage * G_A_BYTES, &mapSlot, &full[stage], 0, s * kTileM);
-          // expand operand straight from the caller's adapters, box starting at roff[t]
-          if (!kBMN) {   // B operand [out, ld8]: K-major rows o, columns boff..boff+63
-            tma_load_2d(sB + stage * G_B_BYTES, &mapV, &full[stage], meta.boff[t], n * G_BN);
-          } else {       // A_cat [rsum, in]: MN-major, K rows roff..roff+63
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              tma_load_2d(sB + stage * G_B_BYTES + c * 8192, &mapV, &full[stage],
-                          n * G_BN + c * 64, meta.roff[t]);
-          }
-          if (++stage == G_STAGES) stage = 0, phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer (single thread)
-      const uint32_t id_main = idesc_bf16(G_BM, G_BN, false, kBMN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int m = tile / args.ntn;
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + acc * G_BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
-#pragma unroll
-          for (int k = 0; k < G_BK / 16; ++k) {
-            const uint64_t ad = sdesc_sw128(a0 + k * 32, 16, 1024);
-            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
-                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
-            mma_bf16(d, ad, bd, id_main, (kb | k) != 0);
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == G_STAGES) stage = 0, phase ^= 1;
-        }
-        for (int s = meta.tile_slot_off[m]; s < meta.tile_slot_off[m + 1]; ++s) {
-          const int nk16 = rpad16(meta.ranks[meta.slot_task[s]]) / 16;
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
-          for (int k = 0; k < nk16; ++k) {
-            const uint64_t bd = kBMN ? sdesc_sw128(b0 + k * 2048, 8192, 1024)
-                                     : sdesc_sw128(b0 + k * 32, 16, 1024);
-            mma_bf16(d, sdesc_sw128(a0 + (meta.band / 16 + k) * 32, 16, 1024), bd, id_main, 1u);
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == G_STAGES) stage = 0, phase ^= 1;
-        }
-        mma_commit(&tfull[acc]);
-      }
-    }
-  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> regs -> bf16 -> global
-    const uint32_t q = warp - 4;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int m = tile / args.ntn, n = tile % args.ntn;
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int row = m * G_BM + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c < G_BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(tmem + ((q * 32u) << 16) + acc * G_BN + c * 32, v);
-        const int col0 = n * G_BN + c * 32;
-        if (row < args.T && col0 < args.N) {
-          uint4* dst = reinterpret_cast<uint4*>(args.C + (size_t)row * args.N + col0);
-          if (args.accumulate) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 o = dst[j];
-              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&o);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h[e]);
-                v[j * 8 + 2 * e] += f.x;
-                v[j * 8 + 2 * e + 1] += f.y;
-              }
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 o;
-            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
-            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
-            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
-            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
-            dst[j] = o;
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-    }
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
 
 // =====================================================================================
 // 2-CTA GEMM with fused K-extension (cta_group::2): a CTA pair computes a 256 x 256 tile,
 // each CTA loads its own 128 rows of A and HALF (128 columns) of B, the leader issues
 // tcgen05.mma.cta_group::2 (M = 256) and each CTA drains its 128 accumulator rows.
-// Per CTA and K step: 32 KB of operands for 128 x 256 outputs (vs 48 KB for the 1-CTA
-// kernel) -> two thirds of the L2->SM operand traffic.
+// Per CTA and K step: 32 KB of operands for 128 x 256 outputs (a 1-CTA 128 x 256 tile needs
+// 48 KB) -> two thirds of the L2->SM operand traffic.
 // K-extension across the pair: the union of the two M tiles' tasks; a CTA whose tile lacks
 // a task feeds the all-zero slot (index meta.nslots) for that step.
 // =====================================================================================
@@ -1716,23 +1529,10 @@ void launch_pad_cols(const __nv_bfloat16* src, __nv_bfloat16* dst, int out, int 
   launch_k(k_pad_cols, dim3(592), dim3(256), 0, st, src, dst, out, ld8, meta);
 }
 
-// rank-r projection configurations: (stages, slots per pass); the resident CTAs per SM
-// follow from the shared memory (2 if <= 113 KB).  LOBRA_RP_CFG selects (tuning).
-struct RpCfg {
-  int stages, p, kb, per_sm;
-};
-static const RpCfg kRpCfg[] = {{3, 2, 1, 2}, {6, 1, 1, 1}, {3, 1, 2, 1}, {2, 1, 2, 2},
-                               {4, 1, 2, 1}, {2, 2, 2, 1}};
-
-int rp_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LOBRA_RP_CFG");
-    v = e ? atoi(e) : 0;
-    if (v < 0 || v > 5) v = 0;
-  }
-  return v;
-}
+// rank-r projection configuration (split-K k_rowproj for batches whose tiles cannot fill
+// the GPU): 3 stages, 2 slots per pass, 1 K block per stage, 2 resident CTAs per SM
+// (the best of the six configurations measured in round 1, profiles/r1_skinny_probes.md).
+constexpr int kRpPerSm = 2;
 
 bool rowproj_uses_ld() {   // opt-in (LOBRA_RP_LD=1): measured slower than TMA on B200
   const char* e = getenv("LOBRA_RP_LD");
@@ -1743,7 +1543,7 @@ int rowproj_splits(int ntiles, int K) {
   // one wave of similar-size CTAs: HBM-bound, so what matters is that every resident CTA
   // streams the same number of bytes
   const int nk = (K + 63) / 64;
-  const int per_sm = rowproj_uses_ld() ? (rp_cfg() == 3 ? 2 : 1) : kRpCfg[rp_cfg()].per_sm;
+  const int per_sm = rowproj_uses_ld() ? 1 : kRpPerSm;
   const int slots = per_sm * 148;
   int s = ntiles > 0 ? slots / ntiles : 1;
   if (const char* fs = getenv("LOBRA_RP_SPLITS")) {   // tuning override
@@ -1796,20 +1596,10 @@ void launch_rowproj(bool v_mn, const CUtensorMap& mapZ, const CUtensorMap& mapV,
   a.meta = meta;
   if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
   const int grid = meta.ntiles * a.nsplit;
-  switch (rp_cfg() * 2 + (v_mn ? 1 : 0)) {
-    case 0: launch_rp<false, 3, 2, 1>(grid, mapZ, mapV, a, st); break;
-    case 1: launch_rp<true, 3, 2, 1>(grid, mapZ, mapV, a, st); break;
-    case 2: launch_rp<false, 6, 1, 1>(grid, mapZ, mapV, a, st); break;
-    case 3: launch_rp<true, 6, 1, 1>(grid, mapZ, mapV, a, st); break;
-    case 4: launch_rp<false, 3, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 5: launch_rp<true, 3, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 6: launch_rp<false, 2, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 7: launch_rp<true, 2, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 8: launch_rp<false, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 9: launch_rp<true, 4, 1, 2>(grid, mapZ, mapV, a, st); break;
-    case 10: launch_rp<false, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
-    default: launch_rp<true, 2, 2, 2>(grid, mapZ, mapV, a, st); break;
-  }
+  if (v_mn)
+    launch_rp<true, 3, 2, 1>(grid, mapZ, mapV, a, st);
+  else
+    launch_rp<false, 3, 2, 1>(grid, mapZ, mapV, a, st);
 }
 
 bool shrink_applies(int ntiles, int num_sms) {
@@ -1931,12 +1721,7 @@ void launch_rowproj_ld(const __nv_bfloat16* Z, int K, const CUtensorMap& mapVk, 
   a.meta = meta;
   if (a.nsplit > 1) cudaMemsetAsync(counters, 0, sizeof(int) * meta.ntiles, st);
   const int grid = meta.ntiles * a.nsplit;
-  switch (rp_cfg()) {
-    case 1: launch_rpld<2, 4>(grid, mapVk, a, st); break;
-    case 2: launch_rpld<4, 2>(grid, mapVk, a, st); break;
-    case 3: launch_rpld<2, 2>(grid, mapVk, a, st); break;
-    default: launch_rpld<3, 2>(grid, mapVk, a, st); break;
-  }
+  launch_rpld<3, 2>(grid, mapVk, a, st);
 }
 
 int dypass_span(int qp) {
@@ -1996,62 +1781,41 @@ int gemm_group_m(int N, int K) {
   const bool big = (double)N * K * 2 > 48e6;
   const char* key = !big ? "LOBRA_GEMM_GM_SMALL" : (K > N ? "LOBRA_GEMM_GM_KBIG" : "LOBRA_GEMM_GM_NBIG");
   if (const char* e = getenv(key)) return atoi(e);
-  return !big ? 1 : 16;
+  // N = 11008 (gate/up fwd, down bwd): 16-block groups; K = 11008 (down fwd, gate/up bwd):
+  // N-fastest -- C3 DRAM bytes per launch 6.5 / 10.3 GB vs 10-18 / 12-20 GB for the other
+  // orders tried, 2-5% shorter launches (profiles/r2_gemm_raster.md)
+  return !big ? 1 : (K > N ? 1 : 16);
 }
 
-bool gemm_uses_pair() {
-  const char* e = getenv("LOBRA_GEMM_1CTA");
-  return !(e && e[0] == '1');
-}
 
 void launch_gemm(bool b_mn, const CUtensorMap& mapZ, const CUtensorMap& mapW,
                  const CUtensorMap& mapSlot, const CUtensorMap& mapVext, int T, int N, int K,
                  __nv_bfloat16* C, int accumulate, const Meta& meta, int num_sms,
                  cudaStream_t st, const TpScatter* tp) {
-  static int use_pair = -1;
-  if (use_pair < 0) {
-    use_pair = gemm_uses_pair() ? 1 : 0;
-    cudaFuncSetAttribute(k_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
-    cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
+  static bool init = false;
+  if (!init) {
     cudaFuncSetAttribute(k_gemm2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
     cudaFuncSetAttribute(k_gemm2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    init = true;
   }
-  if (use_pair) {
-    Gemm2Args a;
-    a.T = T;
-    a.N = N;
-    a.K = K;
-    a.ntm2 = (T + 255) / 256;
-    a.ntn = (N + 255) / 256;
-    a.accumulate = accumulate;
-    a.C = C;
-    a.meta = meta;
-    a.tp = tp ? *tp : TpScatter{};
-    a.group_m = gemm_group_m(N, K);
-    const int tiles = a.ntm2 * a.ntn;
-    int clusters = num_sms / 2;
-    if (tiles < clusters) clusters = tiles;
-    if (b_mn)
-      launch_k(k_gemm2<true>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
-    else
-      launch_k(k_gemm2<false>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
-    return;
-  }
-  GemmArgs a;
+  Gemm2Args a;
   a.T = T;
   a.N = N;
   a.K = K;
-  a.ntm = (T + G_BM - 1) / G_BM;
-  a.ntn = (N + G_BN - 1) / G_BN;
+  a.ntm2 = (T + 255) / 256;
+  a.ntn = (N + 255) / 256;
   a.accumulate = accumulate;
   a.C = C;
   a.meta = meta;
-  const int tiles = a.ntm * a.ntn;
-  const int grid = tiles < num_sms ? tiles : num_sms;
+  a.tp = tp ? *tp : TpScatter{};
+  a.group_m = gemm_group_m(N, K);
+  const int tiles = a.ntm2 * a.ntn;
+  int clusters = num_sms / 2;
+  if (tiles < clusters) clusters = tiles;
   if (b_mn)
-    launch_k(k_gemm<true>, dim3(grid), dim3(G_THREADS), G_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
+    launch_k(k_gemm2<true>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
   else
-    launch_k(k_gemm<false>, dim3(grid), dim3(G_THREADS), G_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
+    launch_k(k_gemm2<false>, dim3(2 * clusters), dim3(G_THREADS), P_SMEM, st, mapZ, mapW, mapSlot, mapVext, a);
 }
 
 void launch_segred(const CUtensorMap& mapZ, const CUtensorMap& mapSlot, int width,

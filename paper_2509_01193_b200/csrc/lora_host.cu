@@ -789,7 +789,7 @@ lobra_status lora_fwd_impl(const lobra_problem* prob, const lobra_batch* batch,
     CUtensorMap mX, mA, mW, mSlot, mB;
     if ((s = make_map(&mX, X, in, P.T, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mA, ad->A, in, (uint64_t)P.rsum, 64, 64)) != LOBRA_OK) return s;
-    const uint32_t bn = gemm_uses_pair() ? 128 : 256;
+    const uint32_t bn = 128;   // the 2-CTA GEMM: each CTA loads half of the 256 W rows
     if ((s = make_map(&mW, W, in, out, 64, bn)) != LOBRA_OK) return s;
     if ((s = make_map(&mSlot, Hs, 64, (uint64_t)(P.nslots + 1) * kTileM, 64, 128)) != LOBRA_OK) return s;
     if ((s = make_map(&mB, Bop, L.ld8, out, 64, bn)) != LOBRA_OK) return s;
@@ -817,7 +817,7 @@ lobra_status lora_fwd_impl(const lobra_problem* prob, const lobra_batch* batch,
     // reduces locally and every rank gathers Y; else the GEMM writes its partial into the
     // peer-visible stage area and the own all-reduce follows (no staging copy either way)
     TpScatter tps;
-    if (prob->tp_kind == LOBRA_TP_ROW && tp_fused() && gemm_uses_pair() &&
+    if (prob->tp_kind == LOBRA_TP_ROW && tp_fused() &&
         symm_scatter_target(comm_symm(prob->tp), P.T, out, &tps)) {
       { Prof p_(LOBRA_K_GEMM_FWD, st); launch_gemm(false, mX, mW, mSlot, mB, P.T, out, in,
                                                      static_cast<__nv_bfloat16*>(Y), 0, meta, ctx->num_sms, st,
@@ -942,7 +942,7 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     // column-parallel with a symmetric TP group: FUSED GEMM -> reduce-scatter (the epilogue adds
     // the local partial in dX when accumulating and stores each row into its owner's buffer)
     TpScatter tps;
-    const bool fused_tp = prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() && gemm_uses_pair() &&
+    const bool fused_tp = prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() &&
                           symm_scatter_target(comm_symm(prob->tp), P.T, in, &tps);
     { Prof p_(LOBRA_K_GEMM_BWD, st); launch_gemm(true, mdY, mWmn, mG, mAt, P.T, in, out, static_cast<__nv_bfloat16*>(dX),
                 accumulate_dx, meta, ctx->num_sms, st, fused_tp ? &tps : nullptr); }
@@ -963,7 +963,7 @@ extern "C" lobra_status lobra_lora_bwd(const lobra_problem* prob, const lobra_ba
     }
   }
   if ((s = check_launch("lobra_lora_bwd")) != LOBRA_OK) return s;
-  if (prob->dtype == LOBRA_BF16 && prob->tp_kind == LOBRA_TP_COLUMN && tp_fused() && gemm_uses_pair()) {
+  if (prob->dtype == LOBRA_BF16 && prob->tp_kind == LOBRA_TP_COLUMN && tp_fused()) {
     TpScatter tps;
     if (symm_scatter_target(comm_symm(prob->tp), P.T, in, &tps))   // the GEMM already scattered
       return symm_scatter_finish(comm_symm(prob->tp), P.T, in, dX, st);
@@ -1018,7 +1018,7 @@ int64_t min_out(const lobra_group_problem* g) {
 
 // Banded path applies: bf16, the bands fit the 64-wide slot, default backward kernels.
 bool group_fused(const lobra_group_problem* g, const lobra_group_adapters* ga) {
-  if (g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld() || !gemm_uses_pair()) return false;
+  if (g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld()) return false;
   int qp = 16;
   for (int t = 0; t < ga->num_tasks; ++t) qp = std::max(qp, (ga->ranks[t] + 15) & ~15);
   return g->num_proj * qp <= kSlotW;
@@ -1078,7 +1078,7 @@ bool wide_planes(const lobra_group_problem* g, const lobra_batch* b, const lobra
     const char* e = getenv("LOBRA_WIDE_GROUP");   // 0: plain per-projection sequence (A/B)
     v = e ? atoi(e) : 1;
   }
-  if (!v || g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld() || !gemm_uses_pair() ||
+  if (!v || g->dtype != LOBRA_BF16 || !dy_fused() || rowproj_uses_ld() ||
       g->tp_kind == LOBRA_TP_ROW || g->num_proj < 2)
     return false;
   int qp = 16;

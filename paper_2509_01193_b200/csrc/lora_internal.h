@@ -126,7 +126,6 @@ void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int 
 //                 Vext = A_cat [rsum, N] (MN-major)
 // true: the 2-CTA (cta_group::2) GEMM is used; its B boxes are 128 rows/columns per CTA
 // (env LOBRA_GEMM_1CTA=1 selects the 1-CTA kernel with 256-wide boxes).
-bool gemm_uses_pair();
 // bf16 2D TMA map, 128-byte swizzle (lora_host.cu)
 lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
                                 uint32_t box_inner, uint32_t box_outer);

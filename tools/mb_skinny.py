@@ -66,7 +66,7 @@ def run(d_in, d_out, reps=20):
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)
-    res = {"cfg": os.environ.get("LOBRA_RP_CFG", "0")}
+    res = {}
     for name, (i, o) in {"q": (4096, 4096), "gate": (4096, 11008), "down": (11008, 4096)}.items():
         res[name] = run(i, o)
     print(json.dumps(res))
