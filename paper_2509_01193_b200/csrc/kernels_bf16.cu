@@ -1106,8 +1106,10 @@ __global__ void __launch_bounds__(256, 1)
 // =====================================================================================
 // The H slot and B_t operands are MN-major (q contiguous) boxes only as wide as the rank needs:
 // `hrow` = 32 / 64 / 128 bytes (16 / 32 / 64 q, TMA and UMMA swizzle of that span), MMA N = nq.
-// A stage is [dY 2 x 16 KB][H 128 tokens x hrow][B 2 x 64 o x hrow]: 40 KB for rank 16, so
-// five stages (160 KB of dY) are in flight.
+// A stage is [dY 2 x 16 KB][B 2 x 64 o x hrow]; the H slot (128 tokens x hrow) is loaded
+// ONCE per (slot, chunk) into a 2-entry ring beside the stages and serves the chunk's four
+// sub-blocks (it used to ride in every stage): 6 / 5 / 4 stages (192 / 160 / 128 KB of dY in
+// flight) for hrow 32 / 64 / 128 instead of 5 / 4 / 3.
 constexpr int Y_Z_BYTES = 2 * 128 * 64 * 2;   // dY tile: 2 boxes of 64 cols x 128 rows
 constexpr int Y_SMEM = 232448;                // stages fill the shared memory (one CTA per SM)
 
@@ -1128,13 +1130,16 @@ __global__ void __launch_bounds__(256, 1)
   const int NS = args.stages, SB = args.stage_bytes, hrow = args.hrow;
   const int hbytes = 128 * hrow;          // H region (128 tokens)
   const int bbox = 64 * hrow;             // one B box (64 o rows)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * SB);
+  uint8_t* hbuf = smem + NS * SB;         // [2][hbytes]: the H ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + 2 * hbytes);
   uint64_t* empty = full + 8;
   uint64_t* gfull = empty + 8;           // [2]
   uint64_t* gempty = gfull + 2;          // [2]
   uint64_t* bfull = gempty + 2;          // [1]
   uint64_t* bempty = bfull + 1;          // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
+  uint64_t* hfull = bempty + 1;          // [2]
+  uint64_t* hempty = hfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
   const uint32_t warp = warp_id(), lane = lane_id();
   const Meta& meta = args.meta;
 
@@ -1144,6 +1149,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) mbar_init(&gfull[a], 1), mbar_init(&gempty[a], 128);
     mbar_init(bfull, 1);
     mbar_init(bempty, 128);
+    for (int a = 0; a < 2; ++a) mbar_init(&hfull[a], 1), mbar_init(&hempty[a], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -1158,30 +1164,34 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      int hcount = 0;
       for (int u = meta.dy_cta_off[blockIdx.x]; u < meta.dy_cta_off[blockIdx.x + 1]; ++u) {
         const int c = meta.dy_unit_chunk[u];
         const int t = meta.dy_unit_task[u];
         const int nb = min(4, args.n128 - c * 4);
         if (nb <= 0) continue;   // a chunk past this projection's width (group of unequal outs)
-        for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k) {
+        for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k, ++hcount) {
           const int sl = meta.task_slots[k];
           const int tile = meta.slot_tile[sl];
+          // the slot's H (this projection's band only, or all 64 columns for hrow 128), once
+          // for the chunk's sub-blocks
+          const int hb = hcount & 1;
+          mbar_wait(&hempty[hb], ((hcount >> 1) & 1) ^ 1);
+          mbar_expect_tx(&hfull[hb], (args.dbg_dy_only & 1) ? 0 : hbytes);
+          if (!(args.dbg_dy_only & 1))
+            tma_load_2d(hbuf + hb * hbytes, &mapH, &hfull[hb], hrow == 128 ? 0 : meta.band, sl * kTileM);
           for (int b = 0; b < nb; ++b) {
             const int col = c * 512 + b * 128;
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], (args.dbg_dy_only & 1) ? Y_Z_BYTES : Y_Z_BYTES + hbytes + 2 * bbox);
+            mbar_expect_tx(&full[stage], (args.dbg_dy_only & 1) ? Y_Z_BYTES : Y_Z_BYTES + 2 * bbox);
             uint8_t* st = smem + stage * SB;
             tma_load_2d(st, &mapDY, &full[stage], col, tile * kTileM);
             tma_load_2d(st + 16384, &mapDY, &full[stage], col + 64, tile * kTileM);
-            if (args.dbg_dy_only & 1) {
-              if (++stage == NS) stage = 0, phase ^= 1;
-              continue;
+            if (!(args.dbg_dy_only & 1)) {
+              // B_t straight from the caller's B (MN-major: q contiguous, rows = o = K)
+              tma_load_2d(st + Y_Z_BYTES, &mapBt, &full[stage], meta.boff[t], col);
+              tma_load_2d(st + Y_Z_BYTES + bbox, &mapBt, &full[stage], meta.boff[t], col + 64);
             }
-            // H slot columns: this projection's band only (narrow box), or all 64 (hrow 128)
-            tma_load_2d(st + Y_Z_BYTES, &mapH, &full[stage], hrow == 128 ? 0 : meta.band, sl * kTileM);
-            // B_t straight from the caller's B (MN-major: q contiguous, rows = o = K)
-            tma_load_2d(st + Y_Z_BYTES + hbytes, &mapBt, &full[stage], meta.boff[t], col);
-            tma_load_2d(st + Y_Z_BYTES + hbytes + bbox, &mapBt, &full[stage], meta.boff[t], col + 64);
             if (++stage == NS) stage = 0, phase ^= 1;
           }
         }
@@ -1194,8 +1204,8 @@ __global__ void __launch_bounds__(256, 1)
       // stage-0 descriptors of the H and B regions; per K step (16 rows) + hstep, per B box
       // + bstep4 (address field units of 16 bytes)
       const uint32_t s0 = smem_u32(smem);
-      const uint64_t hdesc0 = sdesc_sw(s0 + Y_Z_BYTES, hbytes, 8 * hrow, hrow);
-      const uint64_t tdesc0 = sdesc_sw(s0 + Y_Z_BYTES + hbytes, bbox, 8 * hrow, hrow);
+      const uint64_t hdesc0 = sdesc_sw(smem_u32(hbuf), hbytes, 8 * hrow, hrow);
+      const uint64_t tdesc0 = sdesc_sw(s0 + Y_Z_BYTES, bbox, 8 * hrow, hrow);
       const int hstep = hrow;            // 16 rows x hrow bytes >> 4
       const int bstep4 = bbox >> 4;
       int stage = 0;
@@ -1211,8 +1221,10 @@ __global__ void __launch_bounds__(256, 1)
         for (int k = meta.dy_unit_s0[u]; k < meta.dy_unit_s1[u]; ++k, ++gcount) {
           const int gb = gcount & 1;
           mbar_wait(&gempty[gb], ((gcount >> 1) & 1) ^ 1);
+          mbar_wait(&hfull[gb], (gcount >> 1) & 1);   // the H ring advances with the slots
           tc_fence_after();
           const uint32_t dg = tmem + 256 + gb * 64;
+          const uint64_t dh = hdesc0 + ((uint64_t)(gb * hbytes) >> 4);
           for (int b = 0; b < nb; ++b) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
@@ -1221,7 +1233,6 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t z0 = smem_u32(smem + stage * SB);
             const uint64_t dz_mn = sdesc_sw128(z0, 16384, 1024);
             const uint64_t dz_k = sdesc_sw128(z0, 16, 1024);
-            const uint64_t dh = hdesc0 + ((uint64_t)(stage * SB) >> 4);
             const uint64_t dt = tdesc0 + ((uint64_t)(stage * SB) >> 4);
             if (!(args.dbg_dy_only & 2)) {   // probe bit 1: skip the dB MMAs
 #pragma unroll
@@ -1242,6 +1253,7 @@ __global__ void __launch_bounds__(256, 1)
             if (++stage == NS) stage = 0, phase ^= 1;
           }
           mma_commit(&gfull[gb]);
+          mma_commit(&hempty[gb]);
           first_slot = false;
         }
         mma_commit(bfull);
@@ -1745,8 +1757,8 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
   DyArgs a;
   a.hrow = dypass_span(qp);
   a.nq = a.hrow / 2;
-  a.stage_bytes = Y_Z_BYTES + 128 * a.hrow + 2 * 64 * a.hrow;
-  a.stages = std::min(8, (Y_SMEM - 1024 - 256) / a.stage_bytes);
+  a.stage_bytes = Y_Z_BYTES + 2 * 64 * a.hrow;
+  a.stages = std::min(8, (Y_SMEM - 1024 - 256 - 2 * 128 * a.hrow) / a.stage_bytes);
   if (const char* e = getenv("LOBRA_DY_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(e)));
   a.width = width;
   a.n128 = (width + 127) / 128;
