@@ -425,6 +425,10 @@ bool eq3_exact(const Inst& L, const std::vector<i64>& tp, Budget& bud, i64 node_
   }
   lobra::eq3::Stats st;
   st.cap = node_cap > 0 ? node_cap : (i64)1000000;
+  // the branch-and-bound subtrees run on a pool (exact either way; only the certificates
+  // met on the way may differ, never the canonical d)
+  lobra::eq3::Pool pool(lobra::eq3::default_threads());
+  st.pool = &pool;
   MultiLex ml(L, st);
   std::vector<std::vector<i64>> d = dl;
   const bool ok = ml.run(d, UB, t_only);

@@ -19,15 +19,20 @@
 //   * branching: a fractional q of the group with the most replicas, most fractional first,
 //     down branch first;
 //   * incumbents: LP rounding + greedy repair, verified in integer arithmetic.
+//   * parallel: the open subtrees below depth kSplitDepth run on a thread pool; the first
+//     certificate stops the others (same answer, possibly another certificate).
 // Measured (C5-scale steps, B ~ 1952, R = 16; profiles/r2_dispatch_solve_times.md):
-// 3 groups on 8 GPUs ~20-50 ms, 3 groups with p = 4/2/1 and 4 groups ~0.2-0.8 s.
+// 3 groups on 8 GPUs ~20-35 ms, 3 groups with p = 4/2/1 and 4 groups ~60-180 ms (8 cores).
 // Every "feasible" answer carries an integer certificate; every "infeasible" answer is a
 // complete search whose pruning used only valid lower bounds.  The only way to be undecided
 // is the node budget (returned as -1, surfaced as LOBRA_ERR_BUDGET by the caller).
 #include "eq3_bb.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
+#include <deque>
 #include <limits>
 
 namespace lobra {
@@ -152,6 +157,7 @@ struct Model {
   std::vector<int> vi, vj;                 // q var -> (group, bucket)
   std::vector<std::vector<int>> var_of;    // [G][R] -> var index or -1
   std::vector<int> cover_row;              // [R] -> row or -1
+  std::vector<int> repair_order;           // buckets with demand, largest cost first
   int nq = 0;
 };
 
@@ -200,6 +206,15 @@ LP build_lp(const Cover& in, Model& md) {
   }
   for (int j = 0; j < in.R; ++j)
     if (md.cover_row[j] >= 0) rhs[md.cover_row[j]] = -(double)in.D[j];
+  // buckets with the largest costs first (lumpy ones before the fine-grained fillers)
+  md.repair_order.clear();
+  for (int j = 0; j < in.R; ++j)
+    if (in.D[j] > 0) md.repair_order.push_back(j);
+  std::sort(md.repair_order.begin(), md.repair_order.end(), [&](int a, int b) {
+    int64_t ca = 0, cb = 0;
+    for (int i = 0; i < in.G; ++i) ca = std::max(ca, in.c[i][a]), cb = std::max(cb, in.c[i][b]);
+    return ca != cb ? ca > cb : a < b;
+  });
   lp.lo[lp.zcol] = -tmax - 1.0;
   lp.x[lp.zcol] = lp.lo[lp.zcol];
   lp.d[lp.zcol] = 1.0;   // objective min z; slack basis => reduced costs = costs
@@ -265,7 +280,7 @@ double lagrangian(const Cover& in, const LP& lp, const Model& md) {
 struct Scratch {
   std::vector<double> f, lam, g;
   std::vector<int64_t> rest;
-  std::vector<int> ids, order;
+  std::vector<int> ids, order, gids;
   std::vector<int64_t> cnt, room, m;
   std::vector<double> w;
 };
@@ -332,11 +347,11 @@ double knap_min(const Cover& in, const LP& lp, const Model& md, int j, const std
   for (int k = 0; k < n; ++k) {
     int64_t c = cnt[k];
     const int64_t p = in.p[ids[k]];
+    double* F = f.data();
     if (c >= cdiv(rest, p)) {   // effectively unbounded: one forward pass
-      for (int64_t q = 1; q <= rest; ++q) {
-        const double vv = f[(size_t)std::max<int64_t>(0, q - p)] + w[k];
-        if (vv < f[q]) f[q] = vv;
-      }
+      const double wk = w[k];
+      for (int64_t q = 1; q <= std::min(p, rest); ++q) F[q] = std::min(F[q], F[0] + wk);
+      for (int64_t q = p + 1; q <= rest; ++q) F[q] = std::min(F[q], F[q - p] + wk);
       continue;
     }
     for (int64_t chunk = 1; c > 0; chunk <<= 1) {
@@ -344,10 +359,8 @@ double knap_min(const Cover& in, const LP& lp, const Model& md, int j, const std
       c -= take;
       const int64_t cv = take * p;
       const double cw = w[k] * (double)take;
-      for (int64_t q = rest; q >= 1; --q) {
-        const double vv = f[(size_t)std::max<int64_t>(0, q - cv)] + cw;
-        if (vv < f[q]) f[q] = vv;
-      }
+      for (int64_t q = rest; q > cv; --q) F[q] = std::min(F[q], F[q - cv] + cw);
+      for (int64_t q = std::min(cv, rest); q >= 1; --q) F[q] = std::min(F[q], F[0] + cw);
     }
   }
   return f[rest];
@@ -373,7 +386,8 @@ double lagrangian_node(const Cover& in, const LP& lp, const Model& md, Scratch& 
   sc.rest.assign(in.R, 0);
   sc.g.assign(in.R, 0.0);
   sc.order.resize(in.R);
-  std::vector<int> ids(in.G);
+  std::vector<int>& ids = sc.gids;
+  ids.resize(in.G);
   int64_t* rest_of = sc.rest.data();
   double* g_of = sc.g.data();
   for (int j = 0; j < in.R; ++j) {
@@ -467,28 +481,19 @@ bool verify(const Cover& in, const std::vector<std::vector<int64_t>>& q) {
 // Round the LP point down, then cover each bucket's deficit greedily with the group whose
 // budget stays the loosest.  Returns true with q on success.
 bool round_repair(const Cover& in, const LP& lp, const Model& md,
-                  std::vector<std::vector<int64_t>>& q) {
-  q.assign(in.G, std::vector<int64_t>(in.R, 0));
-  std::vector<int64_t> lo(md.nq), L(in.G, 0);
+                  std::vector<std::vector<int64_t>>& q, std::vector<int64_t>& L) {
+  q.resize(in.G);
+  for (auto& r : q) r.assign(in.R, 0);
+  L.assign(in.G, 0);
   for (int v = 0; v < md.nq; ++v) {
     const double val = lp.value(v);
     int64_t f = (int64_t)std::floor(val + 1e-9);
     f = std::max<int64_t>((int64_t)lp.lo[v], std::min<int64_t>((int64_t)lp.hi[v], f));
     q[md.vi[v]][md.vj[v]] = f;
-    lo[v] = (int64_t)lp.lo[v];
   }
   for (int i = 0; i < in.G; ++i)
     for (int j = 0; j < in.R; ++j) L[i] += in.c[i][j] * q[i][j];
-  // buckets with the largest costs first (lumpy ones before the fine-grained fillers)
-  std::vector<int> order;
-  for (int j = 0; j < in.R; ++j)
-    if (in.D[j] > 0) order.push_back(j);
-  std::sort(order.begin(), order.end(), [&](int a, int b) {
-    int64_t ca = 0, cb = 0;
-    for (int i = 0; i < in.G; ++i) ca = std::max(ca, in.c[i][a]), cb = std::max(cb, in.c[i][b]);
-    return ca != cb ? ca > cb : a < b;
-  });
-  for (int j : order) {
+  for (int j : md.repair_order) {
     int64_t cov = 0;
     for (int i = 0; i < in.G; ++i) cov += in.p[i] * q[i][j];
     int64_t def = in.D[j] - cov;
@@ -513,24 +518,64 @@ bool round_repair(const Cover& in, const LP& lp, const Model& md,
       def -= bk * in.p[bi];
     }
   }
-  (void)lo;
   return verify(in, q);
 }
+
+// Shared state of one feasibility search (all threads).
+struct Shared {
+  std::atomic<int64_t> nodes{0};
+  std::atomic<int64_t> pivots{0};
+  std::atomic<int> found{0};    // a certificate is stored in sol: every thread stops
+  std::atomic<int> budget{0};   // the node budget ran out
+  int64_t cap = 0;
+  std::mutex mu;
+  std::vector<std::vector<int64_t>> sol;
+};
+
+// Subtrees below this depth are the parallel tasks (up to 2^depth of them).
+constexpr int kSplitDepth = 10;
 
 struct BB {
   const Cover& in;
   const Model& md;
-  Stats& st;
-  std::vector<std::vector<int64_t>> sol;
+  Shared& sh;
+  std::vector<std::vector<int64_t>> cand;
+  std::vector<int64_t> loads;
+  std::deque<LP> stk;   // child LPs by depth (storage reused; deque: growth keeps references)
   Scratch sc;
-  BB(const Cover& c, const Model& m, Stats& s) : in(c), md(m), st(s) {}
+  std::vector<LP>* frontier = nullptr;   // set while collecting the parallel tasks
+  BB(const Cover& c, const Model& m, Shared& s) : in(c), md(m), sh(s) {}
 
-  // 1 feasible, 0 infeasible subtree, -1 budget
-  int node(LP& lp) {
-    if (++st.nodes > st.cap) return -1;
-    const int rc = lp.solve(ZTOL, 20000, st.lp_pivots);
+  int found(const std::vector<std::vector<int64_t>>& q) {
+    std::lock_guard<std::mutex> lk(sh.mu);
+    if (!sh.found.load()) {
+      sh.sol = q;
+      sh.found.store(1);
+    }
+    return 1;
+  }
+
+  // 1 feasible (certificate in sh.sol), 0 infeasible subtree (or another thread already
+  // found a certificate), -1 budget
+  int node(LP& lp, int depth) {
+    if (sh.found.load(std::memory_order_relaxed)) return 0;
+    if (sh.budget.load(std::memory_order_relaxed)) return -1;
+    if (frontier && depth >= kSplitDepth) {
+      frontier->push_back(lp);
+      return 0;
+    }
+    if (sh.nodes.fetch_add(1, std::memory_order_relaxed) + 1 > sh.cap) {
+      sh.budget.store(1);
+      return -1;
+    }
+    int64_t piv = 0;
+    const int rc = lp.solve(ZTOL, 20000, piv);
+    sh.pivots.fetch_add(piv, std::memory_order_relaxed);
     if (rc == 1) return 0;
-    if (rc == 2) return -1;
+    if (rc == 2) {
+      sh.budget.store(1);
+      return -1;
+    }
     if (lp.z() > ZTOL) return 0;
     // the per-bucket integer covering (Lagrangian) bound sees the ceil(d / p) rounding the
     // LP relaxation ignores (decisive with p_i >= 4: 5-30x fewer nodes, measured)
@@ -548,13 +593,13 @@ struct BB {
       const double s = (double)in.p[md.vi[v]] * 1e6 + dist;
       if (s > bs) bs = s, bv = v, bval = val;
     }
-    if (round_repair(in, lp, md, sol)) return 1;
+    if (round_repair(in, lp, md, cand, loads)) return found(cand);
     if (bv < 0) {
       // LP point integral up to tolerance: its rounding satisfies the integer constraints
       // unless the tolerance hid a violation; branch on the largest deviation instead
-      sol.assign(in.G, std::vector<int64_t>(in.R, 0));
-      for (int v = 0; v < md.nq; ++v) sol[md.vi[v]][md.vj[v]] = (int64_t)std::llround(lp.value(v));
-      if (verify(in, sol)) return 1;
+      cand.assign(in.G, std::vector<int64_t>(in.R, 0));
+      for (int v = 0; v < md.nq; ++v) cand[md.vi[v]][md.vj[v]] = (int64_t)std::llround(lp.value(v));
+      if (verify(in, cand)) return found(cand);
       double dev = 0;
       for (int v = 0; v < md.nq; ++v) {
         if (lp.lo[v] == lp.hi[v]) continue;
@@ -572,9 +617,11 @@ struct BB {
       if (up) l = std::max(l, fl + 1.0);
       else h = std::min(h, fl);
       if (l > h) continue;
-      LP child = lp;
+      while ((int)stk.size() <= depth) stk.emplace_back();
+      LP& child = stk[depth];   // copy-assignment reuses the vectors' storage
+      child = lp;
       child.set_bounds(bv, l, h);
-      const int r = node(child);
+      const int r = node(child, depth + 1);
       if (r != 0) return r;
     }
     return 0;
@@ -607,10 +654,33 @@ int feasible(const Cover& in, std::vector<std::vector<int64_t>>& q, Stats& st) {
   if (rc == 2) return -1;
   if (rc == 1 || lp.z() > ZTOL) return 0;
   if (lagrangian(in, lp, md) > ZTOL) return 0;
-  BB bb(in, md, st);
-  --st.nodes;   // the root is re-entered by node() (warm: already optimal)
-  const int r = bb.node(lp);
-  if (r == 1) q = bb.sol;
+  Shared sh;
+  sh.cap = st.cap - st.nodes + 1;   // the root is re-entered by node() (warm: already optimal)
+  int r;
+  if (!st.pool || st.pool->size() <= 1) {
+    BB bb(in, md, sh);
+    r = bb.node(lp, 0);
+  } else {
+    // depth-first down to kSplitDepth on this thread, the open subtrees below it on the pool
+    std::vector<LP> tasks;
+    BB top(in, md, sh);
+    top.frontier = &tasks;
+    r = top.node(lp, 0);
+    if (r == 0 && !sh.found.load() && !tasks.empty()) {
+      std::vector<BB> bbs;
+      bbs.reserve(st.pool->size());
+      for (int w = 0; w < st.pool->size(); ++w) bbs.emplace_back(in, md, sh);
+      st.pool->run((int)tasks.size(), [&](int w, int k) {
+        if (!sh.found.load(std::memory_order_relaxed) && !sh.budget.load(std::memory_order_relaxed))
+          bbs[w].node(tasks[k], kSplitDepth + 1);
+      });
+    }
+    r = sh.found.load() ? 1 : sh.budget.load() ? -1 : 0;
+  }
+  if (sh.found.load()) r = 1;
+  st.nodes += sh.nodes.load() - 1;
+  st.lp_pivots += sh.pivots.load();
+  if (r == 1) q = sh.sol;
   return r;
 }
 
@@ -623,6 +693,83 @@ double lower_bound(const Cover& in, Stats& st) {
   if (rc == 1) return INF;
   if (rc == 2) return -INF;
   return std::max(lp.z(), lagrangian(in, lp, md));
+}
+
+Pool::Pool(int nthreads) {
+  for (int w = 1; w < nthreads; ++w) threads_.emplace_back([this, w] { work(w); });
+}
+
+Pool::~Pool() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+// Every worker takes part in every generation (wakes, drains the task counter, reports), and
+// run() returns only after all of them reported, so no worker can carry a stale task
+// function into the next run().
+void Pool::work(int worker) {
+  uint64_t seen = 0;
+  for (;;) {
+    const std::function<void(int, int)>* f;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      f = f_;
+    }
+    for (;;) {
+      int k;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (next_ >= ntasks_) break;
+        k = next_++;
+      }
+      (*f)(worker, k);
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      ++reported_;
+    }
+    done_cv_.notify_all();
+  }
+}
+
+void Pool::run(int ntasks, const std::function<void(int, int)>& f) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    f_ = &f;
+    ntasks_ = ntasks;
+    next_ = 0;
+    reported_ = 0;
+    ++gen_;
+  }
+  cv_.notify_all();
+  for (;;) {   // the caller is worker 0
+    int k;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (next_ >= ntasks_) break;
+      k = next_++;
+    }
+    f(0, k);
+  }
+  std::unique_lock<std::mutex> lk(mu_);
+  done_cv_.wait(lk, [&] { return reported_ == (int)threads_.size(); });
+  f_ = nullptr;
+}
+
+int default_threads() {
+  if (const char* e = std::getenv("LOBRA_DISPATCH_THREADS")) {
+    const int n = std::atoi(e);
+    if (n >= 1) return std::min(n, 64);
+  }
+  const int hw = (int)std::thread::hardware_concurrency();
+  return std::max(1, std::min(16, hw - 1));
 }
 
 }  // namespace eq3
