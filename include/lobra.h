@@ -274,6 +274,24 @@ LOBRA_API lobra_status lobra_attn_fwd(int32_t num_seqs, const int32_t* seq_lens,
                                       int32_t n_kv_heads, int32_t head_dim, const void* Q, const void* K,
                                       const void* V, void* O, float* lse, void* ws, size_t ws_bytes,
                                       lobra_stream_t stream);
+/* lobra_attn_bwd: gradients of lobra_attn_fwd (FlashAttention's recomputation: P is rebuilt
+ *   from Q, K and the forward's lse, never stored).  Per query row: Dq = sum_d dO O,
+ *   P = exp(Q K^T / sqrt(128) - lse) under the same causal, per-sequence mask,
+ *   dS = P (dO V^T - Dq); dQ = dS K / sqrt(128), dK = dS^T Q / sqrt(128), dV = P^T dO, summed
+ *   over the query heads of each kv head.  Layouts as lobra_attn_fwd; O, dO, dQ
+ *   [T, n_heads * 128] bf16; dK, dV [T, n_kv_heads * 128] bf16 (overwritten; rows of every
+ *   sequence written, padding none).  P and dS are rounded to bf16 before their products
+ *   (as FlashAttention does), accumulation in fp32 (TMEM; dQ through an fp32 buffer in ws).
+ *   ws >= lobra_attn_bwd_workspace_bytes device bytes, 16-byte aligned pointers, head_dim
+ *   128 (else LOBRA_ERR_UNSUPPORTED).  Three launches (pre: Dq + zeroed dQ accumulator;
+ *   main; post: dQ scale + bf16). */
+LOBRA_API size_t lobra_attn_bwd_workspace_bytes(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads,
+                                                int32_t n_kv_heads);
+LOBRA_API lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads,
+                                      int32_t n_kv_heads, int32_t head_dim, const void* Q, const void* K,
+                                      const void* V, const void* O, const void* dO, const float* lse,
+                                      void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                                      lobra_stream_t stream);
 /* lobra_add: C = A + B elementwise over n bf16 (n % 8 == 0; C may alias A or B): the
  * layer's last residual add. */
 LOBRA_API lobra_status lobra_add(int64_t n, const void* A, const void* B, void* C, lobra_stream_t stream);

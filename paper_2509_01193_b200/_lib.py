@@ -30,7 +30,7 @@ EXPORTED = [
     "lobra_lora_group_bwd", "lobra_rmsnorm_fwd", "lobra_rmsnorm_bwd", "lobra_rope", "lobra_swiglu_fwd",
     "lobra_swiglu_bwd", "lobra_add", "lobra_symm_create", "lobra_symm_open", "lobra_symm_destroy",
     "lobra_symm_data", "lobra_symm_allreduce", "lobra_comm_from_symm", "lobra_comm_attach_symm",
-    "lobra_attn_workspace_bytes", "lobra_attn_fwd", "lobra_replica_time",
+    "lobra_attn_workspace_bytes", "lobra_attn_fwd", "lobra_attn_bwd_workspace_bytes", "lobra_attn_bwd", "lobra_replica_time",
 ]
 K_NAMES = ["gemm_fwd", "gemm_bwd", "rowproj", "segred", "finalize", "pad", "fp32", "optim", "layer", "comm"]
 
@@ -176,6 +176,11 @@ def load() -> C.CDLL:
     lib.lobra_attn_fwd.restype = C.c_int
     lib.lobra_attn_fwd.argtypes = [C.c_int32, _i32p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.lobra_attn_bwd_workspace_bytes.restype = C.c_size_t
+    lib.lobra_attn_bwd_workspace_bytes.argtypes = [C.c_int32, _i32p, C.c_int32, C.c_int32]
+    lib.lobra_attn_bwd.restype = C.c_int
+    lib.lobra_attn_bwd.argtypes = [C.c_int32, _i32p, C.c_int32, C.c_int32, C.c_int32] + [C.c_void_p] * 10 + \
+        [C.c_size_t, C.c_void_p]
     lib.lobra_add.restype = C.c_int
     lib.lobra_add.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.lobra_dispatch.restype = C.c_int
@@ -624,6 +629,21 @@ def lobra_comm_attach_symm(comm: Comm, symm: Symm | None):
 def lobra_attn_workspace_bytes(seq_lens, n_heads) -> int:
     lens = _i32(seq_lens)
     return int(load().lobra_attn_workspace_bytes(len(lens), lens.ctypes.data_as(_i32p), int(n_heads)))
+
+
+def lobra_attn_bwd_workspace_bytes(seq_lens, n_heads, n_kv_heads) -> int:
+    lens = _i32(seq_lens)
+    return int(load().lobra_attn_bwd_workspace_bytes(len(lens), lens.ctypes.data_as(_i32p), int(n_heads),
+                                                     int(n_kv_heads)))
+
+
+def lobra_attn_bwd(seq_lens, Q, K, V, O, dO, lse, dQ, dK, dV, ws, stream=None):
+    """Gradients of lobra_attn_fwd (tcgen05): dQ [T, H, 128], dK, dV [T, Hkv, 128] (include/lobra.h)."""
+    lens = _i32(seq_lens)
+    H, D, Hkv = int(Q.shape[-2]), int(Q.shape[-1]), int(K.shape[-2])
+    _check(load().lobra_attn_bwd(len(lens), lens.ctypes.data_as(_i32p), H, Hkv, D, _ptr(Q), _ptr(K), _ptr(V),
+                                 _ptr(O), _ptr(dO), _ptr(lse), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(ws),
+                                 ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def lobra_attn_fwd(seq_lens, Q, K, V, O, lse, ws, stream=None):

@@ -9,8 +9,8 @@ causal masks (block-diagonal over the pack):
     sequences of the pack addressed through ragged offsets, no padding copies); graphs
     are built once per (batch bucket, max-length bucket) and cached;
   * "flash_attn": FlashAttention-2 varlen kernels (mma.sync; measured ~3x slower on B200);
-  * "lobra": our own tcgen05 forward (lobra_attn_fwd, csrc/attn.cu) with FlashAttention-2's
-    varlen backward consuming its O and LSE.
+  * "lobra": our own tcgen05 kernels, forward (lobra_attn_fwd) and backward
+    (lobra_attn_bwd, recomputation from the forward's LSE), csrc/attn.cu.
 """
 from __future__ import annotations
 
@@ -151,25 +151,34 @@ class FlashVarlenAttention:
                                             1.0 / math.sqrt(self.D), True, -1, -1, 0.0, None, self.det)
 
 
-class LobraVarlenAttention(FlashVarlenAttention):
-    """Own tcgen05 forward (O, LSE in FlashAttention's varlen layout) + FA2 varlen backward."""
+class LobraVarlenAttention:
+    """Own tcgen05 kernels for both directions: lobra_attn_fwd (O, LSE [H, T]) and
+    lobra_attn_bwd (recomputation from the LSE; csrc/attn.cu)."""
 
-    def __init__(self, n_heads: int, head_dim: int, device, deterministic=False):
-        super().__init__(n_heads, head_dim, device, deterministic)
+    def __init__(self, n_heads: int, head_dim: int, device, n_kv_heads: int | None = None):
         from . import _lib
-        self.lib, self.H = _lib, n_heads
+        self.lib, self.H, self.D = _lib, n_heads, head_dim
+        self.Hkv = n_kv_heads or n_heads
+        self.dev = torch.device(device)
         self.ws = torch.empty(0, dtype=torch.uint8, device=self.dev)
 
-    def forward(self, q, k, v, seq_lens):
-        cu = torch.from_numpy(np.concatenate([[0], np.cumsum(seq_lens)]).astype(np.int32)).to(self.dev)
-        m = int(max(seq_lens)) if len(seq_lens) else 0
-        need = self.lib.lobra_attn_workspace_bytes(seq_lens, self.H)
+    def _ws(self, need):
         if self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+        return self.ws
+
+    def forward(self, q, k, v, seq_lens):
+        lens = np.asarray(seq_lens, np.int32)
+        ws = self._ws(self.lib.lobra_attn_workspace_bytes(lens, self.H))
         o = torch.empty_like(q)
         lse = torch.empty(self.H, q.shape[0], dtype=torch.float32, device=self.dev)
-        self.lib.lobra_attn_fwd(seq_lens, q, k, v, o, lse, self.ws)
-        return o, lse, (cu, m)
+        self.lib.lobra_attn_fwd(lens, q, k, v, o, lse, ws)
+        return o, lse, lens
+
+    def backward(self, dO, q, k, v, o, lse, ctx, dq, dk, dv):
+        lens = ctx
+        ws = self._ws(self.lib.lobra_attn_bwd_workspace_bytes(lens, self.H, k.shape[-2]))
+        self.lib.lobra_attn_bwd(lens, q, k, v, o, dO.contiguous(), lse, dq, dk, dv, ws)
 
 
 def make_attention(backend: str, n_heads: int, head_dim: int, device, deterministic=False,
@@ -180,5 +189,5 @@ def make_attention(backend: str, n_heads: int, head_dim: int, device, determinis
     if backend == "flash_attn":
         return FlashVarlenAttention(n_heads, head_dim, device, deterministic)
     if backend == "lobra":
-        return LobraVarlenAttention(n_heads, head_dim, device, deterministic)
+        return LobraVarlenAttention(n_heads, head_dim, device, n_kv_heads)
     raise ValueError(f"unknown attention backend {backend!r}")

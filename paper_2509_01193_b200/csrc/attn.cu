@@ -276,6 +276,342 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// =====================================================================================
+// Varlen causal attention BACKWARD on tcgen05 (FlashAttention's recomputation scheme: P is
+// rebuilt from the forward's LSE, never stored).  Per query row q of a sequence and head h:
+//   P = exp(S / sqrt(D) - LSE),  dP = dO V^T,  Dq = sum_d dO O,  dS = P (dP - Dq),
+//   dV = P^T dO,  dK = dS^T Q / sqrt(D),  dQ = dS K / sqrt(D).
+// One CTA per (sequence, 128-key tile j, kv head): K_j, V_j stay in shared memory; the CTA
+// walks the query tiles i >= j (causal) of every query head of the kv group, so dK_j and dV_j
+// accumulate in TMEM and are written once (no atomics); dQ_i partials are added into an fp32
+// accumulator with red.global.add (k_attn_bwd_post scales and rounds it).  The transposed
+// products put the KEY row in the TMEM lane: S^T = K Q^T and dP^T = V dO^T, so a softmax
+// thread owns one key row and writes P^T / dS^T rows straight into the K-major A layouts of
+// dV += P^T dO and dK += dS^T Q; the same dS^T buffer is the MN-major A operand of dQ = dS K.
+//   warp 0      TMA producer: K_j, V_j once; Q_i (2 stages) and dO_i per iteration
+//   warp 1      MMA issuer
+//   warp 2      TMEM allocator (512 columns: R0, R1, dV, dK)
+//   warps 4-7   P^T / dS^T (one key row per thread), final dK / dV epilogue
+//   warps 8-11  dQ drain (one query row per thread): TMEM -> red.global.add.v4.f32
+// TMEM roles alternate per iteration t: S^T -> R[t&1], dP^T -> R[(t+1)&1], dQ -> R[t&1], so
+// the next S^T is computed while dQ_t drains.
+// =====================================================================================
+constexpr int B_SMEM = 7 * A_TILE_BYTES /*K V Q0 Q1 dO P dS*/ + 2 * 128 * 4 /*lse2, D*/ + 1024 + 256;
+
+struct AttnBwdItem {
+  int kv_row0;    // token index of the sequence start
+  int len;        // sequence length
+  int k_tile;     // key tile j
+  int kv_head;
+};
+
+struct AttnBwdArgs {
+  const AttnBwdItem* items;
+  int H, Hkv, T;
+  float scale_log2;           // log2(e) / sqrt(D)
+  float scale;                // 1 / sqrt(D)
+  const float* lse;           // [H, T] natural log
+  const float* Dq;            // [H, T]
+  float* dq_acc;              // [T, H * 128] fp32
+  __nv_bfloat16* dK;          // [T, Hkv * 128]
+  __nv_bfloat16* dV;
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(384, 1)
+    k_attn_bwd(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+               const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapdO,
+               const AttnBwdArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024a(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + A_TILE_BYTES;
+  uint8_t* sQ = sV + A_TILE_BYTES;             // [2]
+  uint8_t* sdO = sQ + 2 * A_TILE_BYTES;
+  uint8_t* sP = sdO + A_TILE_BYTES;            // P^T  [key rows][query cols], K-major SW128
+  uint8_t* sdS = sP + A_TILE_BYTES;            // dS^T [key rows][query cols]
+  float* s_lse = reinterpret_cast<float*>(sdS + A_TILE_BYTES);   // [128] lse * log2(e)
+  float* s_D = s_lse + 128;                                      // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_D + 128);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;      // [2]
+  uint64_t* q_empty = bars + 3;     // [2]
+  uint64_t* do_full = bars + 5;
+  uint64_t* do_empty = bars + 6;
+  uint64_t* s_full = bars + 7;      // S^T and dP^T of the iteration in TMEM
+  uint64_t* p_full = bars + 8;      // P^T / dS^T in smem (128 arrivals)
+  uint64_t* pds_empty = bars + 9;   // the MMAs reading P^T / dS^T are done
+  uint64_t* dq_full = bars + 10;
+  uint64_t* dq_empty = bars + 11;   // (128 arrivals)
+  uint64_t* fin = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const AttnBwdItem it = args.items[blockIdx.x];
+  const int nt = (it.len + A_TILE - 1) / A_TILE;
+  const int nq = nt - it.k_tile;                     // query tiles i = j .. nt-1
+  const int G = args.H / args.Hkv;
+  const int niter = nq * G;                          // (head of the group, query tile)
+  const int j = it.k_tile;
+
+  if (warp == 0 && lane == 0)
+    tma_prefetch(&mapQ), tma_prefetch(&mapK), tma_prefetch(&mapV), tma_prefetch(&mapdO);
+  if (warp == 1 && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&q_full[s], 1), mbar_init(&q_empty[s], 1);
+    mbar_init(do_full, 1), mbar_init(do_empty, 1);
+    mbar_init(s_full, 1), mbar_init(p_full, 128), mbar_init(pds_empty, 1);
+    mbar_init(dq_full, 1), mbar_init(dq_empty, 128), mbar_init(fin, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto R = [&](int t) { return tmem + (uint32_t)(t & 1) * 128u; };
+  const uint32_t tdV = tmem + 256, tdK = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      const int krow = it.kv_row0 + j * A_TILE;
+      mbar_expect_tx(kv_full, 2 * A_TILE_BYTES);
+      tma_load_2d(sK, &mapK, kv_full, it.kv_head * 128, krow);
+      tma_load_2d(sK + A_BOX, &mapK, kv_full, it.kv_head * 128 + 64, krow);
+      tma_load_2d(sV, &mapV, kv_full, it.kv_head * 128, krow);
+      tma_load_2d(sV + A_BOX, &mapV, kv_full, it.kv_head * 128 + 64, krow);
+      for (int t = 0; t < niter; ++t) {
+        const int h = it.kv_head * G + t / nq, i = j + t % nq;
+        const int qrow = it.kv_row0 + i * A_TILE;
+        const int qb = t & 1;
+        mbar_wait(&q_empty[qb], ((t >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], A_TILE_BYTES);
+        uint8_t* q = sQ + qb * A_TILE_BYTES;
+        tma_load_2d(q, &mapQ, &q_full[qb], h * 128, qrow);
+        tma_load_2d(q + A_BOX, &mapQ, &q_full[qb], h * 128 + 64, qrow);
+        mbar_wait(do_empty, (t & 1) ^ 1);
+        mbar_expect_tx(do_full, A_TILE_BYTES);
+        tma_load_2d(sdO, &mapdO, do_full, h * 128, qrow);
+        tma_load_2d(sdO + A_BOX, &mapdO, do_full, h * 128 + 64, qrow);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t id_kk = idesc_bf16(128, 128, false, false);   // S^T, dP^T: both K-major
+      const uint32_t id_kn = idesc_bf16(128, 128, false, true);    // dV, dK: A K-major, B MN-major
+      const uint32_t id_nn = idesc_bf16(128, 128, true, true);     // dQ: A MN-major, B MN-major
+      const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV), do0 = smem_u32(sdO);
+      const uint32_t p0 = smem_u32(sP), ds0 = smem_u32(sdS);
+      mbar_wait(kv_full, 0);
+      for (int t = 0; t < niter; ++t) {
+        const int qb = t & 1;
+        const uint32_t q0 = smem_u32(sQ + qb * A_TILE_BYTES);
+        mbar_wait(&q_full[qb], (t >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {   // S^T = K Q^T  (K = head dim)
+          const uint32_t off = (kk >> 2) * A_BOX + (kk & 3) * 32;
+          mma_bf16(R(t), sdesc_sw128(k0 + off, 16, 1024), sdesc_sw128(q0 + off, 16, 1024), id_kk, kk ? 1u : 0u);
+        }
+        mbar_wait(do_full, t & 1);
+        if (t >= 1) mbar_wait(dq_empty, (t - 1) & 1);   // R[(t+1)&1] held dQ_{t-1}
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {   // dP^T = V dO^T
+          const uint32_t off = (kk >> 2) * A_BOX + (kk & 3) * 32;
+          mma_bf16(R(t + 1), sdesc_sw128(v0 + off, 16, 1024), sdesc_sw128(do0 + off, 16, 1024), id_kk,
+                   kk ? 1u : 0u);
+        }
+        mma_commit(s_full);
+        mbar_wait(p_full, t & 1);   // P^T, dS^T written; S^T, dP^T consumed
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {   // dV += P^T dO  (K = queries)
+          const uint32_t aoff = (kk >> 2) * A_BOX + (kk & 3) * 32;
+          mma_bf16(tdV, sdesc_sw128(p0 + aoff, 16, 1024), sdesc_sw128(do0 + kk * 2048, A_BOX, 1024), id_kn,
+                   (t | kk) ? 1u : 0u);
+        }
+        mma_commit(do_empty);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {   // dK += dS^T Q
+          const uint32_t aoff = (kk >> 2) * A_BOX + (kk & 3) * 32;
+          mma_bf16(tdK, sdesc_sw128(ds0 + aoff, 16, 1024), sdesc_sw128(q0 + kk * 2048, A_BOX, 1024), id_kn,
+                   (t | kk) ? 1u : 0u);
+        }
+        mma_commit(&q_empty[qb]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)     // dQ_t = dS K  (M = queries, K = keys)
+          mma_bf16(R(t), sdesc_sw128(ds0 + kk * 2048, A_BOX, 1024), sdesc_sw128(k0 + kk * 2048, A_BOX, 1024),
+                   id_nn, kk ? 1u : 0u);
+        mma_commit(dq_full);
+        mma_commit(pds_empty);
+      }
+      mma_commit(fin);
+    }
+  } else if (warp >= 4 && warp < 8) {  // ---------------- P^T / dS^T: one key row per thread
+    const int kr = (warp - 4) * 32 + lane;               // key row of the tile
+    const int kpos = j * A_TILE + kr;                    // position in the sequence
+    const uint32_t trow = ((warp - 4) * 32u) << 16;
+    for (int t = 0; t < niter; ++t) {
+      const int h = it.kv_head * G + t / nq, i = j + t % nq;
+      const int qpos0 = i * A_TILE;
+      {   // the tile's lse (log2 units) and Dq, one query row per thread
+        const int qp = qpos0 + kr;
+        const size_t tok = (size_t)it.kv_row0 + qp;
+        const bool ok = qp < it.len;
+        s_lse[kr] = ok ? __ldg(args.lse + (size_t)h * args.T + tok) * 1.4426950408889634f : 0.0f;
+        s_D[kr] = ok ? __ldg(args.Dq + (size_t)h * args.T + tok) : 0.0f;
+      }
+      named_bar(1, 128);
+      mbar_wait(s_full, t & 1);
+      if (t >= 1) mbar_wait(pds_empty, (t - 1) & 1);     // the previous P^T / dS^T were read
+      tc_fence_after();
+      // masks only where a tile can hold masked pairs: the diagonal and the sequence tail
+      const bool need_mask = (i == j) || (qpos0 + A_TILE > it.len);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float sv[32], dp[32];
+        tmem_ld32(R(t) + trow + c * 32, sv);
+        tmem_ld32(R(t + 1) + trow + c * 32, dp);
+        float p[32], ds[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int q = c * 32 + e;
+          const float pv = ex2(fmaf(sv[e], args.scale_log2, -s_lse[q]));
+          const bool ok = !need_mask || (kpos <= qpos0 + q && qpos0 + q < it.len);
+          p[e] = ok ? pv : 0.0f;
+          ds[e] = p[e] * (dp[e] - s_D[q]);
+        }
+        const int sw = (c & 1) * 4;
+        uint8_t* prow = sP + (c >> 1) * A_BOX + kr * 128;
+        uint8_t* drow = sdS + (c >> 1) * A_BOX + kr * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ch = ((sw + u) ^ (kr & 7)) << 4;
+          uint4 w;
+          w.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
+          w.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
+          w.z = pack_bf16x2(p[u * 8 + 4], p[u * 8 + 5]);
+          w.w = pack_bf16x2(p[u * 8 + 6], p[u * 8 + 7]);
+          *reinterpret_cast<uint4*>(prow + ch) = w;
+          w.x = pack_bf16x2(ds[u * 8 + 0], ds[u * 8 + 1]);
+          w.y = pack_bf16x2(ds[u * 8 + 2], ds[u * 8 + 3]);
+          w.z = pack_bf16x2(ds[u * 8 + 4], ds[u * 8 + 5]);
+          w.w = pack_bf16x2(ds[u * 8 + 6], ds[u * 8 + 7]);
+          *reinterpret_cast<uint4*>(drow + ch) = w;
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();   // P^T / dS^T visible to the tensor core
+      mbar_arrive(p_full);
+      named_bar(1, 128);          // every thread is done with s_lse / s_D of this tile
+    }
+    // dK, dV of the key tile (complete: every query head of the kv group went through them)
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const bool kvalid = kpos < it.len;
+    const size_t tok = (size_t)it.kv_row0 + kpos;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      __nv_bfloat16* base = which ? args.dK : args.dV;
+      const float mul = which ? args.scale : 1.0f;
+      uint4* dst = reinterpret_cast<uint4*>(base + tok * (size_t)(args.Hkv * 128) + it.kv_head * 128);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32((which ? tdK : tdV) + trow + c * 32, v);   // warp-collective
+        if (kvalid) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack_bf16x2(v[u * 8 + 0] * mul, v[u * 8 + 1] * mul);
+            w.y = pack_bf16x2(v[u * 8 + 2] * mul, v[u * 8 + 3] * mul);
+            w.z = pack_bf16x2(v[u * 8 + 4] * mul, v[u * 8 + 5] * mul);
+            w.w = pack_bf16x2(v[u * 8 + 6] * mul, v[u * 8 + 7] * mul);
+            dst[c * 4 + u] = w;
+          }
+        }
+      }
+    }
+  } else if (warp >= 8) {  // ---------------- dQ drain: one query row per thread
+    const int qr = (warp - 8) * 32 + lane;
+    const uint32_t trow = ((warp - 8) * 32u) << 16;
+    for (int t = 0; t < niter; ++t) {
+      const int h = it.kv_head * G + t / nq, i = j + t % nq;
+      const int qpos = i * A_TILE + qr;
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+      float* dst = args.dq_acc + ((size_t)it.kv_row0 + qpos) * (size_t)(args.H * 128) + h * 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(R(t) + trow + c * 32, v);
+        if (qpos < it.len) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) red_add_v4(dst + c * 32 + u * 4, v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Dq[h][t] = sum_d dO[t][h][d] O[t][h][d] (fp32), and the dQ accumulator row zeroed: one warp
+// per (token, head), 4 elements per lane.
+__global__ void k_attn_bwd_pre(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ dO,
+                               int T, int H, float* __restrict__ Dq, float* __restrict__ dq_acc) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (long long)T * H) return;
+  const long long t = w / H;
+  const int h = (int)(w % H);
+  const size_t base = (size_t)t * H * 128 + (size_t)h * 128 + lane * 4;
+  const uint2 a = *reinterpret_cast<const uint2*>(O + base);
+  const uint2 b = *reinterpret_cast<const uint2*>(dO + base);
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float s = 0.0f;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(b2[e]);
+    s = fmaf(x.x, y.x, s);
+    s = fmaf(x.y, y.y, s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) Dq[(size_t)h * T + t] = s;
+  *reinterpret_cast<float4*>(dq_acc + base) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// dQ = scale * accumulator, rounded to bf16 (8 elements per thread).
+__global__ void k_attn_bwd_post(const float* __restrict__ acc, long long n8, float scale,
+                                __nv_bfloat16* __restrict__ dQ) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(acc)[2 * i];
+    const float4 b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+    uint4 w;
+    w.x = pack_bf16x2(a.x * scale, a.y * scale);
+    w.y = pack_bf16x2(a.z * scale, a.w * scale);
+    w.z = pack_bf16x2(b.x * scale, b.y * scale);
+    w.w = pack_bf16x2(b.z * scale, b.w * scale);
+    reinterpret_cast<uint4*>(dQ)[i] = w;
+  }
+}
+
 }  // namespace
 }  // namespace lobra
 
@@ -359,5 +695,120 @@ extern "C" lobra_status lobra_attn_fwd(int32_t num_seqs, const int32_t* seq_lens
   count_launch(LOBRA_K_LAYER, st, false);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(LOBRA_ERR_CUDA, "attn: %s", cudaGetErrorString(e));
+  return LOBRA_OK;
+}
+
+namespace {
+size_t attn_bwd_items(int32_t num_seqs, const int32_t* seq_lens, int32_t n_kv_heads) {
+  size_t n = 0;
+  for (int s = 0; s < num_seqs; ++s) n += (size_t)((std::max(seq_lens[s], 0) + A_TILE - 1) / A_TILE) * n_kv_heads;
+  return n;
+}
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+extern "C" size_t lobra_attn_bwd_workspace_bytes(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads,
+                                                 int32_t n_kv_heads) {
+  if (num_seqs < 1 || !seq_lens || n_heads < 1 || n_kv_heads < 1) return 0;
+  long long T = 0;
+  for (int s = 0; s < num_seqs; ++s) T += std::max(seq_lens[s], 0);
+  return align256(std::max<size_t>(256, attn_bwd_items(num_seqs, seq_lens, n_kv_heads) * sizeof(AttnBwdItem))) +
+         align256((size_t)T * n_heads * sizeof(float)) + (size_t)T * n_heads * 128 * sizeof(float);
+}
+
+extern "C" lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens, int32_t n_heads,
+                                       int32_t n_kv_heads, int32_t head_dim, const void* Q, const void* K,
+                                       const void* V, const void* O, const void* dO, const float* lse, void* dQ,
+                                       void* dK, void* dV, void* ws, size_t ws_bytes, lobra_stream_t stream) {
+  clear_error();
+  if (num_seqs < 1 || !seq_lens || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads)
+    return fail(LOBRA_ERR_INPUT, "attn_bwd: need num_seqs >= 1 and n_kv_heads | n_heads");
+  if (head_dim != 128) return fail(LOBRA_ERR_UNSUPPORTED, "attn_bwd: head_dim %d (only 128)", head_dim);
+  if (!Q || !K || !V || !O || !dO || !lse || !dQ || !dK || !dV || !ws)
+    return fail(LOBRA_ERR_INPUT, "attn_bwd: null pointer");
+  if ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(V) |
+       reinterpret_cast<uintptr_t>(O) | reinterpret_cast<uintptr_t>(dO) | reinterpret_cast<uintptr_t>(dQ) |
+       reinterpret_cast<uintptr_t>(dK) | reinterpret_cast<uintptr_t>(dV) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    return fail(LOBRA_ERR_INPUT, "attn_bwd: pointers must be 16-byte aligned");
+  if (ws_bytes < lobra_attn_bwd_workspace_bytes(num_seqs, seq_lens, n_heads, n_kv_heads))
+    return fail(LOBRA_ERR_INPUT, "attn_bwd: workspace too small");
+  // work items (sequence, key tile, kv head), most query tiles first
+  std::vector<AttnBwdItem> items;
+  long long T = 0;
+  for (int s = 0; s < num_seqs; ++s) {
+    if (seq_lens[s] < 0) return fail(LOBRA_ERR_INPUT, "attn_bwd: negative length");
+    const int nt = (seq_lens[s] + A_TILE - 1) / A_TILE;
+    for (int j = 0; j < nt; ++j)
+      for (int h = 0; h < n_kv_heads; ++h) items.push_back({(int)T, seq_lens[s], j, h});
+    T += seq_lens[s];
+  }
+  if (T > (1LL << 31) - 1) return fail(LOBRA_ERR_INPUT, "attn_bwd: too many tokens");
+  if (items.empty()) return LOBRA_OK;
+  std::stable_sort(items.begin(), items.end(), [](const AttnBwdItem& a, const AttnBwdItem& b) {
+    const int na = (a.len + A_TILE - 1) / A_TILE - a.k_tile, nb = (b.len + A_TILE - 1) / A_TILE - b.k_tile;
+    return na > nb;
+  });
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const size_t items_bytes = align256(std::max<size_t>(256, attn_bwd_items(num_seqs, seq_lens, n_kv_heads) *
+                                                                 sizeof(AttnBwdItem)));
+  float* Dq = reinterpret_cast<float*>(w + items_bytes);
+  float* acc = reinterpret_cast<float*>(w + items_bytes + align256((size_t)T * n_heads * sizeof(float)));
+  static void* pinned = nullptr;
+  static size_t pinned_bytes = 0;
+  static cudaEvent_t done = nullptr;
+  const size_t bytes = items.size() * sizeof(AttnBwdItem);
+  if (!done && cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
+    return fail(LOBRA_ERR_CUDA, "attn_bwd: event creation failed");
+  cudaEventSynchronize(done);
+  if (pinned_bytes < bytes) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned_bytes = std::max<size_t>(bytes, 1 << 16);
+    if (cudaMallocHost(&pinned, pinned_bytes) != cudaSuccess) {
+      pinned = nullptr, pinned_bytes = 0;
+      return fail(LOBRA_ERR_CUDA, "attn_bwd: pinned allocation failed");
+    }
+  }
+  memcpy(pinned, items.data(), bytes);
+  if (cudaMemcpyAsync(ws, pinned, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(LOBRA_ERR_CUDA, "attn_bwd: metadata upload failed");
+  cudaEventRecord(done, st);
+  CUtensorMap mQ, mK, mV, mdO;
+  lobra_status s;
+  if ((s = make_tensor_map_2d(&mQ, Q, (uint64_t)n_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_tensor_map_2d(&mK, K, (uint64_t)n_kv_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_tensor_map_2d(&mV, V, (uint64_t)n_kv_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;
+  if ((s = make_tensor_map_2d(&mdO, dO, (uint64_t)n_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;
+  AttnBwdArgs a;
+  a.items = reinterpret_cast<const AttnBwdItem*>(ws);
+  a.H = n_heads, a.Hkv = n_kv_heads, a.T = (int)T;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
+  a.scale = 1.0f / sqrtf((float)head_dim);
+  a.lse = lse;
+  a.Dq = Dq;
+  a.dq_acc = acc;
+  a.dK = static_cast<__nv_bfloat16*>(dK);
+  a.dV = static_cast<__nv_bfloat16*>(dV);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
+    init = true;
+  }
+  const long long warps = T * n_heads;
+  count_launch(LOBRA_K_LAYER, st, true);
+  k_attn_bwd_pre<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(O),
+                                                                       static_cast<const __nv_bfloat16*>(dO),
+                                                                       (int)T, n_heads, Dq, acc);
+  count_launch(LOBRA_K_LAYER, st, false);
+  count_launch(LOBRA_K_LAYER, st, true);
+  k_attn_bwd<<<(unsigned)items.size(), 384, B_SMEM, st>>>(mQ, mK, mV, mdO, a);
+  count_launch(LOBRA_K_LAYER, st, false);
+  const long long n8 = T * n_heads * 128 / 8;
+  count_launch(LOBRA_K_LAYER, st, true);
+  k_attn_bwd_post<<<(unsigned)std::min<long long>((n8 + 255) / 256, 148 * 16), 256, 0, st>>>(
+      acc, n8, a.scale, static_cast<__nv_bfloat16*>(dQ));
+  count_launch(LOBRA_K_LAYER, st, false);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LOBRA_ERR_CUDA, "attn_bwd: %s", cudaGetErrorString(e));
   return LOBRA_OK;
 }

@@ -74,3 +74,57 @@ def test_attn_fwd_agrees_with_flash_attention():
     f = lambda x: x.float().cpu().numpy().astype(np.float64)
     assert O.max_rel_err(f(o), f(o2)) <= 1e-2
     assert float((lse - lse2).abs().max()) <= 1e-3
+
+
+# ------------------------------------------------------------------ backward (lobra_attn_bwd)
+# P and dS are rounded to bf16 before the tcgen05 products (as FlashAttention does), dQ/dK/dV
+# once more on output; the north-star bf16 tolerance 2e-2 (max-norm relative, per tensor).
+def _attn_bwd_case(torch, lens, H, Hkv, seed):
+    from paper_2509_01193_b200 import _lib
+    T = sum(lens)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    q = torch.randn(T, H, 128, generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, generator=g, device="cuda").to(torch.bfloat16)
+    dO = torch.randn(T, H, 128, generator=g, device="cuda").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    lse = torch.empty(H, T, device="cuda")
+    ws = torch.empty(_lib.lobra_attn_workspace_bytes(lens, H), dtype=torch.uint8, device="cuda")
+    _lib.lobra_attn_fwd(lens, q, k, v, o, lse, ws)
+    dq = torch.full_like(q, float("nan"))
+    dk = torch.full_like(k, float("nan"))
+    dv = torch.full_like(v, float("nan"))
+    wsb = torch.empty(_lib.lobra_attn_bwd_workspace_bytes(lens, H, Hkv), dtype=torch.uint8, device="cuda")
+    _lib.lobra_attn_bwd(lens, q, k, v, o, dO, lse, dq, dk, dv, wsb)
+    torch.cuda.synchronize()
+    return q, k, v, o, dO, lse, dq, dk, dv
+
+
+@pytest.mark.parametrize("lens,H,Hkv", [([1, 300, 57, 129, 200, 33], 4, 2), ([128, 256, 384], 2, 2),
+                                        ([1000, 17, 520], 4, 1), ([5], 1, 1)])
+def test_attn_bwd_matches_oracle(lens, H, Hkv):
+    torch = _torch()
+    q, k, v, o, dO, lse, dq, dk, dv = _attn_bwd_case(torch, lens, H, Hkv, seed=sum(lens) * 3 + H)
+    f = lambda x: x.float().cpu().numpy().astype(np.float64)
+    _, Ps = Dd.attention(f(q), f(k), f(v), lens)
+    rq, rk, rv = Dd.attention_bwd(f(dO), f(q), f(k), f(v), Ps, lens)
+    errs = {"dq": O.max_rel_err(f(dq), rq), "dk": O.max_rel_err(f(dk), rk), "dv": O.max_rel_err(f(dv), rv)}
+    assert all(e <= 2e-2 for e in errs.values()), errs
+
+
+def test_attn_bwd_agrees_with_flash_attention():
+    torch = _torch()
+    fa = pytest.importorskip("flash_attn.flash_attn_interface")
+    lens = [4096, 1500, 33, 2700]
+    H = 8
+    q, k, v, o, dO, lse, dq, dk, dv = _attn_bwd_case(torch, lens, H, H, seed=11)
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    dq2, dk2, dv2 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    fa._flash_attn_varlen_backward(dO, q, k, v, o, lse, dq2, dk2, dv2, cu, cu, max(lens), max(lens), 0.0,
+                                   1 / math.sqrt(128), True, -1, -1, 0.0, None, True)
+    torch.cuda.synchronize()
+    f = lambda x: x.float().cpu().numpy().astype(np.float64)
+    errs = {"dq": O.max_rel_err(f(dq), f(dq2)), "dk": O.max_rel_err(f(dk), f(dk2)),
+            "dv": O.max_rel_err(f(dv), f(dv2))}
+    assert all(e <= 2e-2 for e in errs.values()), errs

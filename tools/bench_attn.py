@@ -1,5 +1,6 @@
-"""Attention forward (varlen causal, D = 128) device time: own tcgen05 kernel vs cuDNN ragged
-SDPA vs FlashAttention-2 (run under gpurun).  Causal FLOPs = 2 * 2 * sum(L^2)/2 * H * D."""
+"""Attention forward and backward (varlen causal, D = 128) device time: own tcgen05 kernels vs
+cuDNN ragged SDPA vs FlashAttention-2 (run under gpurun).  Causal FLOPs: forward
+2 * 2 * sum(L^2)/2 * H * D, backward 2.5x that (five matmuls of the same size)."""
 import json
 import math
 import os
@@ -41,8 +42,13 @@ def main():
         res = {}
         for be in ("lobra", "cudnn", "flash_attn"):
             a = make_attention(be, H, 128, "cuda", n_kv_heads=Hkv)
-            ms = timeit(lambda: a.forward(q, k, v, np.array(lens, np.int32)))
-            res[be] = {"ms": ms, "TFLOPs": flops / ms / 1e9}
+            ln = np.array(lens, np.int32)
+            ms = timeit(lambda: a.forward(q, k, v, ln))
+            o, lse, ctx = a.forward(q, k, v, ln)
+            dO = torch.randn(T, H, 128, generator=g, device="cuda").to(torch.bfloat16)
+            dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            msb = timeit(lambda: a.backward(dO, q, k, v, o, lse, ctx, dq, dk, dv))
+            res[be] = {"ms": ms, "TFLOPs": flops / ms / 1e9, "bwd_ms": msb, "bwd_TFLOPs": 2.5 * flops / msb / 1e9}
         out[name] = res
         print(name, json.dumps(res), flush=True)
     print(json.dumps(out))
