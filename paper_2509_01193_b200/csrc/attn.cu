@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -193,9 +195,15 @@ __global__ void __launch_bounds__(256, 1)
           if (!(qvalid && kpos <= qpos && kpos < it.len)) sv[e] = -INFINITY;
         }
       }
-      float mx = -INFINITY;
+      // row max and (below) row sum as 8 independent chains: one softmax warp per SM
+      // sub-partition has no other warp to hide a 128-long dependent chain behind
+      float mx8[8];
 #pragma unroll
-      for (int e = 0; e < 128; ++e) mx = fmaxf(mx, sv[e]);
+      for (int u = 0; u < 8; ++u) mx8[u] = sv[u];
+#pragma unroll
+      for (int e = 8; e < 128; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], sv[e]);
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= args.scale_log2;                                  // scale > 0: max commutes
       // the previous P V is complete (O quiescent, P buffer free) before P_j is written
       if (j >= 1) {
@@ -219,14 +227,14 @@ __global__ void __launch_bounds__(256, 1)
       }
       l *= alpha;
       m = m_new;
-      float sum = 0.0f;
+      float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float p[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           p[e] = ex2(fmaf(sv[c * 32 + e], args.scale_log2, -m));   // masked: ex2(-inf) = 0
-          sum += p[e];
+          sum8[e & 7] += p[e];
         }
         uint8_t* atom = sP + (c >> 1) * A_BOX + r * 128;     // 64 keys per 128-byte swizzle atom row
 #pragma unroll
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(256, 1)
           *reinterpret_cast<uint4*>(atom + ((chunk ^ (r & 7)) << 4)) = w;
         }
       }
-      l += sum;
+      l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
       tc_fence_before();
       fence_proxy_async_smem();   // P stores visible to the tensor core
       mbar_arrive(p_full);
@@ -291,8 +299,9 @@ __global__ void __launch_bounds__(256, 1)
 //   warp 0      TMA producer: K_j, V_j once; Q_i (2 stages) and dO_i per iteration
 //   warp 1      MMA issuer
 //   warp 2      TMEM allocator (512 columns: R0, R1, dV, dK)
-//   warps 4-7   P^T / dS^T (one key row per thread), final dK / dV epilogue
-//   warps 8-11  dQ drain (one query row per thread): TMEM -> red.global.add.v4.f32
+//   warps 4-11  P^T / dS^T (a key row and 64 query columns per thread: two warps per TMEM
+//               lane group), the dQ drain (TMEM -> red.global.add.v4.f32 into an fp32
+//               accumulator) and the final dK / dV epilogue
 // TMEM roles alternate per iteration t: S^T -> R[t&1], dP^T -> R[(t+1)&1], dQ -> R[t&1], so
 // the next S^T is computed while dQ_t drains.
 // =====================================================================================
@@ -315,14 +324,48 @@ struct AttnBwdArgs {
   float* dq_acc;              // [T, H * 128] fp32
   __nv_bfloat16* dK;          // [T, Hkv * 128]
   __nv_bfloat16* dV;
+  unsigned long long* ts;     // tracing (LOBRA_TRACE_ATTN): per-phase clock64 stamps of CTA 0, else null
 };
+// trace slots: [event][iteration], event-major, 64 iterations
+#define ATTN_TS(ev, t) \
+  do { if (args.ts && blockIdx.x == 0 && (t) < 64) args.ts[(ev) * 64 + (t)] = clock64(); } while (0)
 
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
+}
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
+                                                  int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// P^T (or dS^T) chunk c (32 query columns) of key row kr: 32 bf16 values as four 16-byte
+// shared stores into the 128-byte-swizzled K-major row of the buffer at shared address `buf`.
+__device__ __forceinline__ void store_row_chunk(uint32_t buf, int kr, int c, const uint32_t* pk) {
+  const uint32_t row = buf + (c >> 1) * A_BOX + kr * 128;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t ch = (uint32_t)((((c & 1) * 4) + u) ^ (kr & 7)) << 4;
+    sts128(row + ch, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
+  }
 }
 
 __global__ void __launch_bounds__(384, 1)
@@ -345,13 +388,16 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* q_empty = bars + 3;     // [2]
   uint64_t* do_full = bars + 5;
   uint64_t* do_empty = bars + 6;
-  uint64_t* s_full = bars + 7;      // S^T and dP^T of the iteration in TMEM
-  uint64_t* p_full = bars + 8;      // P^T / dS^T in smem (128 arrivals)
-  uint64_t* pds_empty = bars + 9;   // the MMAs reading P^T / dS^T are done
-  uint64_t* dq_full = bars + 10;
-  uint64_t* dq_empty = bars + 11;   // (128 arrivals)
-  uint64_t* fin = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* s_full = bars + 7;      // S^T in TMEM
+  uint64_t* dp_full = bars + 8;     // dP^T in TMEM
+  uint64_t* p_full = bars + 9;      // P^T in smem (256 arrivals)
+  uint64_t* ds_full = bars + 10;    // dS^T in smem (256 arrivals)
+  uint64_t* p_empty = bars + 11;    // dV (the reader of P^T) done
+  uint64_t* ds_empty = bars + 12;   // dK, dQ (the readers of dS^T) done
+  uint64_t* dq_full = bars + 13;
+  uint64_t* dq_empty = bars + 14;   // dQ_t read out of TMEM (256 arrivals)
+  uint64_t* fin = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const AttnBwdItem it = args.items[blockIdx.x];
@@ -367,8 +413,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&q_full[s], 1), mbar_init(&q_empty[s], 1);
     mbar_init(do_full, 1), mbar_init(do_empty, 1);
-    mbar_init(s_full, 1), mbar_init(p_full, 128), mbar_init(pds_empty, 1);
-    mbar_init(dq_full, 1), mbar_init(dq_empty, 128), mbar_init(fin, 1);
+    mbar_init(s_full, 1), mbar_init(dp_full, 1), mbar_init(p_full, 256), mbar_init(ds_full, 256);
+    mbar_init(p_empty, 1), mbar_init(ds_empty, 1), mbar_init(dq_full, 1), mbar_init(dq_empty, 256);
+    mbar_init(fin, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -404,34 +451,47 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
+      // Order per tile t: [S^T_t issued at the end of t-1] dP^T_t, (P^T) dV_t, (dS^T) S^T_{t+1},
+      // dK_t, dQ_t -- the next tile's S^T runs while the softmax warps write dS^T, and their
+      // P^T phase of t+1 overlaps dK_t / dQ_t.
       const uint32_t id_kk = idesc_bf16(128, 128, false, false);   // S^T, dP^T: both K-major
       const uint32_t id_kn = idesc_bf16(128, 128, false, true);    // dV, dK: A K-major, B MN-major
       const uint32_t id_nn = idesc_bf16(128, 128, true, true);     // dQ: A MN-major, B MN-major
       const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV), do0 = smem_u32(sdO);
       const uint32_t p0 = smem_u32(sP), ds0 = smem_u32(sdS);
-      mbar_wait(kv_full, 0);
-      for (int t = 0; t < niter; ++t) {
+      auto issue_s = [&](int t) {   // S^T_t = K Q_t^T into R[t&1]
         const int qb = t & 1;
         const uint32_t q0 = smem_u32(sQ + qb * A_TILE_BYTES);
         mbar_wait(&q_full[qb], (t >> 1) & 1);
         tc_fence_after();
+        ATTN_TS(0, t);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {   // S^T = K Q^T  (K = head dim)
+        for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * A_BOX + (kk & 3) * 32;
           mma_bf16(R(t), sdesc_sw128(k0 + off, 16, 1024), sdesc_sw128(q0 + off, 16, 1024), id_kk, kk ? 1u : 0u);
         }
+        mma_commit(s_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int t = 0; t < niter; ++t) {
+        const int qb = t & 1;
+        const uint32_t q0 = smem_u32(sQ + qb * A_TILE_BYTES);
         mbar_wait(do_full, t & 1);
+        ATTN_TS(8, t);
         if (t >= 1) mbar_wait(dq_empty, (t - 1) & 1);   // R[(t+1)&1] held dQ_{t-1}
         tc_fence_after();
+        ATTN_TS(1, t);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // dP^T = V dO^T
           const uint32_t off = (kk >> 2) * A_BOX + (kk & 3) * 32;
           mma_bf16(R(t + 1), sdesc_sw128(v0 + off, 16, 1024), sdesc_sw128(do0 + off, 16, 1024), id_kk,
                    kk ? 1u : 0u);
         }
-        mma_commit(s_full);
-        mbar_wait(p_full, t & 1);   // P^T, dS^T written; S^T, dP^T consumed
+        mma_commit(dp_full);
+        mbar_wait(p_full, t & 1);   // P^T in smem
         tc_fence_after();
+        ATTN_TS(2, t);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // dV += P^T dO  (K = queries)
           const uint32_t aoff = (kk >> 2) * A_BOX + (kk & 3) * 32;
@@ -439,6 +499,11 @@ __global__ void __launch_bounds__(384, 1)
                    (t | kk) ? 1u : 0u);
         }
         mma_commit(do_empty);
+        mma_commit(p_empty);
+        mbar_wait(ds_full, t & 1);  // dS^T in smem; S^T_t and dP^T_t consumed
+        tc_fence_after();
+        ATTN_TS(3, t);
+        if (t + 1 < niter) issue_s(t + 1);   // R[(t+1)&1] (dP^T_t) is free
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // dK += dS^T Q
           const uint32_t aoff = (kk >> 2) * A_BOX + (kk & 3) * 32;
@@ -447,86 +512,182 @@ __global__ void __launch_bounds__(384, 1)
         }
         mma_commit(&q_empty[qb]);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)     // dQ_t = dS K  (M = queries, K = keys)
+        for (int kk = 0; kk < 8; ++kk)     // dQ_t = dS K  (M = queries, K = keys) into R[t&1]
           mma_bf16(R(t), sdesc_sw128(ds0 + kk * 2048, A_BOX, 1024), sdesc_sw128(k0 + kk * 2048, A_BOX, 1024),
                    id_nn, kk ? 1u : 0u);
         mma_commit(dq_full);
-        mma_commit(pds_empty);
+        mma_commit(ds_empty);
       }
       mma_commit(fin);
     }
-  } else if (warp >= 4 && warp < 8) {  // ---------------- P^T / dS^T: one key row per thread
-    const int kr = (warp - 4) * 32 + lane;               // key row of the tile
+  } else if (warp >= 4) {  // ---------------- P^T / dS^T and the dQ drain: 8 warps
+    // Two warps per TMEM lane group (two per SM sub-partition): warp w handles key rows
+    // (lanes) 32 (w % 4) .. +31 and query columns (P^T, dS^T) or head-dim columns (dQ)
+    // 64 hw .. +63, hw = (w - 4) / 4.
+    const int g4 = warp & 3, hw = (warp - 4) >> 2;
+    const int kr = g4 * 32 + lane;                       // key row of the tile (TMEM lane)
     const int kpos = j * A_TILE + kr;                    // position in the sequence
-    const uint32_t trow = ((warp - 4) * 32u) << 16;
-    for (int t = 0; t < niter; ++t) {
+    const int tid = (warp - 4) * 32 + lane;              // 0 .. 255
+    const uint32_t trow = (g4 * 32u) << 16;
+    const uint32_t sP_a = smem_u32(sP), sdS_a = smem_u32(sdS), lse_a = smem_u32(s_lse), D_a = smem_u32(s_D);
+    // the tile's lse (log2 units) and Dq, one query row per thread of the first 128; loaded
+    // one iteration ahead (their global latency overlaps the wait for the next S^T)
+    auto load_ld = [&](int t, float& l2, float& dd) {
       const int h = it.kv_head * G + t / nq, i = j + t % nq;
-      const int qpos0 = i * A_TILE;
-      {   // the tile's lse (log2 units) and Dq, one query row per thread
-        const int qp = qpos0 + kr;
-        const size_t tok = (size_t)it.kv_row0 + qp;
-        const bool ok = qp < it.len;
-        s_lse[kr] = ok ? __ldg(args.lse + (size_t)h * args.T + tok) * 1.4426950408889634f : 0.0f;
-        s_D[kr] = ok ? __ldg(args.Dq + (size_t)h * args.T + tok) : 0.0f;
-      }
-      named_bar(1, 128);
-      mbar_wait(s_full, t & 1);
-      if (t >= 1) mbar_wait(pds_empty, (t - 1) & 1);     // the previous P^T / dS^T were read
+      const int qp = i * A_TILE + tid;
+      const size_t tok = (size_t)it.kv_row0 + qp;
+      const bool ok = tid < 128 && qp < it.len;
+      l2 = ok ? __ldg(args.lse + (size_t)h * args.T + tok) * 1.4426950408889634f : 0.0f;
+      dd = ok ? __ldg(args.Dq + (size_t)h * args.T + tok) : 0.0f;
+    };
+    // dQ_t, in two steps.  (a) TMEM -> registers (64 head-dim columns of one query row per
+    // thread), the TMEM region released at once (dq_empty: dP^T_{t+1} may overwrite it).
+    // (b) after the next dS^T phase, through the P^T buffer (free once dV has read it): each
+    // 64-column half is written row-major (256-byte rows, 16-byte chunks XOR-swizzled by
+    // row), read back two rows per warp instruction and added into the fp32 accumulator with
+    // red.global.add.v4 -- 256 contiguous bytes per row and instruction instead of 32
+    // scattered rows (8x fewer L2 requests).
+    float dqv[64];
+    auto drain_tmem = [&](int t) {
+      mbar_wait(dq_full, t & 1);
       tc_fence_after();
-      // masks only where a tile can hold masked pairs: the diagonal and the sequence tail
-      const bool need_mask = (i == j) || (qpos0 + A_TILE > it.len);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float sv[32], dp[32];
-        tmem_ld32(R(t) + trow + c * 32, sv);
-        tmem_ld32(R(t + 1) + trow + c * 32, dp);
-        float p[32], ds[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int q = c * 32 + e;
-          const float pv = ex2(fmaf(sv[e], args.scale_log2, -s_lse[q]));
-          const bool ok = !need_mask || (kpos <= qpos0 + q && qpos0 + q < it.len);
-          p[e] = ok ? pv : 0.0f;
-          ds[e] = p[e] * (dp[e] - s_D[q]);
-        }
-        const int sw = (c & 1) * 4;
-        uint8_t* prow = sP + (c >> 1) * A_BOX + kr * 128;
-        uint8_t* drow = sdS + (c >> 1) * A_BOX + kr * 128;
+      for (int c = 0; c < 2; ++c) {
+        float w[32];
+        tmem_ld32(R(t) + trow + hw * 64 + c * 32, w);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int ch = ((sw + u) ^ (kr & 7)) << 4;
-          uint4 w;
-          w.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
-          w.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
-          w.z = pack_bf16x2(p[u * 8 + 4], p[u * 8 + 5]);
-          w.w = pack_bf16x2(p[u * 8 + 6], p[u * 8 + 7]);
-          *reinterpret_cast<uint4*>(prow + ch) = w;
-          w.x = pack_bf16x2(ds[u * 8 + 0], ds[u * 8 + 1]);
-          w.y = pack_bf16x2(ds[u * 8 + 2], ds[u * 8 + 3]);
-          w.z = pack_bf16x2(ds[u * 8 + 4], ds[u * 8 + 5]);
-          w.w = pack_bf16x2(ds[u * 8 + 6], ds[u * 8 + 7]);
-          *reinterpret_cast<uint4*>(drow + ch) = w;
-        }
+        for (int e = 0; e < 32; ++e) dqv[c * 32 + e] = w[e];
       }
       tc_fence_before();
-      fence_proxy_async_smem();   // P^T / dS^T visible to the tensor core
+      mbar_arrive(dq_empty);
+      if (tid == 0) ATTN_TS(9, t + 1);
+    };
+    auto drain_red = [&](int t) {   // P^T buffer must be free (dV of the current tile done)
+      const int h = it.kv_head * G + t / nq, i = j + t % nq;
+      const int q0 = i * A_TILE;
+      const int rw = tid >> 5;                                       // 16 rows per warp
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        if (hw == half) {
+          const uint32_t row = sP_a + kr * 256;                      // kr = the query row here
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            sts128(row + ((c ^ (kr & 15)) << 4), __float_as_uint(dqv[c * 4]), __float_as_uint(dqv[c * 4 + 1]),
+                   __float_as_uint(dqv[c * 4 + 2]), __float_as_uint(dqv[c * 4 + 3]));
+        }
+        named_bar(1, 256);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = rw * 16 + u * 2 + (lane >> 4), c = lane & 15;
+          const float4 x = lds128f(sP_a + r * 256 + ((c ^ (r & 15)) << 4));
+          if (q0 + r < it.len)
+            red_add_v4(args.dq_acc + ((size_t)it.kv_row0 + q0 + r) * (size_t)(args.H * 128) + h * 128 + half * 64 +
+                           c * 4, x.x, x.y, x.z, x.w);
+        }
+        named_bar(1, 256);
+      }
+      if (tid == 0) ATTN_TS(10, t + 1);
+    };
+    float nl2, ndd;
+    load_ld(0, nl2, ndd);
+    for (int t = 0; t < niter; ++t) {
+      const int i = j + t % nq;
+      const int qpos0 = i * A_TILE;
+      if (tid < 128) s_lse[tid] = nl2, s_D[tid] = ndd;
+      if (t + 1 < niter) load_ld(t + 1, nl2, ndd);
+      named_bar(1, 256);
+      mbar_wait(s_full, t & 1);
+      if (t >= 1) mbar_wait(p_empty, (t - 1) & 1);       // dV_{t-1} has read P^T
+      tc_fence_after();
+      if (tid == 0) ATTN_TS(4, t);
+      // masks only where a tile can hold masked pairs: the diagonal and the sequence tail
+      // (warp-uniform; the common unmasked tiles run without the compare / select work)
+      const bool need_mask = (i == j) || (qpos0 + A_TILE > it.len);
+      const int lim = need_mask ? min(it.len - qpos0, A_TILE) : A_TILE;   // valid query columns
+      const int diag = kpos - qpos0;                       // masked: q < diag
+      uint32_t pk[32];   // P^T row half, bf16 pairs (the rounded values the dV product uses)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cq = hw * 2 + c;                         // 32-column chunk of the 128
+        float sv[32];
+        tmem_ld32(R(t) + trow + cq * 32, sv);
+        float l2[32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 x = lds128f(lse_a + (cq * 32 + u * 4) * 4);
+          l2[u * 4] = x.x, l2[u * 4 + 1] = x.y, l2[u * 4 + 2] = x.z, l2[u * 4 + 3] = x.w;
+        }
+        if (!need_mask) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            pk[(c * 32 + e) >> 1] = pack_bf16x2(ex2(fmaf(sv[e], args.scale_log2, -l2[e])),
+                                                ex2(fmaf(sv[e + 1], args.scale_log2, -l2[e + 1])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int q = cq * 32 + e;
+            float p0v = ex2(fmaf(sv[e], args.scale_log2, -l2[e]));
+            float p1v = ex2(fmaf(sv[e + 1], args.scale_log2, -l2[e + 1]));
+            if (q < diag || q >= lim) p0v = 0.0f;
+            if (q + 1 < diag || q + 1 >= lim) p1v = 0.0f;
+            pk[(c * 32 + e) >> 1] = pack_bf16x2(p0v, p1v);
+          }
+        }
+        store_row_chunk(sP_a, kr, cq, pk + c * 16);
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();   // P^T visible to the tensor core
       mbar_arrive(p_full);
-      named_bar(1, 128);          // every thread is done with s_lse / s_D of this tile
+      if (tid == 0) ATTN_TS(5, t);
+      if (t >= 1) drain_tmem(t - 1);   // dQ_{t-1} (issued before S^T_t, so complete by now)
+      mbar_wait(dp_full, t & 1);
+      if (t >= 1) mbar_wait(ds_empty, (t - 1) & 1);      // dK_{t-1}, dQ_{t-1} have read dS^T
+      tc_fence_after();
+      if (tid == 0) ATTN_TS(6, t);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int cq = hw * 2 + c;
+        float dp[32];
+        tmem_ld32(R(t + 1) + trow + cq * 32, dp);
+        uint32_t dk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 dd = lds128f(D_a + (cq * 32 + e) * 4);
+          const float2 pa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[(c * 32 + e) >> 1]));
+          const float2 pb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[((c * 32 + e) >> 1) + 1]));
+          dk[e >> 1] = pack_bf16x2(pa.x * (dp[e] - dd.x), pa.y * (dp[e + 1] - dd.y));
+          dk[(e >> 1) + 1] = pack_bf16x2(pb.x * (dp[e + 2] - dd.z), pb.y * (dp[e + 3] - dd.w));
+        }
+        store_row_chunk(sdS_a, kr, cq, dk);
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();   // dS^T visible to the tensor core
+      mbar_arrive(ds_full);
+      if (tid == 0) ATTN_TS(7, t);
+      if (t >= 1) {
+        mbar_wait(p_empty, t & 1);   // dV_t has read P^T: its buffer stages dQ_{t-1}
+        drain_red(t - 1);
+      } else {
+        named_bar(1, 256);           // every thread is done with s_lse / s_D of this tile
+      }
     }
-    // dK, dV of the key tile (complete: every query head of the kv group went through them)
+    // the last dQ: its TMEM read, then the staging (dV of the last tile is done: fin)
+    drain_tmem(niter - 1);
     mbar_wait(fin, 0);
     tc_fence_after();
+    drain_red(niter - 1);
+    // dK, dV of the key tile (complete: every query head of the kv group went through them)
     const bool kvalid = kpos < it.len;
     const size_t tok = (size_t)it.kv_row0 + kpos;
 #pragma unroll 1
     for (int which = 0; which < 2; ++which) {
       __nv_bfloat16* base = which ? args.dK : args.dV;
       const float mul = which ? args.scale : 1.0f;
-      uint4* dst = reinterpret_cast<uint4*>(base + tok * (size_t)(args.Hkv * 128) + it.kv_head * 128);
+      uint4* dst = reinterpret_cast<uint4*>(base + tok * (size_t)(args.Hkv * 128) + it.kv_head * 128 + hw * 64);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float v[32];
-        tmem_ld32((which ? tdK : tdV) + trow + c * 32, v);   // warp-collective
+        tmem_ld32((which ? tdK : tdV) + trow + hw * 64 + c * 32, v);   // warp-collective
         if (kvalid) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -539,27 +700,6 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       }
-    }
-  } else if (warp >= 8) {  // ---------------- dQ drain: one query row per thread
-    const int qr = (warp - 8) * 32 + lane;
-    const uint32_t trow = ((warp - 8) * 32u) << 16;
-    for (int t = 0; t < niter; ++t) {
-      const int h = it.kv_head * G + t / nq, i = j + t % nq;
-      const int qpos = i * A_TILE + qr;
-      mbar_wait(dq_full, t & 1);
-      tc_fence_after();
-      float* dst = args.dq_acc + ((size_t)it.kv_row0 + qpos) * (size_t)(args.H * 128) + h * 128;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(R(t) + trow + c * 32, v);
-        if (qpos < it.len) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) red_add_v4(dst + c * 32 + u * 4, v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(dq_empty);
     }
   }
   tc_fence_before();
@@ -789,6 +929,14 @@ extern "C" lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens
   a.dq_acc = acc;
   a.dK = static_cast<__nv_bfloat16*>(dK);
   a.dV = static_cast<__nv_bfloat16*>(dV);
+  a.ts = nullptr;
+  static const char* trace = getenv("LOBRA_TRACE_ATTN");
+  static unsigned long long* d_ts = nullptr;
+  if (trace) {
+    if (!d_ts && cudaMalloc(&d_ts, 16 * 64 * sizeof(unsigned long long)) != cudaSuccess) d_ts = nullptr;
+    if (d_ts) cudaMemsetAsync(d_ts, 0, 16 * 64 * sizeof(unsigned long long), st);
+    a.ts = d_ts;
+  }
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
@@ -803,6 +951,19 @@ extern "C" lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens
   count_launch(LOBRA_K_LAYER, st, true);
   k_attn_bwd<<<(unsigned)items.size(), 384, B_SMEM, st>>>(mQ, mK, mV, mdO, a);
   count_launch(LOBRA_K_LAYER, st, false);
+  if (a.ts) {   // tracing only: synchronous dump of CTA 0's phase stamps
+    std::vector<unsigned long long> h(16 * 64);
+    cudaMemcpyAsync(h.data(), a.ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* f = fopen(trace, "a")) {
+      fprintf(f, "bwd niter_cta0=%d\n", 0);
+      for (int e = 0; e < 16; ++e) {
+        for (int t = 0; t < 64; ++t) fprintf(f, "%llu ", h[e * 64 + t]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   const long long n8 = T * n_heads * 128 / 8;
   count_launch(LOBRA_K_LAYER, st, true);
   k_attn_bwd_post<<<(unsigned)std::min<long long>((n8 + 255) / 256, 148 * 16), 256, 0, st>>>(

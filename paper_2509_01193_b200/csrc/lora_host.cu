@@ -625,9 +625,9 @@ Layout layout(const lobra_problem* prob, const Plan& P) {
 }
 
 lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128) {
+                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128, bool f32 = false) {
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   static int promo = -1;   // LOBRA_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B (default)
@@ -638,7 +638,8 @@ lobra_status make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
   }
   const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+  CUresult r = g_encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                         : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
@@ -701,6 +702,13 @@ lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inne
   lobra_status s = get_ctx(&ctx);
   if (s != LOBRA_OK) return s;
   return make_map(map, ptr, inner, outer, box_inner, box_outer);
+}
+lobra_status make_tensor_map_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+                                    uint32_t box_inner, uint32_t box_outer) {
+  DevCtx* ctx = nullptr;
+  lobra_status s = get_ctx(&ctx);
+  if (s != LOBRA_OK) return s;
+  return make_map(map, ptr, inner, outer, box_inner, box_outer, 128, true);
 }
 }  // namespace lobra
 

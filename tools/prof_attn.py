@@ -1,4 +1,4 @@
-"""One launch of the own attention forward on the long-sequence case (for ncu)."""
+"""Launches of the own attention forward and backward on the long-sequence case (for ncu)."""
 import os
 import sys
 
@@ -17,4 +17,11 @@ lse = torch.empty(H, T, device="cuda")
 ws = torch.empty(_lib.lobra_attn_workspace_bytes(lens, H), dtype=torch.uint8, device="cuda")
 for _ in range(2):
     _lib.lobra_attn_fwd(np.array(lens, np.int32), q, k, v, o, lse, ws)
+torch.cuda.synchronize()
+# ... and one backward launch (lobra_attn_bwd) on the same case
+dO = torch.randn(T, H, 128, generator=g, device="cuda").to(torch.bfloat16)
+dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+wsb = torch.empty(_lib.lobra_attn_bwd_workspace_bytes(lens, H, H), dtype=torch.uint8, device="cuda")
+for _ in range(2):
+    _lib.lobra_attn_bwd(np.array(lens, np.int32), q, k, v, o, dO, lse, dq, dk, dv, wsb)
 torch.cuda.synchronize()
