@@ -43,8 +43,8 @@ def _torch():
 
 
 def _backend(name):
-    mod = "cudnn" if name == "cudnn" else "flash_attn"     # "lobra": own forward + FA2 backward
-    pytest.importorskip(mod)
+    if name != "lobra":                                     # "lobra": own tcgen05 forward + backward
+        pytest.importorskip(name)
     return name
 
 

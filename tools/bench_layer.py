@@ -83,7 +83,7 @@ def main():
             "config": {"workload": "C2 (T=16384, 4 tasks r=16, lengths <= 4096)", "layer": f"llama2-{args.model}" + (" (GQA 64/8 heads, TP1)" if args.model == "70b" else ""),
                        "attention": {"cudnn": "cuDNN 9 ragged SDPA (library)",
                                      "flash_attn": "flash_attn 2.8 varlen (library)",
-                                     "lobra": "own tcgen05 forward + flash_attn 2.8 varlen backward"}[args.attn]},
+                                     "lobra": "own tcgen05 forward + backward (csrc/attn.cu)"}[args.attn]},
             "algorithmic_tflops": fl["total"] / (ms / 1e3) / 1e12,
             "flops_share": {k: fl[k] / fl["total"] for k in ("proj", "lora", "attn")},
             "ms_by_class": cls, "ms_attention_and_glue": ms - ours}
