@@ -3,12 +3,14 @@
 // fp32 softmax, grouped-query heads.
 //
 // One CTA per work item (sequence, 128-query tile, head), items ordered longest first.
-//   warp 0   TMA producer: the Q tile once, then K_j / V_j tiles (2-stage ring)
+//   warp 0   TMA producer: the Q tile once, then K_j and V_j tiles in separate 2-stage rings
+//            (K_j is released as soon as S_j is done, V_j after P_j V_j), K_j ahead of V_{j-1}
 //   warp 1   MMA issuer:   S_j = Q K_j^T into TMEM (double buffered, 2 x 128 columns) while
-//                          the softmax works on S_{j-1}; O_j = P_j V_j into a TMEM scratch
+//                          the softmax works on S_{j-1}; O += P_j V_j (P double buffered)
 //   warp 2   TMEM allocator
-//   warps 4-7 softmax, one query row per thread: row max of S_j (masked: key <= query and
-//            inside the sequence), p = exp2(s log2e / sqrt(D) - m), P_j to shared memory
+//   warps 4-11 softmax, a query row and 64 key columns per thread (two warps per TMEM lane
+//            group, row maxima exchanged through shared memory): row max of S_j (masked:
+//            key <= query and inside the sequence), p = exp2(s log2e / sqrt(D) - m), P_j to shared memory
 //            in the 128-byte-swizzled K-major layout of the next MMA's A operand, running
 //            sum l; O accumulates in TMEM (lazy rescale when the row max grows by > 2^8)
 // Outputs: O (bf16, same layout as Q) and LSE [H, T] fp32 (natural log; FlashAttention's
@@ -38,8 +40,9 @@ using namespace ptx;
 constexpr int A_TILE = 128;                    // queries / keys per tile
 constexpr int A_BOX = 128 * 64 * 2;            // one 64-column box of a 128-row tile: 16 KB
 constexpr int A_TILE_BYTES = 2 * A_BOX;        // 128 x 128 bf16
-constexpr int A_KV_STAGES = 2;
-constexpr int A_SMEM = A_TILE_BYTES /*Q*/ + A_KV_STAGES * 2 * A_TILE_BYTES /*K,V*/ + A_TILE_BYTES /*P*/ + 1024 + 256;
+// Q | K[2] | V[2] | P[2] | barriers | row-max exchange [2 halves][128] (the row-sum exchange
+// at the end reuses it)
+constexpr int A_SMEM = 7 * A_TILE_BYTES + 1024 + 256 + 2 * 128 * 4;
 
 struct AttnItem {
   int q_row0;     // token index of the tile's first query
@@ -55,35 +58,54 @@ struct AttnArgs {
   float scale_log2;           // log2(e) / sqrt(D)
   __nv_bfloat16* O;           // [T, H * 128]
   float* lse;                 // [H, T]
+  unsigned long long* ts;     // tracing (LOBRA_TRACE_ATTN): per-phase clock64 stamps of CTA 0, else null
 };
-
+// trace slots: [event][iteration], event-major, 64 iterations
+#define ATTN_TS(ev, t) \
+  do { if (args.ts && blockIdx.x == 0 && (t) < 64) args.ts[(ev) * 64 + (t)] = clock64(); } while (0)
 __device__ __forceinline__ float ex2(float x) {   // MUFU.EX2; ex2(-inf) = 0
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ uint8_t* align1024a(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     k_attn_fwd(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                const __grid_constant__ CUtensorMap mapV, const AttnArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024a(smem_raw);
   uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + A_TILE_BYTES;                       // stage s: K at +s*2T, V at +s*2T+T
-  uint8_t* sP = sKV + A_KV_STAGES * 2 * A_TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + A_TILE_BYTES);
+  uint8_t* sK = sQ + A_TILE_BYTES;                        // [2]
+  uint8_t* sV = sK + 2 * A_TILE_BYTES;                    // [2]
+  uint8_t* sP = sV + 2 * A_TILE_BYTES;                    // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * A_TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;     // [2]
-  uint64_t* kv_empty = bars + 3;    // [2]
-  uint64_t* s_full = bars + 5;      // [2]
-  uint64_t* s_empty = bars + 7;     // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_full = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* k_full = bars + 1;      // [2]
+  uint64_t* k_empty = bars + 3;     // [2]  S_j done: K_j free (long before V_j)
+  uint64_t* v_full = bars + 5;      // [2]
+  uint64_t* v_empty = bars + 7;     // [2]
+  uint64_t* s_full = bars + 9;      // [2]
+  uint64_t* s_empty = bars + 11;    // [2]
+  uint64_t* p_full = bars + 13;
+  uint64_t* pv_done = bars + 14;    // [2]  P_j V_j done (per P buffer: completes every 2nd tile)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  float* xmax = reinterpret_cast<float*>(bars + 32);     // [2 halves][128 rows]
+  float* xsum = xmax;                                     // [2 halves][128 rows], after the loop
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const AttnItem it = args.items[blockIdx.x];
@@ -94,11 +116,12 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 128);
+      mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 256);
+      mbar_init(&pv_done[s], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
+    mbar_init(p_full, 256);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -106,35 +129,44 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // completion of P_j V_j: its P buffer's barrier, phase j >> 1
+  auto wait_pv = [&](int j) { mbar_wait(&pv_done[j & 1], (j >> 1) & 1); };
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer: K_j ahead of V_{j-1}
       mbar_expect_tx(q_full, A_TILE_BYTES);
       tma_load_2d(sQ, &mapQ, q_full, it.head * 128, it.q_row0);
       tma_load_2d(sQ + A_BOX, &mapQ, q_full, it.head * 128 + 64, it.q_row0);
-      for (int j = 0; j < nkv; ++j) {
+      auto load = [&](int j, bool v) {
         const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[s], 2 * A_TILE_BYTES);
-        uint8_t* k = sKV + s * 2 * A_TILE_BYTES;
+        uint64_t* full = v ? &v_full[s] : &k_full[s];
+        mbar_wait(v ? &v_empty[s] : &k_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(full, A_TILE_BYTES);
+        uint8_t* dst = (v ? sV : sK) + s * A_TILE_BYTES;
         const int row = it.kv_row0 + j * A_TILE;
-        tma_load_2d(k, &mapK, &kv_full[s], hk * 128, row);
-        tma_load_2d(k + A_BOX, &mapK, &kv_full[s], hk * 128 + 64, row);
-        tma_load_2d(k + A_TILE_BYTES, &mapV, &kv_full[s], hk * 128, row);
-        tma_load_2d(k + A_TILE_BYTES + A_BOX, &mapV, &kv_full[s], hk * 128 + 64, row);
+        tma_load_2d(dst, v ? &mapV : &mapK, full, hk * 128, row);
+        tma_load_2d(dst + A_BOX, v ? &mapV : &mapK, full, hk * 128 + 64, row);
+      };
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          load(j, false);
+          ATTN_TS(0, j);
+        }
+        if (j >= 1) load(j - 1, true);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t id_s = idesc_bf16(128, 128, false, false);   // S: Q, K both K-major
       const uint32_t id_o = idesc_bf16(128, 128, false, true);    // O: P K-major, V MN-major
-      const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
+      const uint32_t q0 = smem_u32(sQ);
       auto issue_s = [&](int j) {
         const int s = j & 1;
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        mbar_wait(&k_full[s], (j >> 1) & 1);
         mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k0 = smem_u32(sKV + s * 2 * A_TILE_BYTES);
+        ATTN_TS(1, j);
+        const uint32_t k0 = smem_u32(sK + s * A_TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // K = head_dim 128: 2 swizzle atoms x 4 steps of 16
           const uint32_t off = (kk >> 2) * A_BOX + (kk & 3) * 32;
@@ -142,32 +174,42 @@ __global__ void __launch_bounds__(256, 1)
                    kk ? 1u : 0u);
         }
         mma_commit(&s_full[s]);
+        mma_commit(&k_empty[s]);
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) issue_s(j + 1);
+        const int s = j & 1;
         mbar_wait(p_full, j & 1);   // P_j written (and O rescaled if the softmax had to)
+        mbar_wait(&v_full[s], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t v0 = smem_u32(sKV + (j & 1) * 2 * A_TILE_BYTES + A_TILE_BYTES);
+        ATTN_TS(2, j);
+        const uint32_t v0 = smem_u32(sV + s * A_TILE_BYTES), p0 = smem_u32(sP + s * A_TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // K = 128 keys: P (K-major) x V (MN-major)
           const uint32_t poff = (kk >> 2) * A_BOX + (kk & 3) * 32;
           mma_bf16(tmem + 256, sdesc_sw128(p0 + poff, 16, 1024), sdesc_sw128(v0 + kk * 2048, A_BOX, 1024), id_o,
                    (j | kk) ? 1u : 0u);   // O accumulates in TMEM over the key tiles
         }
-        mma_commit(o_full);
-        mma_commit(&kv_empty[j & 1]);
+        mma_commit(&pv_done[s]);
+        mma_commit(&v_empty[s]);
       }
     }
-  } else if (warp >= 4) {  // ---------------- softmax / epilogue: one query row per thread
+  } else if (warp >= 4) {  // ---------------- softmax / epilogue: 8 warps
+    // Two warps per TMEM lane group (two per SM sub-partition, so the exp / max / pack chains
+    // of one hide the latencies of the other): warp w owns query row r = 32 (w % 4) + lane
+    // and key columns (and O columns) 64 hw .. +63, hw = (w - 4) / 4; the two halves of a row
+    // exchange their maxima through shared memory once per key tile.
     // O accumulates in TMEM; P is computed against a reference max m that is raised (and O, l
     // rescaled in place) only when a tile's max exceeds it by more than 8 (log2 units, i.e.
     // p <= 256): the final O / l is exact either way.
-    const int r = (warp - 4) * 32 + lane;
+    const int g4 = warp & 3, hw = (warp - 4) >> 2;
+    const int r = g4 * 32 + lane;
     const int qpos = it.q_tile * A_TILE + r;               // position inside the sequence
     const bool qvalid = qpos < it.len;
-    const uint32_t trow = ((warp - 4) * 32u) << 16;
+    const uint32_t trow = (g4 * 32u) << 16;
+    const uint32_t sP_a = smem_u32(sP);
     // invalid rows (past the sequence end in its last tile) keep m = 0 and only see -inf
     float m = qvalid ? -INFINITY : 0.0f, l = 0.0f;
     // per-element masks only where a tile can hold masked keys: the diagonal tile and the
@@ -177,91 +219,91 @@ __global__ void __launch_bounds__(256, 1)
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      const int kbase = j * A_TILE;
-      float sv[128];
+      if (r == 0 && hw == 0) ATTN_TS(3, j);
+      const int kbase = j * A_TILE + hw * 64;
+      float sv[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float v[32];
-        tmem_ld32(tmem + trow + sb * 128 + c * 32, v);
+        tmem_ld32(tmem + trow + sb * 128 + hw * 64 + c * 32, v);
 #pragma unroll
         for (int e = 0; e < 32; ++e) sv[c * 32 + e] = v[e];
       }
       tc_fence_before();
       mbar_arrive(&s_empty[sb]);                             // S buffer free for S_{j+2}
-      if (j == nkv - 1 || tail_rows || kbase + A_TILE > it.len) {   // warp-uniform
+      if (j == nkv - 1 || tail_rows || j * A_TILE + A_TILE > it.len) {   // warp-uniform
 #pragma unroll
-        for (int e = 0; e < 128; ++e) {
+        for (int e = 0; e < 64; ++e) {
           const int kpos = kbase + e;
           if (!(qvalid && kpos <= qpos && kpos < it.len)) sv[e] = -INFINITY;
         }
       }
-      // row max and (below) row sum as 8 independent chains: one softmax warp per SM
-      // sub-partition has no other warp to hide a 128-long dependent chain behind
+      // row max of this half as 8 independent chains, then the other half's through smem
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = sv[u];
 #pragma unroll
-      for (int e = 8; e < 128; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], sv[e]);
+      for (int e = 8; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], sv[e]);
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      mx *= args.scale_log2;                                  // scale > 0: max commutes
-      // the previous P V is complete (O quiescent, P buffer free) before P_j is written
-      if (j >= 1) {
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-      }
-      // raise the reference max where needed; the TMEM rescale is warp-collective
-      // (tcgen05.ld / st are .sync.aligned): every lane takes part, alpha = 1 where unchanged
+      xmax[hw * 128 + r] = mx;
+      named_bar(1, 256);
+      mx = fmaxf(mx, xmax[(hw ^ 1) * 128 + r]) * args.scale_log2;   // scale > 0: max commutes
+      named_bar(1, 256);   // both halves read before the next tile's maxima are written
+      if (r == 0 && hw == 0) ATTN_TS(4, j);
+      if (r == 0 && hw == 0) ATTN_TS(5, j);
+      // raise the reference max where needed (both halves decide identically); the TMEM
+      // rescale is warp-collective (tcgen05.ld / st are .sync.aligned): every lane takes
+      // part, alpha = 1 where unchanged
       const bool raise = qvalid && (j == 0 || mx > m + 8.0f);
       const float m_new = raise ? fmaxf(m, mx) : m;
       const float alpha = (raise && j >= 1) ? ex2(m - m_new) : 1.0f;
       if (j >= 1 && __any_sync(0xffffffffu, raise)) {
+        wait_pv(j - 1);   // O quiescent before it is rescaled in place
+        tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           float v[32];
-          tmem_ld32(tmem + trow + 256 + c * 32, v);
+          tmem_ld32(tmem + trow + 256 + hw * 64 + c * 32, v);
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] *= alpha;
-          tmem_st32(tmem + trow + 256 + c * 32, v);
+          tmem_st32(tmem + trow + 256 + hw * 64 + c * 32, v);
         }
       }
       l *= alpha;
       m = m_new;
       float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (j >= 2) wait_pv(j - 2);   // P buffer j & 1 was last read by P_{j-2} V_{j-2}
+      const uint32_t row = sP_a + (j & 1) * A_TILE_BYTES + hw * A_BOX + r * 128;   // 64 keys = one atom row
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float p[32];
+      for (int u = 0; u < 8; ++u) {                         // 16-byte chunk u of the row
+        float p[8];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          p[e] = ex2(fmaf(sv[c * 32 + e], args.scale_log2, -m));   // masked: ex2(-inf) = 0
-          sum8[e & 7] += p[e];
+        for (int e = 0; e < 8; ++e) {
+          p[e] = ex2(fmaf(sv[u * 8 + e], args.scale_log2, -m));   // masked: ex2(-inf) = 0
+          sum8[e] += p[e];
         }
-        uint8_t* atom = sP + (c >> 1) * A_BOX + r * 128;     // 64 keys per 128-byte swizzle atom row
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;                 // 16-byte chunk within the 128-byte row
-          uint4 w;
-          w.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
-          w.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
-          w.z = pack_bf16x2(p[u * 8 + 4], p[u * 8 + 5]);
-          w.w = pack_bf16x2(p[u * 8 + 6], p[u * 8 + 7]);
-          *reinterpret_cast<uint4*>(atom + ((chunk ^ (r & 7)) << 4)) = w;
-        }
+        sts128(row + ((u ^ (r & 7)) << 4), pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]),
+               pack_bf16x2(p[4], p[5]), pack_bf16x2(p[6], p[7]));
       }
       l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
       tc_fence_before();
       fence_proxy_async_smem();   // P stores visible to the tensor core
       mbar_arrive(p_full);
+      if (r == 0 && hw == 0) ATTN_TS(6, j);
     }
-    mbar_wait(o_full, (nkv - 1) & 1);
+    xsum[hw * 128 + r] = l;
+    named_bar(1, 256);
+    l += xsum[(hw ^ 1) * 128 + r];
+    wait_pv(nkv - 1);               // the last P V (and with it every earlier one) is done
     tc_fence_after();
     const float inv = qvalid ? 1.0f / l : 0.0f;
     const size_t tok = (size_t)it.q_row0 + r;
-    uint4* dst = reinterpret_cast<uint4*>(args.O + tok * (size_t)(args.H * 128) + it.head * 128);
+    uint4* dst = reinterpret_cast<uint4*>(args.O + tok * (size_t)(args.H * 128) + it.head * 128 + hw * 64);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       float v[32];
-      tmem_ld32(tmem + trow + 256 + c * 32, v);            // warp-collective: every lane
+      tmem_ld32(tmem + trow + 256 + hw * 64 + c * 32, v);   // warp-collective: every lane
       if (qvalid) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -274,7 +316,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-    if (qvalid) args.lse[(size_t)it.head * args.T + tok] = (m + log2f(l)) * 0.69314718055994531f;
+    if (qvalid && hw == 0) args.lse[(size_t)it.head * args.T + tok] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -326,21 +368,7 @@ struct AttnBwdArgs {
   __nv_bfloat16* dV;
   unsigned long long* ts;     // tracing (LOBRA_TRACE_ATTN): per-phase clock64 stamps of CTA 0, else null
 };
-// trace slots: [event][iteration], event-major, 64 iterations
-#define ATTN_TS(ev, t) \
-  do { if (args.ts && blockIdx.x == 0 && (t) < 64) args.ts[(ev) * 64 + (t)] = clock64(); } while (0)
 
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-__device__ __forceinline__ float4 lds128f(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -825,14 +853,35 @@ extern "C" lobra_status lobra_attn_fwd(int32_t num_seqs, const int32_t* seq_lens
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
+  a.ts = nullptr;
+  static const char* trace = getenv("LOBRA_TRACE_ATTN");
+  static unsigned long long* d_ts = nullptr;
+  if (trace) {
+    if (!d_ts && cudaMalloc(&d_ts, 16 * 64 * sizeof(unsigned long long)) != cudaSuccess) d_ts = nullptr;
+    if (d_ts) cudaMemsetAsync(d_ts, 0, 16 * 64 * sizeof(unsigned long long), st);
+    a.ts = d_ts;
+  }
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, A_SMEM);
     init = true;
   }
   count_launch(LOBRA_K_LAYER, st, true);
-  k_attn_fwd<<<a.nitems, 256, A_SMEM, st>>>(mQ, mK, mV, a);
+  k_attn_fwd<<<a.nitems, 384, A_SMEM, st>>>(mQ, mK, mV, a);
   count_launch(LOBRA_K_LAYER, st, false);
+  if (a.ts) {   // tracing only: synchronous dump of CTA 0's phase stamps
+    std::vector<unsigned long long> h(16 * 64);
+    cudaMemcpyAsync(h.data(), a.ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* f = fopen(trace, "a")) {
+      fprintf(f, "fwd\n");
+      for (int e = 0; e < 16; ++e) {
+        for (int t = 0; t < 64; ++t) fprintf(f, "%llu ", h[e * 64 + t]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(LOBRA_ERR_CUDA, "attn: %s", cudaGetErrorString(e));
   return LOBRA_OK;
@@ -956,7 +1005,7 @@ extern "C" lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens
     cudaMemcpyAsync(h.data(), a.ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     if (FILE* f = fopen(trace, "a")) {
-      fprintf(f, "bwd niter_cta0=%d\n", 0);
+      fprintf(f, "bwd\n");
       for (int e = 0; e < 16; ++e) {
         for (int t = 0; t < 64; ++t) fprintf(f, "%llu ", h[e * 64 + t]);
         fprintf(f, "\n");
