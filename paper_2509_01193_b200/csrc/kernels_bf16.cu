@@ -1117,6 +1117,7 @@ struct DyArgs {
   int width, nchunks, nitems, n128, qp;
   int hrow, nq, stages, stage_bytes;
   int dbg_dy_only;   // tuning probe (LOBRA_DBG_DY_ONLY=1): stream dY only, skip H / B loads
+  unsigned long long* ts;   // tracing (LOBRA_TRACE_DY): per CTA {start, end, smid} globaltimer, else null
   float* gpart;    // [nslots][nchunks][128][qp]
   float* bpart;    // [segments][4][qp][128]
   Meta meta;
@@ -1159,6 +1160,12 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_launch_dependents();
+  if (args.ts && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    args.ts[blockIdx.x * 3 + 0] = gtimer();
+    args.ts[blockIdx.x * 3 + 2] = smid;
+  }
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -1309,6 +1316,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   __syncthreads();
+  if (args.ts && threadIdx.x == 0) args.ts[blockIdx.x * 3 + 1] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -1781,7 +1789,40 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
     }
     a.dbg_dy_only = dbg;
   }
+  a.ts = nullptr;
+  static const char* trace = getenv("LOBRA_TRACE_DY");
+  static unsigned long long* d_ts = nullptr;
+  if (trace && meta.ndyunits > 0) {
+    if (!d_ts && cudaMalloc(&d_ts, 3 * 4096 * sizeof(unsigned long long)) != cudaSuccess) d_ts = nullptr;
+    if (d_ts && meta.ndycta <= 4096) a.ts = d_ts;
+  }
   if (meta.ndyunits > 0) launch_k(k_dypass, dim3(meta.ndycta), dim3(256), Y_SMEM, st, mapDY, mapH, mapBt, a);
+  if (a.ts) {   // tracing only: per-CTA times with the CTA's entry ranges, one JSON line per launch
+    std::vector<unsigned long long> h(3 * meta.ndycta);
+    std::vector<int> off(meta.ndycta + 1), ut(meta.ndyunits), u0(meta.ndyunits), u1(meta.ndyunits),
+        uc(meta.ndyunits), rk(meta.ntasks);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), a.ts, h.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(off.data(), meta.dy_cta_off, off.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ut.data(), meta.dy_unit_task, ut.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(u0.data(), meta.dy_unit_s0, u0.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(u1.data(), meta.dy_unit_s1, u1.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(uc.data(), meta.dy_unit_chunk, uc.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rk.data(), meta.ranks, rk.size() * 4, cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace, "a")) {
+      fprintf(f, "{\"width\": %d, \"qp\": %d, \"ranks\": [", width, qp);
+      for (int t = 0; t < meta.ntasks; ++t) fprintf(f, "%s%d", t ? ", " : "", rk[t]);
+      fprintf(f, "], \"cta\": [");
+      for (int b = 0; b < meta.ndycta; ++b) {
+        fprintf(f, "%s[%llu, %llu, %llu, [", b ? ", " : "", h[3 * b], h[3 * b + 1], h[3 * b + 2]);
+        for (int u = off[b]; u < off[b + 1]; ++u)
+          fprintf(f, "%s[%d, %d, %d, %d]", u > off[b] ? ", " : "", ut[u], uc[u], u0[u], u1[u]);
+        fprintf(f, "]]");
+      }
+      fprintf(f, "]}\n");
+      fclose(f);
+    }
+  }
   launch_k(k_gfin, dim3(num_sms * 2), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
 }
 
