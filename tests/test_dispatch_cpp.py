@@ -180,6 +180,29 @@ def test_c5_scale_exact_vs_oracle_fixture(case):
     assert dt < 10.0, dt   # measured solve times: profiles/r2_dispatch_solve_times.md
 
 
+@pytest.mark.parametrize("threads", ["1", "3"])
+def test_c5_scale_thread_count_invariant(threads, monkeypatch):
+    """The >= 3-group solver explores subtrees on a thread pool (LOBRA_DISPATCH_THREADS):
+    the answer, including every per-sequence output, is the fixture's for any thread count."""
+    from paper_2509_01193_b200 import _lib
+    cases = [c for c in C5["cases"] if c["name"] in ("G3", "G4")][:2]
+    if not cases:
+        pytest.skip("no C5 fixture")
+    monkeypatch.setenv("LOBRA_DISPATCH_THREADS", threads)
+    for case in cases:
+        groups = [D.Group(*g) for g in case["deployment"]]
+        cost = _c5_cost(groups, C5["cost_unit"])
+        tasks = synth.c3_tasks()
+        wl = synth.sample_batch(tasks, seed=case["seed"], l_max=16384,
+                                per_task=[t.batch_size for t in tasks[:12]] + [64] * 4)
+        got = _lib.lobra_dispatch([g.tp for g in groups], [g.replicas for g in groups],
+                                  [g.max_tokens for g in groups], cost, wl.seq_lens, wl.seq_task,
+                                  C5["grid_step"], C5["grid_max"], C5["R"], 0, chunking=C5["chunking"])
+        assert got["d"].tolist() == case["d"]
+        assert _digest(got["seq_bucket"], got["seq_replica"], got["seq_chunk"], got["pack_order"],
+                       got["replica_cost"]) == case["sha256"]
+
+
 def test_c5_scale_live_oracle_g3():
     """One C5-scale 3-group step against the live oracle (not the fixture)."""
     tasks = synth.c3_tasks()
