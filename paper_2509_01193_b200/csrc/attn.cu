@@ -374,17 +374,6 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
-__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
-                                                  int32_t c1) {
-  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];"
-               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit_and_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-
 // P^T (or dS^T) chunk c (32 query columns) of key row kr: 32 bf16 values as four 16-byte
 // shared stores into the 128-byte-swizzled K-major row of the buffer at shared address `buf`.
 __device__ __forceinline__ void store_row_chunk(uint32_t buf, int kr, int c, const uint32_t* pk) {

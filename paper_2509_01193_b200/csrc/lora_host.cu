@@ -362,29 +362,49 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     std::vector<int> task, s0, s1, chunk, off, cta_off{0};
     int ncta = 1, nch = 1;
   };
-  auto build_dy = [&](int width, int chunk_cols) {
+  // weighted = true (the dY pass): an entry's weight is its measured cost, 5 per 128-column
+  // dY sub-block + 10 fixed (the H ring load and the 128-row G partial written per entry) +
+  // 7 for a task of rank > 32 (wider B_t / H boxes, G and dB partials).  Least-squares fit of
+  // per-CTA times against each CTA's entries (LOBRA_TRACE_DY, tools/trace_dy.py, C3): full
+  // entries 3.0 us, rank > 32 3.65, the 256-column last chunk of width 11008 2.0 / 2.7, plus
+  // 1.5 per segment.  With equal entry counts per CTA the CTA times spread 179-343 us
+  // (11008) and 89-123 us (4096).
+  auto build_dy = [&](int width, int chunk_cols, bool weighted) {
     DyVecs v;
     const int nch = std::max(1, (width + chunk_cols - 1) / chunk_cols);
-    long long W = 0;
-    for (int t = 0; t < G; ++t) W += (long long)(task_slot_off[t + 1] - task_slot_off[t]) * nch;
-    const int ncta = (int)std::max<long long>(1, std::min<long long>(std::max(num_sms, 1), W));
+    const int n128 = (width + 127) / 128;
+    auto weight = [&](int t, int c) -> long long {
+      if (!weighted) return 1;
+      const int nb = std::max(0, std::min(chunk_cols / 128, n128 - c * (chunk_cols / 128)));
+      return 5LL * nb + 10 + (ad->ranks[t] > 32 ? 7 : 0);
+    };
+    long long W = 0, nent = 0;
+    for (int t = 0; t < G; ++t)
+      for (int c = 0; c < nch; ++c) {
+        const long long n_t = task_slot_off[t + 1] - task_slot_off[t];
+        W += n_t * weight(t, c);
+        nent += n_t;
+      }
+    const int ncta = (int)std::max<long long>(1, std::min<long long>(std::max(num_sms, 1), nent));
     v.off.assign((size_t)G * nch + 1, 0);
-    long long e = 0;   // entry index in (task, chunk, slot) order
+    long long e = 0;   // cumulative weight of the entries in (task, chunk, slot) order
     int cta = 0;
     auto cta_end = [&](int c) { return (long long)W * (c + 1) / ncta; };
     for (int t = 0; t < G; ++t) {
       const int k0 = task_slot_off[t], k1 = task_slot_off[t + 1];
       for (int c = 0; c < nch; ++c) {
+        const long long w = std::max<long long>(1, weight(t, c));
         int k = k0;
         while (k < k1) {
           while (cta < ncta - 1 && e >= cta_end(cta)) {
             v.cta_off.push_back((int)v.task.size());
             ++cta;
           }
-          const int take = (int)std::min<long long>(k1 - k, cta_end(cta) - e);
+          const long long room = cta == ncta - 1 ? (long long)(k1 - k) * w : cta_end(cta) - e;
+          const int take = (int)std::min<long long>(k1 - k, std::max<long long>(1, (room + w - 1) / w));
           v.task.push_back(t), v.chunk.push_back(c);
           v.s0.push_back(k), v.s1.push_back(k + take);
-          k += take, e += take;
+          k += take, e += take * w;
         }
         v.off[(size_t)t * nch + c + 1] = (int)v.task.size();
       }
@@ -403,7 +423,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     bool seen = false;
     for (const auto& d : P.sr) seen = seen || d.width == wdt;
     if (seen || wdt <= 0) continue;
-    srv.push_back(build_dy(wdt, 128));
+    srv.push_back(build_dy(wdt, 128, false));
     Plan::DySet ds;
     ds.width = wdt;
     ds.ncta = srv.back().ncta;
@@ -421,7 +441,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
     bool seen = false;
     for (const auto& d : P.dy) seen = seen || d.width == wdt;
     if (seen) continue;
-    dyv.push_back(build_dy(wdt, 512));
+    dyv.push_back(build_dy(wdt, 512, true));
     Plan::DySet ds;
     ds.width = wdt;
     ds.ncta = dyv.back().ncta;
@@ -702,13 +722,6 @@ lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inne
   lobra_status s = get_ctx(&ctx);
   if (s != LOBRA_OK) return s;
   return make_map(map, ptr, inner, outer, box_inner, box_outer);
-}
-lobra_status make_tensor_map_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-                                    uint32_t box_inner, uint32_t box_outer) {
-  DevCtx* ctx = nullptr;
-  lobra_status s = get_ctx(&ctx);
-  if (s != LOBRA_OK) return s;
-  return make_map(map, ptr, inner, outer, box_inner, box_outer, 128, true);
 }
 }  // namespace lobra
 

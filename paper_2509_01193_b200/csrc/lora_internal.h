@@ -129,9 +129,6 @@ void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int 
 // bf16 2D TMA map, 128-byte swizzle (lora_host.cu)
 lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
                                 uint32_t box_inner, uint32_t box_outer);
-// fp32 2D TMA map, 128-byte swizzle (box_inner * 4 <= 128 bytes per row)
-lobra_status make_tensor_map_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-                                    uint32_t box_inner, uint32_t box_outer);
 // Fused GEMM -> TP reduce-scatter (symm.cu): output row r is stored into rank
 // (r / chunk_rows)'s symmetric buffer, slot `rank`, row r % chunk_rows (bf16 [chunk_rows, N]
 // per slot) instead of C (with accumulate, the row of C is added first: C holds the local
