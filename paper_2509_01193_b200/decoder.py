@@ -47,6 +47,28 @@ class DecoderLayer:
         self.g_attn = (1 + 0.1 * torch.randn(self.h, generator=g, device=self.dev)).to(dtype)
         self.g_mlp = (1 + 0.1 * torch.randn(self.h, generator=g, device=self.dev)).to(dtype)
         self.cache = {}
+        self.saved = None
+        self._ctx, self._ctxs = 0, {}
+
+    # ------------------------------------------------------------------ micro-batch contexts
+    def select_context(self, k):
+        """Pipeline schedules (1F1B, pipeline.py) keep several micro-batches in flight: each
+        context k owns its activations (the buffer cache and the saved state of forward) and
+        the projections' saved H_s; the adapter gradients and workspaces are shared."""
+        if k == self._ctx:
+            return
+        L = self.lora
+        self._ctxs[self._ctx] = (self.cache, self.saved, L.group_Hs, [p.Hs for p in L.projs])
+        c = self._ctxs.pop(k, None)
+        if c is None:
+            self.cache, self.saved, L.group_Hs = {}, None, {}
+            for p in L.projs:
+                p.Hs = None
+        else:
+            self.cache, self.saved, L.group_Hs, hs = c
+            for p, h in zip(L.projs, hs):
+                p.Hs = h
+        self._ctx = k
 
     # ------------------------------------------------------------------ buffers
     def _buf(self, name, shape, dtype=torch.bfloat16):
