@@ -241,3 +241,17 @@ def test_uniform_mode_cpp():
     with pytest.raises(_lib.LobraError):
         _lib.lobra_dispatch([1, 2], [2, 1], [2048, 4096], _cost_table([D.Group(1, 2, 2048), D.Group(2, 1, 4096)], 16, 256),
                             lens, tasks, 256, 4096, 8, 2)
+
+
+def test_micro_batches_and_packing_order_hand_worked_cpp():
+    """The C++ steps 9-10 on the hand-worked instance (tests/golden/dispatch_pack_example.json)."""
+    from paper_2509_01193_b200 import _lib
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "dispatch_pack_example.json")))
+    tp, p, M = g["group"]
+    for chunking, key in ((0, "padded"), (1, "packed")):
+        got = _lib.lobra_dispatch([tp], [p], [M], [g["cost"]], g["seq_lens"], g["seq_task"], g["grid_step"],
+                                  g["grid_max"], g["R"], 0, chunking=chunking)
+        assert got["boundaries"].tolist() == g["boundaries"]
+        assert got["d"].ravel().tolist() == g["d"] and got["t_hat"] == g["t_hat"]
+        assert got["seq_chunk"].tolist() == g[key]["seq_chunk"], key
+        assert got["pack_order"].tolist() == g[key]["pack_order"], key

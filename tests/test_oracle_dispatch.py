@@ -256,3 +256,22 @@ def test_chunks_and_packing_order_hand_worked():
     r1 = D.dispatch(groups, cost, lens, tasks, 256, 1024, 2, chunking=1)
     assert r1.seq_chunk.tolist() == [1, 0, 2, 2, 1, 2]
     assert r1.pack_order.tolist() == [1, 0, 1, 0, 0, 2]
+
+
+# --------------------------------------------------------------------------- steps 9-10 pin
+def test_micro_batches_and_packing_order_hand_worked():
+    """Steps 9-10 (padded micro-batches of App. D P:1494-1496 in descending cost; packed
+    next-fit chunks, reading Q6b; task-grouped order inside a chunk, reading Q6) against a
+    hand-worked instance (tests/golden/dispatch_pack_example.json, derivation inside)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "dispatch_pack_example.json")))
+    groups = [D.Group(*g["group"])]
+    for chunking, key in ((0, "padded"), (1, "packed")):
+        res = D.dispatch(groups, [g["cost"]], np.array(g["seq_lens"]), np.array(g["seq_task"]), g["grid_step"],
+                         g["grid_max"], g["R"], mode=0, chunking=chunking)
+        assert list(res.boundaries) == g["boundaries"]
+        assert [int(x) for x in np.asarray(res.d).ravel()] == g["d"]
+        assert int(res.t_hat) == g["t_hat"]
+        assert res.seq_chunk.tolist() == g[key]["seq_chunk"], key
+        assert res.pack_order.tolist() == g[key]["pack_order"], key
