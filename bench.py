@@ -619,13 +619,15 @@ def main():
     clocks = clocks if clocks is not None else {}
     dom_fl = fl_fwd if dom == "gemm_fwd" else fl_bwd
     dom_ms = prof[dom][1]
-    # Peak: the measured BURST cuBLAS figure, always.  The sustained figure (cuBLAS back to
-    # back for 4 s under the 1000 W cap) is lower than what this GEMM reaches under the same
-    # cap, so it would give frac > 1; it is reported beside as `frac_vs_sustained`.
+    # Peak: the task's rule -- the burst figure for a kernel timed alone, the SUSTAINED one
+    # for a kernel timed inside a long step.  The dominant GEMM is timed inside the
+    # multi-second C3 step (the roofline pass below), where the 1000 W cap holds the clock,
+    # so the denominator is MEASURED_PEAKS' sustained cuBLAS throughput (back to back for 4 s
+    # under the same cap); the burst ratio is reported beside as `frac_vs_burst`.
     capped = bool(clocks and "sw_power_cap" in clocks.get("reasons", []))
-    peak_kind = "bf16_tflops"
+    peak_burst = float(peaks["bf16_tflops"])
+    peak_kind = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
     peak_t = float(peaks[peak_kind])
-    peak_sus = float(peaks.get("bf16_tflops_sustained", peak_t))
     achieved = dom_fl / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -638,8 +640,9 @@ def main():
     roofline = {"bound": "tensor", "kernel": f"k_gemm ({dom})", "achieved": achieved, "peak": peak_t,
                 "algorithmic_bytes_per_launch": alg_b,
                 "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": traffic,
-                "peak_source": f"{peak_src} {peak_kind} (burst)" + ("; sw_power_cap was active in the timed region" if capped else ""),
-                "frac_vs_sustained": achieved / peak_sus,
+                "peak_source": f"{peak_src} {peak_kind} (the kernel is timed inside a long step)" +
+                               ("; sw_power_cap was active in the timed region" if capped else ""),
+                "frac_vs_burst": achieved / peak_burst,
                 "share_of_step": dom_ms / ms_local if ms_local > 0 else 0.0,
                 "flops_per_launch": dom_fl / max(prof[dom][0], 1),
                 "ms_per_launch": dom_ms / max(prof[dom][0], 1), "roofline_pass": rf}
