@@ -1,0 +1,5 @@
+set -x
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_lora.py tests/test_gpu_group.py tests/test_gpu_layer_parity.py tests/test_gpu_trainer.py tests/test_gpu_tp70b.py -x -q > gpurun_out/r3g_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r3g_tests.txt
+bash tools/ncu_skinny.sh r3g_c3
+bash tools/ncu_skinny.sh r3g_c2 --workload c2
