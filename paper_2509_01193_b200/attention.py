@@ -1,16 +1,15 @@
-"""Varlen causal attention for the decoder layer, library backends.
+"""Varlen causal attention for the decoder layer.
 
-Attention is not on the north-star path; the layer calls a library for it the way the
-projections would call cuBLAS (our own tcgen05 attention is the planned replacement,
-DESIGN.md §10).  Two backends over the packed layout q, k, v [T, H, D] with per-sequence
-causal masks (block-diagonal over the pack):
+Attention is not on the north-star path; three backends over the packed layout q, k, v
+[T, H, D] with per-sequence causal masks (block-diagonal over the pack):
 
-  * "cudnn": cuDNN 9 frontend SDPA forward / backward on RAGGED tensors (THD layout: the
-    sequences of the pack addressed through ragged offsets, no padding copies); graphs
-    are built once per (batch bucket, max-length bucket) and cached;
-  * "flash_attn": FlashAttention-2 varlen kernels (mma.sync; measured ~3x slower on B200);
+  * "cudnn" (default): cuDNN 9 frontend SDPA forward / backward on RAGGED tensors (THD
+    layout: the sequences of the pack addressed through ragged offsets, no padding copies);
+    graphs are built once per (batch bucket, max-length bucket) and cached -- a library
+    call like cuBLAS, and today the fastest;
   * "lobra": our own tcgen05 kernels, forward (lobra_attn_fwd) and backward
-    (lobra_attn_bwd, recomputation from the forward's LSE), csrc/attn.cu.
+    (lobra_attn_bwd, recomputation from the forward's LSE), csrc/attn.cu;
+  * "flash_attn": FlashAttention-2 varlen kernels (mma.sync; ~3x slower on B200).
 """
 from __future__ import annotations
 

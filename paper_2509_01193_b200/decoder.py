@@ -11,9 +11,10 @@ Public Llama-2 layer (reading Q27; oracle/decoder.py is its fp64 defin
 
 Our kernels (C ABI, liblobra.so): the seven LoRA projections (q/k/v and gate/up as
 projection groups), RMSNorm with the fused residual add / residual-gradient add, RoPE,
-SwiGLU, the last residual add.  Attention: a library call like cuBLAS (attention.py: cuDNN's
-ragged SDPA by default, FlashAttention-2 varlen as the alternative; our own tcgen05
-attention is the next step).  PyTorch only allocates memory.
+SwiGLU, the last residual add.  Attention (attention.py): cuDNN's ragged SDPA by default (a
+library call like cuBLAS; faster than ours today), `attn_backend="lobra"` for our own tcgen05
+forward and backward (csrc/attn.cu), FlashAttention-2 varlen as a further
+alternative.  PyTorch only allocates memory.
 """
 from __future__ import annotations
 
