@@ -952,6 +952,169 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// =====================================================================================
+// Planes shrink (a projection group whose bands exceed the 64-wide slot, e.g. q/k/v with
+// rank-64 tasks): H_s of every projection of the group from ONE pass over X, the adapter
+// operand being the task's np * qp packed rows (MMA N = np * qp, plane p = columns
+// [p qp, (p+1) qp)).  Its adapter slice (24 KB per 64-column K block at np * qp = 192) is
+// bigger than the X block (16 KB), so X and the adapter get separate rings: X 8 deep (128 KB
+// in flight per SM, the amount the single-projection shrink streams at 0.8 of HBM) and the
+// L2-resident adapter 4 deep, the X loads running 4 K blocks ahead of the adapter loads.
+// (In k_shrink's shared stages only 5 x 16 KB of X were in flight: 0.55-0.60 of HBM.)
+// Work item = tile (persistent over tiles), one pass per slot of the tile.
+// =====================================================================================
+constexpr int SP_NX = 8, SP_NV = 4, SP_LEAD = 4;
+
+struct PlanesCursor {   // walks the (tile, slot, K block) steps of one CTA
+  int w, s, s_end, kb, nk, nitems, stride;
+  const Meta* meta;
+  __device__ bool valid() const { return w < nitems; }
+  __device__ void init(const Meta& m, int w0, int stride_, int nk_, int nitems_) {
+    meta = &m, stride = stride_, nk = nk_, nitems = nitems_, kb = 0;
+    for (w = w0; w < nitems; w += stride)
+      if (m.tile_slot_off[w] < m.tile_slot_off[w + 1]) break;
+    if (w < nitems) s = m.tile_slot_off[w], s_end = m.tile_slot_off[w + 1];
+  }
+  __device__ void next() {
+    if (++kb < nk) return;
+    kb = 0;
+    if (++s < s_end) return;
+    for (w += stride; w < nitems; w += stride)
+      if (meta->tile_slot_off[w] < meta->tile_slot_off[w + 1]) break;
+    if (w < nitems) s = meta->tile_slot_off[w], s_end = meta->tile_slot_off[w + 1];
+  }
+};
+
+__global__ void __launch_bounds__(256, 1)
+    k_shrink_planes(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapV,
+                    const ShrinkArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int qv = args.qv, vbox = qv * 128;
+  uint8_t* sX = smem;                                   // [SP_NX][16 KB]
+  uint8_t* sV = sX + SP_NX * R_A_BYTES;                 // [SP_NV][vbox]
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(sV + SP_NV * vbox);
+  uint64_t* xempty = xfull + SP_NX;
+  uint64_t* vfull = xempty + SP_NX;
+  uint64_t* vempty = vfull + SP_NV;
+  uint64_t* tfull = vempty + SP_NV;     // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const Meta& meta = args.meta;
+  const int nk = (args.K + 63) / 64;
+
+  if (warp == 0 && lane == 0) tma_prefetch(&mapZ), tma_prefetch(&mapV);
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < SP_NX; ++i) mbar_init(&xfull[i], 1), mbar_init(&xempty[i], 1);
+    for (int i = 0; i < SP_NV; ++i) mbar_init(&vfull[i], 1), mbar_init(&vempty[i], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&tfull[b], 1), mbar_init(&tempty[b], 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: X of step g + SP_LEAD, then V of step g
+      PlanesCursor cx, cv;
+      cx.init(meta, blockIdx.x, gridDim.x, nk, meta.ntiles);
+      cv.init(meta, blockIdx.x, gridDim.x, nk, meta.ntiles);
+      int gx = 0, gv = 0;
+      auto issue_x = [&]() {
+        const int i = gx % SP_NX;
+        mbar_wait(&xempty[i], ((gx / SP_NX) & 1) ^ 1);
+        mbar_expect_tx(&xfull[i], R_A_BYTES);
+        tma_load_2d(sX + i * R_A_BYTES, &mapZ, &xfull[i], cx.kb * 64, cx.w * kTileM);
+        cx.next();
+        ++gx;
+      };
+      for (int l = 0; l < SP_LEAD && cx.valid(); ++l) issue_x();
+      while (cv.valid()) {
+        if (cx.valid()) issue_x();
+        const int i = gv % SP_NV;
+        mbar_wait(&vempty[i], ((gv / SP_NV) & 1) ^ 1);
+        mbar_expect_tx(&vfull[i], vbox);
+        tma_load_2d(sV + i * vbox, &mapV, &vfull[i], cv.kb * 64, meta.roff[meta.slot_task[cv.s]]);
+        cv.next();
+        ++gv;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t id = idesc_bf16(128, qv, false, false);
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < meta.ntiles; w += gridDim.x) {
+        for (int s = meta.tile_slot_off[w]; s < meta.tile_slot_off[w + 1]; ++s, ++it) {
+          const int b = it & 1;
+          mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t acc = tmem + b * 256;
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const int ix = g % SP_NX, iv = g % SP_NV;
+            mbar_wait(&xfull[ix], (g / SP_NX) & 1);
+            mbar_wait(&vfull[iv], (g / SP_NV) & 1);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sX + ix * R_A_BYTES), b0 = smem_u32(sV + iv * vbox);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(acc, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), id,
+                       (kb | k) ? 1u : 0u);
+            mma_commit(&xempty[ix]);
+            mma_commit(&vempty[iv]);
+          }
+          mma_commit(&tfull[b]);
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue: plane p <- columns [p pq, p pq + pq)
+    const uint32_t q = warp - 4;
+    const int lrow = q * 32 + lane;
+    if (blockIdx.x == 0) {   // the all-zero slot (index nslots) used by the 2-CTA GEMM
+      float z[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) z[j] = 0.0f;
+      for (int pl = 0; pl < args.nplanes; ++pl)
+        store_slot_row(args.out + pl * args.plane_stride, meta.nslots, lrow, z, 0.0f, 0);
+    }
+    int it = 0;
+    for (int w = blockIdx.x; w < meta.ntiles; w += gridDim.x) {
+      const int row = w * kTileM + lrow;
+      const int my_task = row < meta.T ? row_task(meta, row) : -1;
+      for (int s = meta.tile_slot_off[w]; s < meta.tile_slot_off[w + 1]; ++s, ++it) {
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
+        const int ts = meta.slot_task[s];
+        const bool mine = ts == my_task;
+        float v[64];
+        for (int pl = 0; pl < args.nplanes; ++pl) {
+          const uint32_t ta = tmem + ((q * 32u) << 16) + b * 256 + pl * args.pq;
+          tmem_ld32(ta, *reinterpret_cast<float(*)[32]>(v));
+          if (args.pq > 32) tmem_ld32(ta + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+          else {
+#pragma unroll
+            for (int j = 32; j < 64; ++j) v[j] = 0.0f;
+          }
+          store_slot_row(args.out + pl * args.plane_stride, s, lrow, v, mine ? args.sc[ts] : 0.0f,
+                         mine ? args.rk[ts] : 0);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // B [out, rsum] -> Bt [rsum, out] (the backward projection's K-major operand)
 __global__ void k_transpose_b(const __nv_bfloat16* __restrict__ B, __nv_bfloat16* __restrict__ Bt,
                               int out, int rsum) {
@@ -1670,6 +1833,17 @@ void launch_shrink(const CUtensorMap& mapZ, const CUtensorMap& mapV, int K, cons
   if (init < smem) {
     cudaFuncSetAttribute(k_shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     init = kMaxSmem;
+  }
+  if (planes && !getenv("LOBRA_PLANES_SHARED_STAGES")) {   // separate X / adapter rings
+    const int psmem = SP_NX * R_A_BYTES + SP_NV * a.qv * 128 + 1024 + 256;
+    static bool pinit = false;
+    if (!pinit) {
+      cudaFuncSetAttribute(k_shrink_planes, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+      pinit = true;
+    }
+    const int pgrid = std::max(1, std::min(meta.ntiles, num_sms));
+    launch_k(k_shrink_planes, dim3(pgrid), dim3(256), psmem, st, mapZ, mapV, a);
+    return;
   }
   const int grid = std::max(1, std::min(a.per_slot ? meta.nslots : meta.ntiles, num_sms));
   launch_k(k_shrink, dim3(grid), dim3(256), smem, st, mapZ, mapV, a);
