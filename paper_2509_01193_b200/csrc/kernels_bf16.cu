@@ -7,11 +7,13 @@
 //              model can be fused into a batched operation whilst ... multiple LoRA
 //              adapters ... customized operations".
 // k_shrink   : the forward rank-r shrink H_s = s_t X A_t^T, HBM-bound: one CTA per slot (or
-//              per tile) over the whole K, deep TMA ring, the slots of a tile as one MMA;
-//              planes mode for wide projection groups.
+//              per tile) over the whole K, deep TMA ring, the slots of a tile as one MMA.
+// k_shrink_planes: the same for wide projection groups (every projection's H_s from one X
+//              pass, MMA N = np * qp), separate X / adapter rings.
 // k_rowproj  : the same with split-K over CTAs (small batches; the unfused backward G_s).
 // k_dypass   : the fused backward dY pass: G_s = s_t dY B_t partials and dB_t partials from
-//              ONE read of dY (static balanced schedule); k_gfin writes the G slots.
+//              ONE read of dY (static schedule weighted by the measured per-entry cost);
+//              k_gfin writes the G slots.
 // k_segred   : the token reductions dA_t = X^T G_s (and unfused dB_t = dY^T H_s) on tensor
 //              cores, Z tiles used as MN-major A operands (one HBM read of Z), static balanced
 //              schedule, deterministic two-pass (segment partials + k_finalize_multi).
