@@ -711,6 +711,8 @@ def main():
             for ci, cs in enumerate(copy_ss):
                 ready[b][ci].record(cs)
 
+        trace = os.environ.get("LOBRA_E2E_TRACE") == "1"   # per-item event timeline on stderr
+        tev = []
         if items:
             issue_copy(0)
         for k, (step_i, lens, tsk, last) in enumerate(items):
@@ -719,6 +721,10 @@ def main():
             b = k % 2
             for ev in ready[b]:
                 comp.wait_event(ev)
+            if trace:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(comp)
+                tev.append(("start", k, e))
             T = int(lens.sum())
             first_of_step = k == 0 or items[k - 1][0] != step_i
             if first_of_step and tp_size > 1:
@@ -734,9 +740,16 @@ def main():
                     layer.sync_adapter_grads(stream=comp)
                 host_grad.copy_(layer.flat_grad, non_blocking=True)
                 d2h += layer.flat_grad.numel() * 4
+            if trace:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(comp)
+                tev.append(("end", k, e))
         f1.record(comp)
         torch.cuda.synchronize()
         e_ms = f0.elapsed_time(f1)
+        if trace:
+            print(json.dumps({"e2e_trace_ms": [(w, k, round(f0.elapsed_time(e), 1)) for w, k, e in tev],
+                              "total_ms": round(e_ms, 1)}), file=sys.stderr)
         if world > 1:
             t = torch.tensor([e_ms], device="cpu" if gloo_test else dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -128,7 +128,7 @@ int64_t count_launch(int kind, cudaStream_t st, bool begin) {
 // ------------------------------------------------------------------ per-device context
 namespace {
 
-constexpr int kRing = 8;
+constexpr int kRing = 64;   // metadata uploads in flight before a slot is reused (a host wait)
 
 struct DevCtx {
   int dev = -1, num_sms = 0, cc_major = 0, cc_minor = 0;
@@ -178,6 +178,21 @@ lobra_status get_ctx(DevCtx** out) {
   return LOBRA_OK;
 }
 
+// The metadata reaches the device through a KERNEL that reads the pinned staging buffer over
+// PCIe (UVA: cudaMallocHost memory is mapped), not through cudaMemcpyAsync: a copy-engine
+// transfer queues behind whatever else the copy engines carry, so while a caller streams the
+// next micro-batch's activations host -> device (bench.py's e2e leg: 8.6 GB per C3 step) each
+// call's few-KB metadata copy waited for them and the compute serialised with the copies.
+__global__ void k_meta_copy(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int n4) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int n16 = n4 >> 2;   // 16-byte words, then the 4-byte tail
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  const int t = (n16 << 2) + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n4) dst[t] = src[t];
+}
+
 // Copies `bytes` of host data to device `dst` on `st` through a pinned staging ring.
 lobra_status upload(DevCtx* c, const void* src, size_t bytes, void* dst, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(c->mu);
@@ -192,8 +207,25 @@ lobra_status upload(DevCtx* c, const void* src, size_t bytes, void* dst, cudaStr
     c->pinned_bytes[k] = sz;
   }
   std::memcpy(c->pinned[k], src, bytes);
-  if (cudaMemcpyAsync(dst, c->pinned[k], bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && bytes % 4 == 0) {   // read over PCIe
+    const int n4 = (int)(bytes / 4);
+    const int grid = std::max(1, std::min(64, (n4 / 4 + 255) / 256));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_meta_copy, static_cast<const uint32_t*>(static_cast<const void*>(c->pinned[k])),
+                           static_cast<uint32_t*>(dst), n4) != cudaSuccess)
+      return fail(LOBRA_ERR_CUDA, "metadata copy kernel launch failed");
+    note_launch();
+  } else if (cudaMemcpyAsync(dst, c->pinned[k], bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
     return fail(LOBRA_ERR_CUDA, "cudaMemcpyAsync H2D failed");
+  }
   if (cudaEventRecord(c->ev[k], st) != cudaSuccess) return fail(LOBRA_ERR_CUDA, "event record");
   return LOBRA_OK;
 }
