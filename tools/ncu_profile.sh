@@ -8,7 +8,7 @@
 set -x
 TAG=${1:-r1}
 OUT=gpurun_out
-K="regex:k_(gemm|gemm2|rowproj|shrink|segred|finalize|finalize_multi|pad_cols|transpose_b|dypass|gfin|pack_a_group)"
+K="regex:k_(gemm|gemm2|rowproj|shrink|shrink_planes|segred|finalize|finalize_multi|pad_cols|transpose_b|dypass|gfin|pack_a_group|meta_copy)"
 B="python bench.py --steps 1 --warmup 1 --profile-only --no-cpu --no-e2e"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
     --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
