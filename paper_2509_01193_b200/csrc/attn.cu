@@ -809,27 +809,9 @@ extern "C" lobra_status lobra_attn_fwd(int32_t num_seqs, const int32_t* seq_lens
   if (ws_bytes < items.size() * sizeof(AttnItem)) return fail(LOBRA_ERR_INPUT, "attn: workspace too small");
   std::stable_sort(items.begin(), items.end(), [](const AttnItem& a, const AttnItem& b) { return a.q_tile > b.q_tile; });
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // metadata through a persistent pinned staging buffer (the previous copy from it is
-  // waited for before it is overwritten)
-  static void* pinned = nullptr;
-  static size_t pinned_bytes = 0;
-  static cudaEvent_t done = nullptr;
-  const size_t bytes = items.size() * sizeof(AttnItem);
-  if (!done && cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
-    return fail(LOBRA_ERR_CUDA, "attn: event creation failed");
-  cudaEventSynchronize(done);
-  if (pinned_bytes < bytes) {
-    if (pinned) cudaFreeHost(pinned);
-    pinned_bytes = std::max<size_t>(bytes, 1 << 16);
-    if (cudaMallocHost(&pinned, pinned_bytes) != cudaSuccess) {
-      pinned = nullptr, pinned_bytes = 0;
-      return fail(LOBRA_ERR_CUDA, "attn: pinned allocation failed");
-    }
-  }
-  memcpy(pinned, items.data(), bytes);
-  if (cudaMemcpyAsync(ws, pinned, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return fail(LOBRA_ERR_CUDA, "attn: metadata upload failed");
-  cudaEventRecord(done, st);
+  // metadata through the library's pinned staging ring (k_meta_copy: no copy-engine
+  // transfer, no host wait per call)
+  if (upload_host_meta(items.data(), items.size() * sizeof(AttnItem), ws, st) != LOBRA_OK) return LOBRA_ERR_CUDA;
   CUtensorMap mQ, mK, mV;
   lobra_status s;
   if ((s = make_tensor_map_2d(&mQ, Q, (uint64_t)n_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;
@@ -932,25 +914,8 @@ extern "C" lobra_status lobra_attn_bwd(int32_t num_seqs, const int32_t* seq_lens
                                                                  sizeof(AttnBwdItem)));
   float* Dq = reinterpret_cast<float*>(w + items_bytes);
   float* acc = reinterpret_cast<float*>(w + items_bytes + align256((size_t)T * n_heads * sizeof(float)));
-  static void* pinned = nullptr;
-  static size_t pinned_bytes = 0;
-  static cudaEvent_t done = nullptr;
-  const size_t bytes = items.size() * sizeof(AttnBwdItem);
-  if (!done && cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
-    return fail(LOBRA_ERR_CUDA, "attn_bwd: event creation failed");
-  cudaEventSynchronize(done);
-  if (pinned_bytes < bytes) {
-    if (pinned) cudaFreeHost(pinned);
-    pinned_bytes = std::max<size_t>(bytes, 1 << 16);
-    if (cudaMallocHost(&pinned, pinned_bytes) != cudaSuccess) {
-      pinned = nullptr, pinned_bytes = 0;
-      return fail(LOBRA_ERR_CUDA, "attn_bwd: pinned allocation failed");
-    }
-  }
-  memcpy(pinned, items.data(), bytes);
-  if (cudaMemcpyAsync(ws, pinned, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return fail(LOBRA_ERR_CUDA, "attn_bwd: metadata upload failed");
-  cudaEventRecord(done, st);
+  if (upload_host_meta(items.data(), items.size() * sizeof(AttnBwdItem), ws, st) != LOBRA_OK)
+    return LOBRA_ERR_CUDA;
   CUtensorMap mQ, mK, mV, mdO;
   lobra_status s;
   if ((s = make_tensor_map_2d(&mQ, Q, (uint64_t)n_heads * 128, (uint64_t)T, 64, 128)) != LOBRA_OK) return s;

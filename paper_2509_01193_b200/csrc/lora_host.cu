@@ -207,7 +207,8 @@ lobra_status upload(DevCtx* c, const void* src, size_t bytes, void* dst, cudaStr
     c->pinned_bytes[k] = sz;
   }
   std::memcpy(c->pinned[k], src, bytes);
-  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && bytes % 4 == 0) {   // read over PCIe
+  static const bool memcpy_path = getenv("LOBRA_META_MEMCPY") != nullptr;   // A/B switch
+  if (!memcpy_path && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && bytes % 4 == 0) {   // read over PCIe
     const int n4 = (int)(bytes / 4);
     const int grid = std::max(1, std::min(64, (n4 / 4 + 255) / 256));
     cudaLaunchConfig_t cfg = {};
@@ -748,6 +749,12 @@ using namespace lobra;
 namespace lobra {
 // TMA map for other translation units (attn.cu): bf16 2D [outer, inner] row-major, 128-byte
 // swizzle; initialises the driver entry point on first use.
+lobra_status upload_host_meta(const void* src, size_t bytes, void* dst, cudaStream_t st) {
+  DevCtx* ctx = nullptr;
+  lobra_status s = get_ctx(&ctx);
+  if (s != LOBRA_OK) return s;
+  return upload(ctx, src, bytes, dst, st);
+}
 lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
                                 uint32_t box_inner, uint32_t box_outer) {
   DevCtx* ctx = nullptr;

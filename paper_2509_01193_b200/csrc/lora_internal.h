@@ -129,6 +129,9 @@ void launch_transpose_b(const __nv_bfloat16* B, __nv_bfloat16* Bt, int out, int 
 // bf16 2D TMA map, 128-byte swizzle (lora_host.cu)
 lobra_status make_tensor_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
                                 uint32_t box_inner, uint32_t box_outer);
+// host metadata -> device (`bytes` % 4 == 0, dst 16-byte aligned) through the library's
+// pinned staging ring and k_meta_copy, in stream order on st (lora_host.cu)
+lobra_status upload_host_meta(const void* src, size_t bytes, void* dst, cudaStream_t st);
 // Fused GEMM -> TP reduce-scatter (symm.cu): output row r is stored into rank
 // (r / chunk_rows)'s symmetric buffer, slot `rank`, row r % chunk_rows (bf16 [chunk_rows, N]
 // per slot) instead of C (with accumulate, the row of C is added first: C holds the local
