@@ -64,7 +64,16 @@ __global__ void k_symm_barrier(uint8_t* const* __restrict__ peer, int rank, int 
     st_release_sys(reinterpret_cast<uint64_t*>(peer[t]) + kind * kMaxRanks + rank, epoch);
   if (t < world && t != rank) {
     const uint64_t* f = reinterpret_cast<const uint64_t*>(peer[rank]) + kind * kMaxRanks + t;
-    while (ld_acquire_sys(f) < epoch) {
+    // a peer that never arrives (a crashed rank, a broken mapping) must not hang the GPU:
+    // after 30 s the kernel traps and the error surfaces at the caller's next sync
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    for (uint32_t spin = 0; ld_acquire_sys(f) < epoch; ++spin) {
+      if ((spin & 0xFFFF) == 0xFFFF) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 30000000000ull) __trap();
+      }
     }
   }
   __syncthreads();
