@@ -345,6 +345,9 @@ typedef struct {
  * node_cap: branch-and-bound node budget for >= 3 groups (<= 0: default 1e6 nodes, ~5-10 s);
  * when it is exhausted the call returns LOBRA_ERR_BUDGET with the LENGTH-BASED d (mode 1's)
  * in `out` -- never a silent substitute: the status says the Eq. 3 optimum was not reached.
+ * With >= 3 deployed groups the branch-and-bound subtrees run on a thread pool created for
+ * the call (LOBRA_DISPATCH_THREADS, default hardware threads - 1, at most 16); the result
+ * does not depend on the thread count.
  * Errors: LOBRA_ERR_INPUT, LOBRA_ERR_INFEASIBLE, LOBRA_ERR_BUDGET.  Host only; thread-safe
  * (no global state). */
 LOBRA_API lobra_status lobra_dispatch(const lobra_deployment* dep, const lobra_batch* batch,
