@@ -65,14 +65,15 @@ __global__ void k_symm_barrier(uint8_t* const* __restrict__ peer, int rank, int 
   if (t < world && t != rank) {
     const uint64_t* f = reinterpret_cast<const uint64_t*>(peer[rank]) + kind * kMaxRanks + t;
     // a peer that never arrives (a crashed rank, a broken mapping) must not hang the GPU:
-    // after 30 s the kernel traps and the error surfaces at the caller's next sync
+    // after 300 s (far beyond any start-up skew between ranks) the kernel traps and the
+    // error surfaces at the caller's next sync
     uint64_t t0;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
     for (uint32_t spin = 0; ld_acquire_sys(f) < epoch; ++spin) {
       if ((spin & 0xFFFF) == 0xFFFF) {
         uint64_t t1;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 30000000000ull) __trap();
+        if (t1 - t0 > 300000000000ull) __trap();
       }
     }
   }
