@@ -400,7 +400,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
   // 7 for a task of rank > 32 (wider B_t / H boxes, G and dB partials).  Least-squares fit of
   // per-CTA times against each CTA's entries (LOBRA_TRACE_DY, tools/trace_dy.py, C3): full
   // entries 3.0 us, rank > 32 3.65, the 256-column last chunk of width 11008 2.0 / 2.7, plus
-  // 1.5 per segment.  With equal entry counts per CTA the CTA times spread 179-343 us
+  // 1.5 per segment (each (task, chunk) run is charged one).  With equal entry counts per CTA the CTA times spread 179-343 us
   // (11008) and 89-123 us (4096).
   auto build_dy = [&](int width, int chunk_cols, bool weighted) {
     DyVecs v;
@@ -411,11 +411,13 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
       const int nb = std::max(0, std::min(chunk_cols / 128, n128 - c * (chunk_cols / 128)));
       return 5LL * nb + 10 + (ad->ranks[t] > 32 ? 7 : 0);
     };
+    // each (task, chunk) run also costs one segment (a dB drain: ~1.5 us, weight 15)
+    const long long seg_w = weighted ? 15 : 0;
     long long W = 0, nent = 0;
     for (int t = 0; t < G; ++t)
       for (int c = 0; c < nch; ++c) {
         const long long n_t = task_slot_off[t + 1] - task_slot_off[t];
-        W += n_t * weight(t, c);
+        W += n_t * weight(t, c) + (n_t ? seg_w : 0);
         nent += n_t;
       }
     const int ncta = (int)std::max<long long>(1, std::min<long long>(std::max(num_sms, 1), nent));
@@ -427,6 +429,7 @@ void build_plan(const lobra_batch* b, const lobra_adapters* ad, int width_hint, 
       const int k0 = task_slot_off[t], k1 = task_slot_off[t + 1];
       for (int c = 0; c < nch; ++c) {
         const long long w = std::max<long long>(1, weight(t, c));
+        if (k1 > k0) e += seg_w;
         int k = k0;
         while (k < k1) {
           while (cta < ncta - 1 && e >= cta_end(cta)) {
