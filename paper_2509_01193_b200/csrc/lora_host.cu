@@ -1073,11 +1073,6 @@ int64_t max_out(const lobra_group_problem* g) {
   for (int p = 0; p < g->num_proj; ++p) m = std::max<int64_t>(m, g->out[p]);
   return m;
 }
-int64_t min_out(const lobra_group_problem* g) {
-  int64_t m = g->out[0];
-  for (int p = 0; p < g->num_proj; ++p) m = std::min<int64_t>(m, g->out[p]);
-  return m;
-}
 
 // Banded path applies: bf16, the bands fit the 64-wide slot, default backward kernels.
 bool group_fused(const lobra_group_problem* g, const lobra_group_adapters* ga) {
