@@ -55,6 +55,9 @@ def main(tag):
         lines.append(f"| {i} | {x['k']} | {x['gpu__time_duration.sum'] / 1000.0:.1f} |")
     open(os.path.join(prof, f"{tag}_launches_summary.md"), "w").write("\n".join(lines) + "\n")
 
+    if not os.path.exists(os.path.join(out, f"gemm_traffic_{tag}.csv")):   # launch list only
+        print(open(os.path.join(prof, f"{tag}_launches_summary.md")).read()[:2500])
+        return
     G = records(os.path.join(out, f"gemm_traffic_{tag}.csv"))
     shutil.copy(os.path.join(out, f"gemm_traffic_{tag}.csv"), os.path.join(prof, f"{tag}_gemm_traffic.csv"))
     fwd = [x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in G if "k_gemm2<0>" in x["k"]]
