@@ -106,7 +106,10 @@ def _worker(rank, world, port, host_staging, q):
         order = schedule_1f1b(world, rank, len(MICRO))
         assert all(l.log == order for l in layers), (layers[0].log, order)
         assert all(not l.saved for l in layers)
-        q.put((rank, {"outs": outs, "dxs": dxs, "grads": [l.grad for l in layers]}))
+        # plain arrays through the queue (bf16 -> fp32 is exact): torch tensors would travel
+        # as shared-memory handles that die with this process
+        npy = lambda d: {k: v.float().numpy() for k, v in d.items()}
+        q.put((rank, {"outs": npy(outs), "dxs": npy(dxs), "grads": [l.grad.numpy() for l in layers]}))
         dist.barrier()
         dist.destroy_process_group()
     except Exception:  # pragma: no cover - reported to the parent
@@ -133,8 +136,9 @@ def test_pipeline_1f1b_gloo_world3(host_staging):
     assert sorted(last["outs"]) == list(range(len(MICRO))) and not res[1]["outs"]
     assert sorted(first["dxs"]) == list(range(len(MICRO))) and not res[1]["dxs"]
     for k in range(len(MICRO)):
-        assert torch.equal(last["outs"][k], ref_outs[k])
-        assert torch.equal(first["dxs"][k], ref_dxs[k])
+        assert torch.equal(torch.from_numpy(last["outs"][k]), ref_outs[k].float())
+        assert torch.equal(torch.from_numpy(first["dxs"][k]), ref_dxs[k].float())
     got = [g for r in range(world) for g in res[r]["grads"]]
+    assert len(got) == len(ref_grads)
     for a, b in zip(got, ref_grads):
-        assert torch.equal(a, b)
+        assert torch.equal(torch.from_numpy(a), b)
