@@ -66,7 +66,11 @@ def main(tag):
           "source": f"profiles/{tag}_gemm_traffic.csv (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
                     f"{len(fwd) + len(bwd)} GEMM launches of one bench step)",
           "per_launch_fwd": fwd, "per_launch_bwd": bwd}
-    json.dump(tj, open(os.path.join(prof, "traffic.json"), "w"), indent=1)
+    # bench.py looks the entry up by workload (the default bench step is C3)
+    path = os.path.join(prof, "traffic.json")
+    allw = json.load(open(path)) if os.path.exists(path) else {}
+    allw[os.environ.get("LOBRA_TRAFFIC_WORKLOAD", "c3")] = tj
+    json.dump(allw, open(path, "w"), indent=1)
     print(open(os.path.join(prof, f"{tag}_launches_summary.md")).read()[:2500])
     print(json.dumps({k: v for k, v in tj.items() if not k.startswith("per")}))
 
