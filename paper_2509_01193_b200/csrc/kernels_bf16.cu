@@ -1493,6 +1493,8 @@ __global__ void __launch_bounds__(256, 1)
 // One thread per (slot row, 8 output columns of this projection's band): float4 loads of the
 // chunk partials, summed in chunk order, scaled, masked, one 16-byte store at column
 // band + 8 g (a projection group's other bands are left untouched).
+constexpr int GF_BATCH = 8;
+constexpr int GF_CTAS_PER_SM = 4;   // chunk partials loaded per batch (independent loads in flight)
 __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Meta meta,
                        __nv_bfloat16* __restrict__ out) {
   pdl_wait();
@@ -1513,16 +1515,16 @@ __global__ void k_gfin(const float* __restrict__ gpart, int nchunks, int qp, Met
       // row's task is looked up; rows of other tasks are masked afterwards
       const float* src = gpart + ((size_t)s * nchunks * kTileM + lrow) * qp + g * 8;
       const size_t cstride = (size_t)kTileM * qp;
-      for (int c = 0; c < nchunks; c += 4) {
-        float4 a[4], b[4];
+      for (int c = 0; c < nchunks; c += GF_BATCH) {
+        float4 a[GF_BATCH], b[GF_BATCH];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < GF_BATCH; ++j) {
           const bool ok = c + j < nchunks;
           a[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + (c + j) * cstride)) : make_float4(0, 0, 0, 0);
           b[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + (c + j) * cstride) + 1) : make_float4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {   // chunk order, as before
+        for (int j = 0; j < GF_BATCH; ++j) {   // chunk order, as before
           if (c + j >= nchunks) break;
           v[0] += a[j].x; v[1] += a[j].y; v[2] += a[j].z; v[3] += a[j].w;
           v[4] += b[j].x; v[5] += b[j].y; v[6] += b[j].z; v[7] += b[j].w;
@@ -1999,7 +2001,7 @@ void launch_dypass(const CUtensorMap& mapDY, const CUtensorMap& mapH, const CUte
       fclose(f);
     }
   }
-  launch_k(k_gfin, dim3(num_sms * 2), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
+  launch_k(k_gfin, dim3(num_sms * GF_CTAS_PER_SM), dim3(256), 0, st, (const float*)gpart, a.nchunks, qp, meta, gslots);
 }
 
 // Tile order of the 2-CTA GEMM per shape class (pair_tile).  Measured defaults
