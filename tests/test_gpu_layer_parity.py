@@ -163,6 +163,19 @@ def test_c3_qkv_gate_up_vs_oracle():
     _check(layer, runs, ranks, scales, sub_rows=8192)
 
 
+def test_c3_o_down_vs_oracle():
+    """C3 (BASELINE configs[2]): the single-call projections, o (4096 -> 4096) and down
+    (11008 -> 4096, the K = 11008 GEMMs and the widest X of the dA reduction), 16 tasks with
+    ranks 8..64, T = 65536 with sequences up to 16K -- with the group test above, every
+    projection bench.py times on C3 is compared with the oracle at full size."""
+    from paper_2509_01193_b200.layer import LLAMA2_7B
+    tasks = synth.c3_tasks()
+    ranks, scales = [t.rank for t in tasks], [t.scale for t in tasks]
+    shapes = [s for s in LLAMA2_7B if s[0] in ("o", "down")]
+    layer, runs = _run(shapes, ranks, scales, [synth.config_c3(seed=4)], seed=34)
+    _check(layer, runs, ranks, scales, sub_rows=8192)
+
+
 def test_launch_counter_matches_cupti():
     """lobra_launch_count (the bench's `gpu_launches`) counts every kernel the library
     enqueues -- the dY pass's G finalize included -- as CUPTI sees them."""
